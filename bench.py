@@ -1,0 +1,433 @@
+#!/usr/bin/env python3
+"""Throughput bench of the B200 Hi-DFT (BASELINE.json metric: support-DFT
+coeffs/s = B*k/s, and the fraction of the HBM-gather roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+
+A step is one pass of the hot path -- hidft(f_b, J, pivots(J)) +
+hidft_to_dft for every signal of the batch -- over one batch of synthetic
+signals resident in HBM.  The default workload is BASELINE config 2
+(N=2^20, k=1024, B=1024 signals per GPU sharing one support, complex64).
+Under torchrun each rank owns its own B-signal batch (weak scaling, no
+data-path collective); the timed region is bracketed by a barrier and a
+device synchronise and the max over ranks is reported.
+
+L2: the gather footprint of one batch (~32-40 MiB) fits in the 126 MB L2,
+so the timed steps rotate over R input sets whose combined footprint is
+several times L2 (each set is the same signals at different addresses).
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy port in oracle/, pinned to the reference by golden vectors) on the
+host cores with a process pool, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "support-DFT coeffs/s (B·k/s)"
+UNIT = "coeffs/s"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ------------------------------------------------------------- clocks ---
+
+class ClockSampler:
+    """nvidia-smi SM clock / throttle sampling in the background."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------- roofline bytes ---
+
+def gather_bytes(pattern: np.ndarray, esz: int) -> tuple[int, int]:
+    """(sector bytes, element bytes) of one signal's gather at a 32B-aligned base."""
+    sectors = np.unique((pattern * esz) // 32).size
+    return 32 * sectors, pattern.size * esz
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------ b200 arm ---
+
+def run_b200(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_15299_b200 as S
+    from paper_2211_15299_b200 import workloads as W
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = args.config
+    spec = W.CONFIGS[cfg]
+    B = args.batch or spec["B"]
+    wl = W.make_workload(cfg, B, b0=rank * B)
+    cdt = torch.complex64 if wl.dtype == "complex64" else torch.complex128
+    esz = 8 if cdt == torch.complex64 else 16
+    N = wl.N
+
+    # rotation sets so that the timed steps read cold HBM, not L2
+    L2 = 126 * 2 ** 20
+    pattern_bytes = None
+    per_sig_sector = []
+    if wl.support.ndim == 1:
+        piv = S.pivots(S.SupportSet(N, wl.support))
+        pat = S.pivoted_pattern(piv, wl.M).as_array()
+        gb, ub = gather_bytes(pat, esz)
+        per_sig_sector = [gb] * B
+        pattern_bytes = (gb, ub)
+    else:
+        ub_sum = 0
+        for b in range(B):
+            pat = W.pattern_of(W.config_pivots(cfg, rank * B + b), wl.M)
+            gb, ub = gather_bytes(pat, esz)
+            per_sig_sector.append(gb)
+            ub_sum += ub
+        pattern_bytes = (None, ub_sum / B)
+    footprint = sum(per_sig_sector)
+    R = max(2, math.ceil(4 * L2 / max(footprint, 1)))
+    R = min(R, args.max_sets)
+    sig_bytes = B * N * esz
+    free = torch.cuda.mem_get_info(dev)[0]
+    R = max(1, min(R, int((free * 0.85) // sig_bytes)))
+    sets = [torch.empty((B, N), dtype=cdt, device=dev) for _ in range(R)]
+    W.synthesize_into(sets[0], wl.support, wl.coeffs)
+    for s in sets[1:]:
+        s.copy_(sets[0])
+    if wl.support.ndim == 1:
+        J = S.SupportSet(N, wl.support)
+    else:
+        J = torch.from_numpy(wl.support).to(dev)
+    out = torch.empty((B, wl.k), dtype=cdt, device=dev)
+    status = torch.zeros(wl.support.shape[0] if wl.support.ndim == 2 else 1, dtype=torch.int32, device=dev)
+
+    def step(i):
+        S.hidft_to_dft_batched(sets[i % R], J, out=out, status=status, check=False)
+
+    # correctness gate on the measured configuration: planted spectrum recovered
+    step(0)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    err = float(np.max(np.linalg.norm(got - wl.coeffs, axis=1) / np.linalg.norm(wl.coeffs, axis=1)))
+    tol = 1e-5 if esz == 8 else 1e-11
+    worst = int(status.max().item())
+    if not (err < tol) or worst != 0:
+        raise SystemExit(f"bench parity gate failed: rel L2 {err:.3e} status {worst}")
+
+    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    sampler = ClockSampler(vis[local] if local < len(vis) else local)
+    sampler.start()
+    # ~1 s soak so that clock samples exist under load, then W warm-up steps
+    t_end = time.time() + args.soak
+    i = 0
+    while time.time() < t_end:
+        for _ in range(64):
+            step(i)
+            i += 1
+        torch.cuda.synchronize()
+    for w in range(args.warmup):
+        step(w)
+    stream = torch.cuda.current_stream(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for t in range(args.steps):
+        step(t)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    clocks = sampler.stop()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    ms_per_step = ms / args.steps
+    coeffs_per_step = B * wl.k * world
+    value = coeffs_per_step / (ms_per_step / 1e3)
+
+    # roofline of the one kernel a step launches
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
+    # gather sectors + coefficient writes + support reads (shared: once; per-signal: B*k int64)
+    G = footprint + B * wl.k * esz + wl.support.size * 8
+    achieved = G / (ms_per_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": int(G),
+            "element_bytes_per_launch": int(B * (pattern_bytes[1] if pattern_bytes else 0) + B * wl.k * esz)}
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                tr = json.load(fh).get(f"cfg{cfg}")
+            if tr:
+                roof["traffic"] = tr
+        except (OSError, ValueError):
+            pass
+
+    # end to end through the public API with host buffers (rank-local)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, S, torch, sets[0], J, wl, esz, dev)
+        if world > 1:
+            t = torch.tensor([e2e["seconds_per_step"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["value"] = coeffs_per_step / float(t.item())
+        del e2e["seconds_per_step"]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = run_cpu_reference(cfg, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (f32)" if esz == 8 else "c128 (f64)",
+            "data": "synthetic: seeded supports (reference generators) and complex-Gaussian spectra, "
+                    "signals = inverse DFT synthesised on device",
+            "config": {"workload": f"config {cfg}: N=2^{wl.M}, k={wl.k}, B={B} per GPU, {wl.dtype}, "
+                                   + ("shared support" if wl.support.ndim == 1 else "per-signal supports"),
+                       "global_batch": B * world, "N": N, "k": wl.k, "parallelism": f"batch shard x{world}",
+                       "l2": f"rotating {R} input sets, gather footprint {R * footprint / 2**20:.0f} MiB "
+                             f"vs 126 MB L2"},
+            "gpu_launches": args.steps,
+            "roofline": roof,
+            "clocks": clocks,
+            "parity": {"rel_l2_vs_planted_max": err, "tol": tol},
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
+    """Public API, host buffers: signals in page-locked host memory (zero-copy
+    gather of the 2^s needed samples per signal over PCIe), coefficients
+    returned to host memory; every step synchronises."""
+    host = torch.empty(dev_signals.shape, dtype=dev_signals.dtype, pin_memory=True)
+    host.copy_(dev_signals)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        S.hidft_to_dft_batched(host, J)
+    steps = max(3, min(args.steps, args.e2e_steps))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = S.hidft_to_dft_batched(host, J)
+    dt = (time.perf_counter() - t0) / steps
+    B = dev_signals.shape[0]
+    A = wl.k if wl.support.ndim == 1 else wl.support.shape[1]
+    del host
+    return {"value": B * wl.k / dt, "unit": UNIT, "h2d_bytes_per_step": int(B * A * esz),
+            "d2h_bytes_per_step": int(res.numel() * esz), "seconds_per_step": dt,
+            "path": "hidft_to_dft_batched(pinned host tensor) -> zero-copy gather, D2H result"}
+
+
+# ------------------------------------------------------- CPU reference ---
+
+def _cpu_worker(args):
+    cfg, rows, barrier_path, deadline = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import structfft_oracle as O
+    from paper_2211_15299_b200 import workloads as W
+    spec = W.CONFIGS[cfg]
+    dt = np.complex64 if spec["dtype"] == "complex64" else np.complex128
+    sigs = []
+    for b in rows:
+        J, M = W.config_support(cfg, b)
+        coef = W.coefficients(cfg, b, J.size)
+        sigs.append((J, M, O.synthesize(J, coef, M).astype(dt)))
+    fn = O.reference_sas_call if cfg == 3 else O.reference_call
+    t0 = time.perf_counter()
+    done = 0
+    for J, M, f in sigs:
+        fn(f, J, M)
+        done += 1
+        if time.perf_counter() - t0 > deadline:
+            break
+    return done, sum(s[0].size for s in sigs[:done]), time.perf_counter() - t0
+
+
+def run_cpu_reference(cfg: int, seconds: float) -> dict:
+    """The reference algorithm (oracle port) on all host cores, bounded sample."""
+    import multiprocessing as mp
+    P = os.cpu_count() or 1
+    # per-signal cost probe, then size the sample for ~`seconds` of wall time
+    probe = _cpu_worker((cfg, [0], None, 1e9))
+    per_sig = max(probe[2], 1e-4)
+    n_per = max(1, min(16, int(seconds / per_sig)))
+    from paper_2211_15299_b200 import workloads as W
+    Bmax = W.CONFIGS[cfg]["B"]
+    total = min(Bmax, n_per * P) if cfg != 5 else min(Bmax, 2 * P)
+    rows = list(range(total))
+    chunks = [rows[i::P] for i in range(P) if rows[i::P]]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(len(chunks)) as pool:
+        res = pool.map(_cpu_worker, [(cfg, c, None, 2 * seconds) for c in chunks])
+    wall = time.perf_counter() - t0
+    # workers synthesise before timing; report the slowest worker's timed span
+    span = max(r[2] for r in res)
+    coeffs = sum(r[1] for r in res)
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"value": coeffs / span, "unit": UNIT, "cores": len(chunks), "kind": "port",
+            "sample": f"{sum(r[0] for r in res)} signals of config {cfg} (oracle port of hidft+hidft_to_dft"
+                      f"{' / sas_transform' if cfg == 3 else ''}, dense host arrays, per-call plan), "
+                      f"{len(chunks)} worker processes on {model or 'host CPU'}; wall incl. synthesis {wall:.1f}s"}
+
+
+def run_reference(args) -> None:
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    world = env_int("WORLD_SIZE", 1)
+    cfg = args.config
+    from paper_2211_15299_b200 import workloads as W
+    vals = []
+    cpu = None
+    for _ in range(args.warmup + args.steps):
+        cpu = run_cpu_reference(cfg, args.cpu_seconds / 3)
+        vals.append(cpu["value"])
+    timed = vals[args.warmup:]
+    value = statistics.median(timed)
+    spec = W.CONFIGS[cfg]
+    k = 4096 if cfg == 3 else (1 << spec["p"])
+    B = spec["B"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": B * k / value * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c64 input, f64 compute (reference upcasts)" if spec["dtype"] == "complex64" else "c128 (f64)",
+            "data": "synthetic, same seeds as the b200 arm",
+            "config": {"workload": f"config {cfg}: N=2^{spec['M']}, k={k}, B={B}", "global_batch": B,
+                       "parallelism": "host process pool"},
+            "cpu_baseline": {**cpu, "value": value},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6])
+    ap.add_argument("--batch", type=int, default=0, help="signals per GPU (default: config's B)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--max-sets", type=int, default=8)
+    ap.add_argument("--soak", type=float, default=1.0)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

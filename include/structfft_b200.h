@@ -1,0 +1,154 @@
+/*
+ * structfft_b200.h -- C-ABI of the B200-native Hi-DFT (arXiv 2211.15299).
+ *
+ * Plain C: pointers, sizes, status codes, an opaque plan handle and a raw
+ * cudaStream_t.  No torch types.  Every entry point replaces one function of
+ * the reference Python package `structfft` (paths relative to
+ * /root/reference/pkg/src/structfft); INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions (core.py:3-6): forward kernel e^{-2 pi i m n / N}; a shift a
+ * reads the samples at (I - a) mod N; hidft output is the UNSCALED product
+ * F(J, I) f_I; the DFT epilogue multiplies by N/|J| (hidft.py:188-207).
+ *
+ * Status codes mirror the reference exception classes and the CLI exit codes
+ * (errors.py:4-17, cli.py:366-378): 0 ok, 2 InvalidInputError,
+ * 3 ContractViolationError, 4 BudgetExceededError.  5 = CUDA runtime error,
+ * 6 = size outside the device path.  The message of the last
+ * failing call on the calling thread is available from sfft_last_error().
+ *
+ * Pointers: support indices J may be host or device memory (detected with
+ * cudaPointerGetAttributes).  Signals may be device memory or page-locked
+ * host memory mapped into the device address space (zero-copy gather).
+ * Outputs are device (or mapped host) memory owned by the caller.
+ * All calls are stream-ordered on `stream` and deterministic (no atomics in
+ * the arithmetic).
+ */
+#ifndef STRUCTFFT_B200_H
+#define STRUCTFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SFFT_API __attribute__((visibility("default")))
+#else
+#define SFFT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sfft_stream_t; /* == cudaStream_t */
+
+enum sfft_status {
+  SFFT_OK = 0,
+  SFFT_ERR_INVALID = 2,    /* errors.py:8  InvalidInputError       */
+  SFFT_ERR_CONTRACT = 3,   /* errors.py:12 ContractViolationError  */
+  SFFT_ERR_BUDGET = 4,     /* errors.py:16 BudgetExceededError     */
+  SFFT_ERR_CUDA = 5,
+  SFFT_ERR_UNSUPPORTED = 6
+};
+
+enum sfft_dtype { SFFT_C64 = 0, SFFT_C128 = 1 };
+
+/* what the transform writes per signal row */
+enum sfft_out_kind {
+  SFFT_OUT_NODES = 0, /* HiDftResult.node_values, ascending node residue (hidft.py:168-178) */
+  SFFT_OUT_DFT = 1,   /* hidft_to_dft: ascending-J order x N/|J| (hidft.py:188-207)          */
+  SFFT_OUT_SAS = 2,   /* sas_transform mu*=1: ascending-J order x N/|I| (sas.py:358-371)     */
+  SFFT_OUT_SLOTS = 3  /* HiDftResult.slot_values, slot order (hidft.py:180)                   */
+};
+
+SFFT_API const char* sfft_version(void);
+SFFT_API const char* sfft_last_error(void);
+/* 1 if the library was compiled for and can run on the current device */
+SFFT_API int sfft_device_ok(void);
+
+/* pivots(J) -> bit mask of pivot levels, and classify(J) homogeneity.
+ * Replaces congruence.py:76-101 (pivots) and congruence.py:235-241 (classify).
+ * J: k strictly increasing indices in [0, 2^M), 1 <= M <= 31. */
+SFFT_API int sfft_analyze(const int64_t* J, int64_t k, int M, uint64_t* pivot_mask,
+                 int* homogeneous, sfft_stream_t stream);
+
+/* pivoted_pattern(r, M).samples (sampling.py:62-71): the 2^n_r elements of
+ * I_r in ascending order, written to `out` (host or device int64). */
+SFFT_API int sfft_pivoted_pattern(const int32_t* r, int n_r, int M, int64_t* out,
+                         sfft_stream_t stream);
+
+typedef struct sfft_plan sfft_plan;
+
+typedef struct sfft_plan_info {
+  int M;               /* log2 N                                   */
+  int dtype;           /* SFFT_C64 / SFFT_C128                     */
+  int n_r;             /* len(r)                                   */
+  int height;          /* n                                        */
+  int s;               /* pivots merged by the butterfly           */
+  int level;           /* output nodes live at this tree level     */
+  int homogeneous;     /* classify(J).is_homogeneous               */
+  int reserved;
+  int64_t k;           /* |J|                                      */
+  int64_t A;           /* 2^s slots = |I|                          */
+  int64_t n_nodes;     /* real slots = nodes at `level`            */
+  int64_t mu_star;     /* max node weight at `level` (sas.py:73-76)*/
+  uint64_t pivot_mask; /* pivots(J)                                */
+  int32_t used[32];    /* r[:n_r-height]                           */
+} sfft_plan_info;
+
+/* ButterflyPlan for (J, r, height): the checks of hidft.py:149-153
+ * (validate_pivot_vector, assert_part_homogeneous, height range) and the
+ * tables of _build_plan (hidft.py:69-95), built on the device.  Contract
+ * failures return SFFT_ERR_CONTRACT with the offending pivot in the message. */
+SFFT_API int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_t* r, int n_r,
+                     int height, int dtype, sfft_stream_t stream, sfft_plan** plan);
+SFFT_API int sfft_plan_destroy(sfft_plan* plan);
+SFFT_API int sfft_plan_get_info(const sfft_plan* plan, sfft_plan_info* info);
+
+/* Copy plan tables (bit-exact with _build_plan) to caller buffers, host or
+ * device; any pointer may be NULL.  twiddles: A-1 complex of the plan dtype,
+ * stage-major (stage k at offset 2^(k-1)-1).  offsets: slot order
+ * (hidft.py:155-158).  Synchronises `stream`. */
+SFFT_API int sfft_plan_tables(const sfft_plan* plan, int64_t* element_slots, int64_t* slot_residues,
+                     uint8_t* slot_real, int64_t* node_residues, int64_t* offsets,
+                     void* twiddles, sfft_stream_t stream);
+
+/* hidft(f_b, J, r, height, shift) for B signal rows (hidft.py:135-185),
+ * batched.  signals: B rows of N complex (plan dtype), row stride `ld`
+ * elements.  out: B rows of n_out complex (n_out = n_nodes for NODES, k for
+ * DFT/SAS, A for SLOTS), row stride ld_out.  slot_out: optional second output
+ * of slot values (A per row, stride ld_slot) or NULL.
+ * DFT requires a homogeneous J at height 0; SAS requires mu* = 1. */
+SFFT_API int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld,
+               int64_t shift, int out_kind, void* out, int64_t ld_out, void* slot_out,
+               int64_t ld_slot, sfft_stream_t stream);
+
+/* Same transform on samples already gathered in slot order (B rows of A
+ * complex, row stride ld >= A): the path for callable / synthesised sources
+ * (hidft.py:41-45, where the caller evaluates the signal at the offsets). */
+SFFT_API int sfft_hidft_gathered(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld,
+                                 int out_kind, void* out, int64_t ld_out, void* slot_out,
+                                 int64_t ld_slot, sfft_stream_t stream);
+
+/* Reorder/scale slot values (B rows, stride ld >= A) into an output kind:
+ * hidft_to_dft(res) (hidft.py:188-207) or the mu*=1 SAS read (sas.py:363-371)
+ * or node order. */
+SFFT_API int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const void* slot_values,
+                                 int64_t B, int64_t ld, void* out, int64_t ld_out,
+                                 sfft_stream_t stream);
+
+/* Fused hidft(f_b, J_b, pivots(J_b)) + hidft_to_dft for homogeneous supports:
+ * pivots, pattern, tables and twiddles are derived on chip per CTA, so one
+ * launch does plan + gather + butterfly + scaled, ascending-J store.
+ * J: n_supports rows of k indices (n_supports = 1: shared by all B signals;
+ * n_supports = B: one support per signal, config 4), int64, device or host.
+ * status: optional device int32[n_supports] receiving 0 / 2 / 3 per support;
+ * when NULL the call synchronises and returns the worst status. */
+SFFT_API int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_supports, int M,
+                            const void* signals, int64_t B, int64_t ld, int dtype,
+                            void* out, int64_t ld_out, int32_t* status,
+                            sfft_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STRUCTFFT_B200_H */

@@ -1,0 +1,20 @@
+"""structfft on B200: the Hi-DFT hot path of arXiv 2211.15299 as sm_100a CUDA.
+
+Drop-in names for the reference package's hot path (reference
+__init__.py:10-92): SupportSet, pivots, classify, is_part_homogeneous,
+pivoted_pattern, hidft, hidft_to_dft, sas_transform (mu* = 1), plus the
+batched fused entry `hidft_to_dft_batched`.  All compute runs through the
+C-ABI library libsfft_b200.so (include/structfft_b200.h); there is no CPU
+fallback.
+"""
+
+from .congruence import (Classification, SupportSet, as_support, assert_part_homogeneous, classify,
+                         height_of, is_part_homogeneous, pivots, v2, validate_pivot_vector)
+from .counting import OpCounter
+from .errors import (BudgetExceededError, ContractViolationError, DeviceError, InvalidInputError,
+                     StructFFTError)
+from .hidft import ButterflyPlan, HiDftResult, get_plan, hidft, hidft_to_dft, hidft_to_dft_batched
+from .sampling import SamplingPattern, pivoted_pattern, pivoted_pattern_tensor
+from .sas import SasPlan, SasResult, predicted_cost, sas_transform, select_pivots
+
+__version__ = "0.1.0"

@@ -1,0 +1,92 @@
+// Shared device/host helpers for the B200 Hi-DFT library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "structfft_b200.h"
+
+namespace sfft {
+
+// ------------------------------------------------------------ complex ---
+template <typename T> struct Cx;
+template <> struct __align__(8) Cx<float> { float x, y; };
+template <> struct __align__(16) Cx<double> { double x, y; };
+
+template <typename T>
+__device__ __forceinline__ Cx<T> cadd(Cx<T> a, Cx<T> b) { return {a.x + b.x, a.y + b.y}; }
+template <typename T>
+__device__ __forceinline__ Cx<T> csub(Cx<T> a, Cx<T> b) { return {a.x - b.x, a.y - b.y}; }
+template <typename T>
+__device__ __forceinline__ Cx<T> cmul(Cx<T> a, Cx<T> b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T>
+__device__ __forceinline__ Cx<T> cscale(Cx<T> a, T s) { return {a.x * s, a.y * s}; }
+
+// Streaming sample loads: one sector per sample in the sparse patterns, no
+// reuse through L1, so bypass L1 allocation.
+__device__ __forceinline__ Cx<float> load_sample(const Cx<float>* p) {
+  Cx<float> r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
+               : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Cx<double> load_sample(const Cx<double>* p) {
+  Cx<double> r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+// Twiddle exp(-2 pi i (shared + 2^rk) / 2^(rk+1)) (hidft.py:83), evaluated
+// with an exact reduced argument: u = (shared + 2^rk) mod 2^(rk+1), angle
+// -u/2^rk in units of pi.
+__device__ __forceinline__ void twiddle_d(uint32_t shared, int rk, double& c, double& s) {
+  const uint64_t u = ((uint64_t)shared + (1ull << rk)) & ((2ull << rk) - 1);
+  const double th = -(double)u * ldexp(1.0, -rk);
+  sincospi(th, &s, &c);
+}
+template <typename T> __device__ __forceinline__ Cx<T> twiddle(uint32_t shared, int rk);
+template <> __device__ __forceinline__ Cx<double> twiddle<double>(uint32_t shared, int rk) {
+  double c, s;
+  twiddle_d(shared, rk, c, s);
+  return {c, s};
+}
+template <> __device__ __forceinline__ Cx<float> twiddle<float>(uint32_t shared, int rk) {
+  if (rk < 23) {  // u < 2^24: the fp32 argument is exact, sincospif is ~1 ulp
+    const uint32_t u = (shared + (1u << rk)) & ((2u << rk) - 1);
+    const float th = -(float)u * ldexpf(1.0f, -rk);
+    float s, c;
+    sincospif(th, &s, &c);
+    return {c, s};
+  }
+  double c, s;
+  twiddle_d(shared, rk, c, s);
+  return {(float)c, (float)s};
+}
+
+// bit extract: pattern bits of j at the pivot positions piv[0..s)
+__device__ __forceinline__ uint32_t pext_pivots(uint32_t j, const int* piv, int s) {
+  uint32_t p = 0;
+  for (int i = 0; i < s; ++i) p |= ((j >> piv[i]) & 1u) << i;
+  return p;
+}
+
+// ------------------------------------------------------------ host side ---
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define SFFT_CUDA(call)                                        \
+  do {                                                         \
+    cudaError_t e__ = (call);                                  \
+    if (e__ != cudaSuccess) return ::sfft::cuda_fail(e__, #call); \
+  } while (0)
+
+bool is_device_pointer(const void* p);
+int num_sms();
+
+}  // namespace sfft

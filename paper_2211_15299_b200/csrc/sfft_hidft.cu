@@ -1,0 +1,701 @@
+// Hi-DFT transform kernels for sm_100a: gather -> generalised radix-2
+// butterfly -> permuted, scaled store, one launch per batch.
+//
+// Reference: hidft.py:135-185 (hidft), hidft.py:188-207 (hidft_to_dft),
+// sas.py:336-371 (sas_transform, mu*=1).
+//
+// Slot a (0 <= a < A = 2^s) holds, before stage 1, the sample at
+//   off(a) = sum_i bit_i(a) 2^(M-1-used_i)            (hidft.py:155-158)
+// and stage k pairs slots differing in bit k-1 with the twiddle
+// tw_k[a mod 2^(k-1)]; branch 0 = v0 - w v1, branch 1 = v0 + w v1
+// (hidft.py:160-167).  That is a radix-2 DIT network with data-dependent
+// twiddles, so it is executed as a register-blocked Stockham-style FFT:
+// every thread owns E slots, runs log2(E) stages in registers, and trades
+// slots through (swizzled) shared memory between passes.
+//
+// Layout in HBM: signals are rows of N complex (c64 = float2, c128 =
+// double2) with row stride ld; outputs are rows of n_out complex.
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "sfft_common.cuh"
+#include "sfft_plan.h"
+
+namespace sfft {
+
+constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+
+template <typename T> struct EMax;
+template <> struct EMax<float> { static constexpr int v = 16; static constexpr int SWZ = 4; };
+template <> struct EMax<double> { static constexpr int v = 8; static constexpr int SWZ = 3; };
+
+template <typename T, int S>
+struct Geo {
+  static constexpr int A = 1 << S;
+  static constexpr int E = A < EMax<T>::v ? A : EMax<T>::v;  // slots per thread
+  static constexpr int LE = ilog2c(E);
+  static constexpr int TPS = A / E;                           // threads per signal
+  static constexpr int NT = TPS > 256 ? TPS : 256;            // threads per CTA
+  static constexpr int SPC = NT / TPS;                        // signals per CTA
+  static constexpr int NPASS = S == 0 ? 1 : (S + LE - 1) / LE;
+  static constexpr int NTAB = S <= 8 ? 1 : (S + 7) / 8;       // offset tables
+  static constexpr int TABW = S < 8 ? A : 256;                // entries per table
+};
+
+// Bank-conflict-free shared-memory slot position: XOR the low SWZ bits with
+// the XOR-fold of the higher bits.  A bijection inside each aligned block,
+// conflict-free for every power-of-two lane stride used below.
+template <typename T, int S>
+__device__ __forceinline__ int swz(int a) {
+  constexpr int B = EMax<T>::SWZ;
+  int y = a >> B, f = 0;
+#pragma unroll
+  for (int i = 0; i < (S + B - 1) / B; ++i) {
+    f ^= y & ((1 << B) - 1);
+    y >>= B;
+  }
+  return a ^ f;
+}
+
+// Slot owned by thread t (within its signal) for register x in pass p:
+// bits [w0, w0+LE) come from x, the rest from t.
+template <int S, int LE>
+__device__ __forceinline__ int slot_of(int p, int t, int x) {
+  const int w0 = (p * LE < S - LE) ? p * LE : S - LE;
+  return (t & ((1 << w0) - 1)) | (x << w0) | ((t >> w0) << (w0 + LE));
+}
+
+// Stages [p*LE, min(p*LE+LE, S)) of pass p, in registers.
+template <typename T, int S, int E, int LE>
+__device__ __forceinline__ void pass_stages(Cx<T> (&v)[E], int p, int t, const Cx<T>* __restrict__ tw) {
+  const int b0 = p * LE;
+  const int b1 = (b0 + LE < S) ? b0 + LE : S;
+  const int w0 = (b0 < S - LE) ? b0 : S - LE;
+#pragma unroll
+  for (int beta = b0; beta < b1; ++beta) {
+    const int lb = beta - w0;
+#pragma unroll
+    for (int x = 0; x < E; ++x) {
+      if (x & (1 << lb)) continue;
+      const int a = slot_of<S, LE>(p, t, x);
+      const int h = a & ((1 << beta) - 1);
+      const Cx<T> w = tw[(1 << beta) - 1 + h];
+      const Cx<T> u = v[x];
+      const Cx<T> z = cmul(w, v[x | (1 << lb)]);
+      v[x] = csub(u, z);
+      v[x | (1 << lb)] = cadd(u, z);
+    }
+  }
+}
+
+// Whole butterfly for one signal per thread group.  On entry v holds the
+// pass-0 slots (x + t*E); on exit the slot values sit in sd (swizzled) and
+// the CTA has passed a barrier.
+template <typename T, int S>
+__device__ __forceinline__ void butterfly(Cx<T> (&v)[Geo<T, S>::E], int t, Cx<T>* sd,
+                                          const Cx<T>* __restrict__ tw) {
+  using G = Geo<T, S>;
+#pragma unroll
+  for (int p = 0; p < G::NPASS; ++p) {
+    if (p > 0) {
+#pragma unroll
+      for (int x = 0; x < G::E; ++x) v[x] = sd[swz<T, S>(slot_of<S, G::LE>(p, t, x))];
+    }
+    pass_stages<T, S, G::E, G::LE>(v, p, t, tw);
+#pragma unroll
+    for (int x = 0; x < G::E; ++x) sd[swz<T, S>(slot_of<S, G::LE>(p, t, x))] = v[x];
+    __syncthreads();
+  }
+}
+
+// Pass-0 gather: slot a = x + t*E reads sample (off(a) - shift) mod N.
+template <typename T, int S>
+__device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S>::E], int t, const Cx<T>* row,
+                                       const int* tab, uint32_t negshift, uint32_t nmask) {
+  using G = Geo<T, S>;
+  uint32_t idx[G::E];
+#pragma unroll
+  for (int x = 0; x < G::E; ++x) {
+    const int a = x + t * G::E;
+    uint32_t off = (uint32_t)tab[a & (G::TABW - 1)];
+    if (G::NTAB > 1) off += (uint32_t)tab[256 + ((a >> 8) & 255)];
+    if (G::NTAB > 2) off += (uint32_t)tab[512 + ((a >> 16) & 255)];
+    idx[x] = (off + negshift) & nmask;
+  }
+#pragma unroll
+  for (int x = 0; x < G::E; ++x) v[x] = load_sample(row + idx[x]);
+}
+
+// offset tables: tab[q][v] = sum over bits b of v of 2^(M-1-piv[8q+b])
+__device__ __forceinline__ void build_offset_tables(int* tab, int ntab, int tabw, const int* piv, int s,
+                                                    int M, int tid, int nthr) {
+  for (int i = tid; i < ntab * tabw; i += nthr) {
+    const int q = i / tabw, v = i % tabw;
+    uint32_t off = 0;
+    for (int b = 0; b < 8; ++b) {
+      const int pi = 8 * q + b;
+      if (pi < s && ((v >> b) & 1)) off += 1u << (M - 1 - piv[pi]);
+    }
+    tab[i] = (int)off;
+  }
+}
+
+// ------------------------------------------------------ plan-driven kernel ---
+
+struct PlanArgs {
+  const void* sig;
+  int64_t B, ld;
+  int M;
+  uint32_t negshift;
+  int32_t used[32];
+  const void* tw;
+  const int32_t* map1;  // NULL => identity
+  int64_t n1;
+  double scale1;
+  void* out1;
+  int64_t ld1;
+  void* out2;  // optional slot values (identity map)
+  int64_t ld2;
+  int identity;  // samples already gathered in slot order (row[a] = slot a)
+};
+
+template <typename T, int S> constexpr bool plan_tw_in_smem() {
+  return (size_t)(Geo<T, S>::SPC + 1) * Geo<T, S>::A * sizeof(Cx<T>) <= 160 * 1024;
+}
+template <typename T, int S> constexpr size_t plan_smem() {
+  using G = Geo<T, S>;
+  return (size_t)G::SPC * G::A * sizeof(Cx<T>) +
+         (plan_tw_in_smem<T, S>() ? (size_t)(G::A > 1 ? G::A - 1 : 1) * sizeof(Cx<T>) : 0) +
+         (size_t)G::NTAB * G::TABW * sizeof(int);
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(Geo<T, S>::NT)
+k_hidft_plan(const PlanArgs args) {
+  using G = Geo<T, S>;
+  constexpr bool TWS = plan_tw_in_smem<T, S>();  // twiddles staged in smem, else read via L1/L2
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);
+  Cx<T>* stw = sdata + G::SPC * G::A;
+  int* stab = reinterpret_cast<int*>(stw + (TWS ? (G::A > 1 ? G::A - 1 : 1) : 0));
+  __shared__ int spiv[32];
+
+  const int tid = threadIdx.x;
+  const int g = tid / G::TPS, t = tid % G::TPS;
+  if (tid < 32) spiv[tid] = args.used[tid];
+  const Cx<T>* gtw = reinterpret_cast<const Cx<T>*>(args.tw);
+  if (TWS)
+    for (int i = tid; i < G::A - 1; i += G::NT) stw[i] = gtw[i];
+  const Cx<T>* tw = TWS ? stw : gtw;
+  __syncthreads();
+  if (args.identity) {  // off(a) = a: table q maps v -> v << 8q
+    for (int i = tid; i < G::NTAB * G::TABW; i += G::NT) stab[i] = (i % G::TABW) << (8 * (i / G::TABW));
+  } else {
+    build_offset_tables(stab, G::NTAB, G::TABW, spiv, S, args.M, tid, G::NT);
+  }
+  __syncthreads();
+
+  const uint32_t nmask = args.identity ? (uint32_t)(G::A - 1)
+                                        : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
+  const int64_t ngroups = (args.B + G::SPC - 1) / G::SPC;
+  const T scale = (T)args.scale1;
+  Cx<T>* sd = sdata + g * G::A;
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t b = grp * G::SPC + g;
+    const bool live = b < args.B;
+    Cx<T> v[G::E];
+    if (live) {
+      const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
+      gather<T, S>(v, t, row, stab, args.negshift, nmask);
+    } else {
+#pragma unroll
+      for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
+    }
+    butterfly<T, S>(v, t, sd, tw);
+    if (live) {
+      Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
+      for (int64_t i = t; i < args.n1; i += G::TPS) {
+        const int a = args.map1 ? args.map1[i] : (int)i;
+        o1[i] = cscale(sd[swz<T, S>(a)], scale);
+      }
+      if (args.out2) {
+        Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2;
+        for (int i = t; i < G::A; i += G::TPS) o2[i] = sd[swz<T, S>(i)];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------- fused homogeneous to_dft ---
+//
+// pivots(J) for a homogeneous J without sorting: every pivot shows up as
+// v2(j - j0) for the fixed element j0 (all nodes at a pivot level split), so
+// P0 = OR_e 1 << ctz(j_e ^ j_0).  J is homogeneous iff |J| = 2^|P0|, the
+// pattern map j -> pext(j, P0) is a bijection onto [0, 2^s), and for every
+// slot x != 0 the element at x and the one at x minus its top bit first
+// differ exactly at the pivot of that top bit (then every pairwise v2 lies in
+// P0; congruence.py:235-241).  Representatives of every slot prefix are the
+// elements at slot h < 2^(k-1) (all members of a prefix agree below the next
+// pivot), which gives the twiddles of hidft.py:81-83.
+
+struct FusedArgs {
+  const int64_t* J;  // n_supports x k
+  int64_t n_supports;
+  const void* sig;
+  int64_t B, ld;
+  int M;
+  void* out;
+  int64_t ld_out;
+  int32_t* status;  // n_supports
+};
+
+// Plan for one support on `nthr` threads (tid in [0, nthr)).  Every thread
+// of the CTA must call it at the same time (it uses CTA barriers); several
+// thread groups may build several plans concurrently.  Writes spats
+// (element -> slot), stw (A-1 twiddles) and stab (offset tables).
+// scratch: 2*A ints.  Returns 0 ok, 2 invalid support, 3 not homogeneous.
+template <typename T, int S>
+__device__ int fused_plan(const int64_t* __restrict__ Jrow, bool live, int M, int tid, int nthr,
+                          int* spats, Cx<T>* stw, int* stab, int* scratch, int* sctl) {
+  using G = Geo<T, S>;
+  constexpr int A = G::A;
+  int* sJ = scratch;
+  int* sElem = scratch + A;
+  int* spiv = sctl + 2;  // sctl[0] = pivot mask P0, sctl[1] = status
+  const int64_t N = 1ll << M;
+  if (tid == 0) { sctl[0] = 0; sctl[1] = 0; }
+  __syncthreads();
+  int bad = 0;
+  if (live) {
+    for (int e = tid; e < A; e += nthr) {
+      const int64_t j = Jrow[e];
+      if (j < 0 || j >= N) bad = 2;
+      sJ[e] = (int)(j & (N - 1));
+    }
+  }
+  __syncthreads();
+  uint32_t mask = 0;
+  if (live) {
+    const int j0 = sJ[0];
+    for (int e = tid; e < A; e += nthr) {
+      const int j = sJ[e];
+      if (e > 0) {
+        if (sJ[e - 1] >= j) bad = 2;
+        else mask |= 1u << (__ffs(j ^ j0) - 1);
+      }
+    }
+  }
+  if (mask) atomicOr(reinterpret_cast<unsigned*>(&sctl[0]), mask);
+  if (bad) atomicMax(&sctl[1], bad);
+  __syncthreads();
+  mask = (uint32_t)sctl[0];
+  const bool go = live && sctl[1] == 0 && __popc(mask) == S;
+  if (go && tid < S) spiv[tid] = (int)__fns(mask, 0, tid + 1);
+  __syncthreads();
+  int piv[S > 0 ? S : 1];
+  if (go) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) piv[i] = spiv[i];
+    for (int e = tid; e < A; e += nthr) {
+      const uint32_t j = (uint32_t)sJ[e];
+      uint32_t p = 0;
+#pragma unroll
+      for (int i = 0; i < S; ++i) p |= ((j >> piv[i]) & 1u) << i;
+      spats[e] = (int)p;
+      sElem[p] = (int)j;
+    }
+  }
+  __syncthreads();
+  if (go) {
+    bad = 0;
+    for (int e = tid; e < A; e += nthr)
+      if (sElem[spats[e]] != sJ[e]) bad = 3;  // two elements share a pattern
+    for (int x = tid + 1; x < A; x += nthr) {
+      const int top = 31 - __clz(x);
+      const uint32_t d = (uint32_t)(sElem[x] ^ sElem[x ^ (1 << top)]);
+      if (d == 0 || __ffs(d) - 1 != piv[top]) bad = 3;  // v2 outside P0
+    }
+    if (bad) atomicMax(&sctl[1], bad);
+    for (int idx = tid; idx < A - 1; idx += nthr) {
+      const int beta = 31 - __clz(idx + 1);
+      const int h = idx + 1 - (1 << beta);
+      const int rk = piv[beta];
+      const uint32_t shared = (uint32_t)sElem[h] & ((1u << rk) - 1u);
+      stw[idx] = twiddle<T>(shared, rk);
+    }
+    build_offset_tables(stab, G::NTAB, G::TABW, spiv, S, M, tid, nthr);
+  }
+  __syncthreads();
+  if (!live) return 0;
+  if (sctl[1] != 0) return sctl[1];
+  return __popc(mask) == S ? 0 : 3;
+}
+
+template <typename T, int S, bool PER_SIGNAL>
+__global__ void __launch_bounds__(Geo<T, S>::NT)
+k_fused_to_dft(const FusedArgs args) {
+  using G = Geo<T, S>;
+  constexpr int A = G::A;
+  constexpr int NP = PER_SIGNAL ? G::SPC : 1;  // plans held per CTA
+  constexpr int TWN = A > 1 ? A - 1 : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);          // SPC * A
+  Cx<T>* stw_all = sdata + G::SPC * A;                        // NP * TWN
+  int* spats_all = reinterpret_cast<int*>(stw_all + NP * TWN);  // NP * A
+  int* stab_all = spats_all + NP * A;                         // NP * NTAB*TABW
+  __shared__ int sctl[NP][2 + (S > 0 ? S : 1)];
+
+  const int tid = threadIdx.x;
+  const int g = tid / G::TPS, t = tid % G::TPS;
+  const uint32_t nmask = (args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u);
+  const T scale = (T)((double)(1ll << args.M) / (double)A);
+  const int64_t ngroups = (args.B + G::SPC - 1) / G::SPC;
+  Cx<T>* sd = sdata + g * A;
+  const int pg = PER_SIGNAL ? g : 0;
+  int* pats = spats_all + pg * A;
+  Cx<T>* tw = stw_all + pg * TWN;
+  int* tab = stab_all + pg * G::NTAB * G::TABW;
+
+  if (!PER_SIGNAL) {
+    // one plan per CTA, built by all its threads; scratch aliases the data area
+    const int st = fused_plan<T, S>(args.J, true, args.M, tid, G::NT, pats, tw, tab,
+                                    reinterpret_cast<int*>(sdata), &sctl[0][0]);
+    if (blockIdx.x == 0 && tid == 0 && args.status) args.status[0] = st;
+    if (st != 0) return;  // uniform across the CTA
+  }
+
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t b = grp * G::SPC + g;
+    const bool live = b < args.B;
+    int st = 0;
+    if (PER_SIGNAL) {
+      // every group builds the plan of its own signal's support, concurrently
+      st = fused_plan<T, S>(args.J + (live ? b : 0) * (int64_t)A, live, args.M, t, G::TPS,
+                            pats, tw, tab, reinterpret_cast<int*>(sd), &sctl[g][0]);
+      if (live && t == 0 && args.status) args.status[b] = st;
+    }
+    const bool ok = live && st == 0;
+    Cx<T> v[G::E];
+    if (ok) {
+      const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
+      gather<T, S>(v, t, row, tab, 0u, nmask);
+    } else {
+#pragma unroll
+      for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
+    }
+    butterfly<T, S>(v, t, sd, tw);
+    if (ok) {
+      Cx<T>* o = reinterpret_cast<Cx<T>*>(args.out) + b * args.ld_out;
+      for (int i = t; i < A; i += G::TPS) o[i] = cscale(sd[swz<T, S>(pats[i])], scale);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ launchers ---
+
+template <typename T, int S, bool PS> constexpr size_t fused_smem() {
+  using G = Geo<T, S>;
+  constexpr size_t NP = PS ? G::SPC : 1;
+  return (size_t)G::SPC * G::A * sizeof(Cx<T>) + NP * (G::A > 1 ? G::A - 1 : 1) * sizeof(Cx<T>) +
+         NP * G::A * sizeof(int) + NP * G::NTAB * G::TABW * sizeof(int);
+}
+
+template <typename K>
+static int prep_grid(K kernel, int nt, size_t smem, int64_t ngroups, int* grid) {
+  if (smem > 48 * 1024)
+    SFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  SFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, smem));
+  if (occ < 1) return fail(SFFT_ERR_UNSUPPORTED, "kernel does not fit on an SM");
+  const int64_t cap = (int64_t)num_sms() * occ;
+  *grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, ngroups));
+  return SFFT_OK;
+}
+
+template <typename T, int S>
+static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {
+  using G = Geo<T, S>;
+  constexpr size_t smem = plan_smem<T, S>();
+  static_assert(smem <= 227 * 1024, "plan kernel smem");
+  auto kern = k_hidft_plan<T, S>;
+  int grid = 0;
+  const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
+  int rc = prep_grid(kern, G::NT, smem, ngroups, &grid);
+  if (rc) return rc;
+  kern<<<grid, G::NT, smem, st>>>(a);
+  SFFT_CUDA(cudaGetLastError());
+  return SFFT_OK;
+}
+
+template <typename T, int S, bool PS>
+static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
+  using G = Geo<T, S>;
+  constexpr size_t smem = fused_smem<T, S, PS>();
+  static_assert(smem <= 227 * 1024, "fused kernel smem");
+  auto kern = k_fused_to_dft<T, S, PS>;
+  int grid = 0;
+  const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
+  int rc = prep_grid(kern, G::NT, smem, ngroups, &grid);
+  if (rc) return rc;
+  kern<<<grid, G::NT, smem, st>>>(a);
+  SFFT_CUDA(cudaGetLastError());
+  return SFFT_OK;
+}
+
+// largest s handled on one CTA (data for one signal resident in shared memory)
+constexpr int kMaxPlanS_c64 = 14, kMaxPlanS_c128 = 13;
+constexpr int kMaxFusedS_c64 = 13, kMaxFusedS_c128 = 12;
+
+int max_supported_s(int dtype) { return dtype == SFFT_C64 ? kMaxPlanS_c64 : kMaxPlanS_c128; }
+
+#define SFFT_CASES_12(M_, ...) \
+  M_(0, __VA_ARGS__) M_(1, __VA_ARGS__) M_(2, __VA_ARGS__) M_(3, __VA_ARGS__) M_(4, __VA_ARGS__) \
+  M_(5, __VA_ARGS__) M_(6, __VA_ARGS__) M_(7, __VA_ARGS__) M_(8, __VA_ARGS__) M_(9, __VA_ARGS__) \
+  M_(10, __VA_ARGS__) M_(11, __VA_ARGS__) M_(12, __VA_ARGS__)
+
+#define PLAN_CASE(S_, T_) case S_: return run_plan_kernel<T_, S_>(a, st);
+#define FUSED_CASE(S_, T_, PS_) case S_: return run_fused_kernel<T_, S_, PS_>(a, st);
+
+static int dispatch_plan(int dtype, int s, const PlanArgs& a, cudaStream_t st) {
+  if (dtype == SFFT_C64) {
+    switch (s) {
+      SFFT_CASES_12(PLAN_CASE, float)
+      PLAN_CASE(13, float)
+      PLAN_CASE(14, float)
+      default: break;
+    }
+  } else {
+    switch (s) {
+      SFFT_CASES_12(PLAN_CASE, double)
+      PLAN_CASE(13, double)
+      default: break;
+    }
+  }
+  return fail(SFFT_ERR_UNSUPPORTED, "2^s slots exceed the single-CTA transform (s=" +
+                                        std::to_string(s) + ")");
+}
+
+template <bool PS>
+static int dispatch_fused(int dtype, int s, const FusedArgs& a, cudaStream_t st) {
+  if (dtype == SFFT_C64) {
+    switch (s) {
+      SFFT_CASES_12(FUSED_CASE, float, PS)
+      FUSED_CASE(13, float, PS)
+      default: break;
+    }
+  } else {
+    switch (s) {
+      SFFT_CASES_12(FUSED_CASE, double, PS)
+      default: break;
+    }
+  }
+  return fail(SFFT_ERR_UNSUPPORTED, "2^s slots exceed the fused single-CTA transform (s=" +
+                                        std::to_string(s) + ")");
+}
+
+int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld, int64_t shift,
+                      const int32_t* map1, int64_t n1, double scale1, void* out1, int64_t ld1,
+                      void* out2, int64_t ld2, int identity, cudaStream_t st) {
+  PlanArgs a{};
+  a.identity = identity;
+  a.sig = sig;
+  a.B = B;
+  a.ld = ld;
+  a.M = p->M;
+  const int64_t N = 1ll << p->M;
+  const int64_t sh = ((shift % N) + N) % N;
+  a.negshift = (uint32_t)((N - sh) & (N - 1));
+  for (int i = 0; i < 32; ++i) a.used[i] = i < p->s ? p->used[i] : 0;
+  a.tw = p->d_twiddles;
+  a.map1 = map1;
+  a.n1 = n1;
+  a.scale1 = scale1;
+  a.out1 = out1;
+  a.ld1 = ld1;
+  a.out2 = out2;
+  a.ld2 = ld2;
+  return dispatch_plan(p->dtype, p->s, a, st);
+}
+
+template <typename T>
+__global__ void k_apply_map(const Cx<T>* __restrict__ in, int64_t B, int64_t ld_in,
+                            const int32_t* __restrict__ map, int64_t n, T scale, Cx<T>* __restrict__ out,
+                            int64_t ld_out) {
+  const int64_t total = B * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / n, e = i % n;
+    out[b * ld_out + e] = cscale(in[b * ld_in + map[e]], scale);
+  }
+}
+
+// resolve (map, n_out, scale) for an output kind, checking its contract
+static int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, int64_t* n_out,
+                    double* scale) {
+  const double N = (double)(1ll << plan->M);
+  *scale = 1.0;
+  switch (out_kind) {
+    case SFFT_OUT_NODES:
+      *map = plan->d_node_slots;
+      *n_out = plan->n_nodes;
+      return SFFT_OK;
+    case SFFT_OUT_SLOTS:
+      *map = nullptr;
+      *n_out = plan->A;
+      return SFFT_OK;
+    case SFFT_OUT_DFT:  // hidft.py:196-207
+      if (!plan->homogeneous)
+        return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a homogeneous support");
+      if (plan->height != 0)
+        return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a height-0 transform");
+      *map = plan->d_element_slots;
+      *n_out = plan->k;
+      *scale = N / (double)plan->k;
+      return SFFT_OK;
+    case SFFT_OUT_SAS:  // sas.py:363-371, weight-1 nodes only
+      if (plan->mu_star != 1)
+        return fail(SFFT_ERR_CONTRACT, "mu* > 1: node systems need Vandermonde decoding");
+      if (plan->height != 0) return fail(SFFT_ERR_CONTRACT, "sas decode needs height 0");
+      *map = plan->d_element_slots;
+      *n_out = plan->k;
+      *scale = N / (double)plan->A;
+      return SFFT_OK;
+    default:
+      return fail(SFFT_ERR_INVALID, "unknown out_kind");
+  }
+}
+
+}  // namespace sfft
+
+// ------------------------------------------------------------------ C-ABI ---
+using namespace sfft;
+
+static int hidft_common(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld,
+                        int64_t min_ld, int64_t shift, int out_kind, void* out, int64_t ld_out,
+                        void* slot_out, int64_t ld_slot, int identity, cudaStream_t st) {
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (B < 0) return fail(SFFT_ERR_INVALID, "negative batch");
+  const int32_t* map = nullptr;
+  int64_t n_out = 0;
+  double scale = 1.0;
+  int rc = out_spec(plan, out_kind, &map, &n_out, &scale);
+  if (rc) return rc;
+  if (B == 0) return SFFT_OK;
+  if (!signals || !out) return fail(SFFT_ERR_INVALID, "null signal or output pointer");
+  if (ld < min_ld) return fail(SFFT_ERR_INVALID, "signal row stride too small");
+  if (ld_out < n_out) return fail(SFFT_ERR_INVALID, "output row stride too small");
+  if (slot_out && ld_slot < plan->A) return fail(SFFT_ERR_INVALID, "slot row stride too small");
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  if (dev != plan->device) return fail(SFFT_ERR_INVALID, "plan belongs to another device");
+  return launch_hidft_plan(plan, signals, B, ld, shift, map, n_out, scale, out, ld_out, slot_out,
+                           ld_slot, identity, st);
+}
+
+extern "C" int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld,
+                          int64_t shift, int out_kind, void* out, int64_t ld_out, void* slot_out,
+                          int64_t ld_slot, sfft_stream_t stream) {
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  return hidft_common(plan, signals, B, ld, 1ll << plan->M, shift, out_kind, out, ld_out, slot_out,
+                      ld_slot, 0, (cudaStream_t)stream);
+}
+
+extern "C" int sfft_hidft_gathered(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld,
+                                   int out_kind, void* out, int64_t ld_out, void* slot_out,
+                                   int64_t ld_slot, sfft_stream_t stream) {
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  return hidft_common(plan, samples, B, ld, plan->A, 0, out_kind, out, ld_out, slot_out, ld_slot, 1,
+                      (cudaStream_t)stream);
+}
+
+extern "C" int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const void* slot_values,
+                                   int64_t B, int64_t ld, void* out, int64_t ld_out,
+                                   sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  const int32_t* map = nullptr;
+  int64_t n_out = 0;
+  double scale = 1.0;
+  int rc = out_spec(plan, out_kind, &map, &n_out, &scale);
+  if (rc) return rc;
+  if (!map) return fail(SFFT_ERR_INVALID, "slot output needs no map");
+  if (B <= 0) return B < 0 ? fail(SFFT_ERR_INVALID, "negative batch") : SFFT_OK;
+  if (ld < plan->A || ld_out < n_out) return fail(SFFT_ERR_INVALID, "row stride too small");
+  const int64_t total = B * n_out;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
+  if (plan->dtype == SFFT_C64)
+    k_apply_map<float><<<grid, 256, 0, st>>>((const Cx<float>*)slot_values, B, ld, map, n_out,
+                                             (float)scale, (Cx<float>*)out, ld_out);
+  else
+    k_apply_map<double><<<grid, 256, 0, st>>>((const Cx<double>*)slot_values, B, ld, map, n_out, scale,
+                                              (Cx<double>*)out, ld_out);
+  SFFT_CUDA(cudaGetLastError());
+  return SFFT_OK;
+}
+
+extern "C" int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_supports, int M,
+                                       const void* signals, int64_t B, int64_t ld, int dtype,
+                                       void* out, int64_t ld_out, int32_t* status,
+                                       sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
+  if (dtype != SFFT_C64 && dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown dtype");
+  if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
+  if (B < 0 || (n_supports != 1 && n_supports != B))
+    return fail(SFFT_ERR_INVALID, "n_supports must be 1 or B");
+  if (B == 0) return SFFT_OK;
+  if (!J || !signals || !out) return fail(SFFT_ERR_INVALID, "null pointer");
+  if (ld < (1ll << M)) return fail(SFFT_ERR_INVALID, "signal row stride smaller than N");
+  if (ld_out < k) return fail(SFFT_ERR_INVALID, "output row stride too small");
+  if (k & (k - 1)) return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a homogeneous support");
+  const int s = 63 - __builtin_clzll((unsigned long long)k);
+  if (s > (dtype == SFFT_C64 ? kMaxFusedS_c64 : kMaxFusedS_c128))
+    return fail(SFFT_ERR_UNSUPPORTED, "fused transform limited to 2^" +
+                                          std::to_string(dtype == SFFT_C64 ? kMaxFusedS_c64
+                                                                           : kMaxFusedS_c128) +
+                                          " slots");
+  const int64_t* dJ = J;
+  int64_t* tmpJ = nullptr;
+  if (!is_device_pointer(J)) {
+    SFFT_CUDA(cudaMallocAsync((void**)&tmpJ, sizeof(int64_t) * k * n_supports, st));
+    SFFT_CUDA(cudaMemcpyAsync(tmpJ, J, sizeof(int64_t) * k * n_supports, cudaMemcpyHostToDevice, st));
+    dJ = tmpJ;
+  }
+  int32_t* dstat = status;
+  int32_t* tmpStat = nullptr;
+  if (!dstat) {
+    SFFT_CUDA(cudaMallocAsync((void**)&tmpStat, sizeof(int32_t) * n_supports, st));
+    SFFT_CUDA(cudaMemsetAsync(tmpStat, 0, sizeof(int32_t) * n_supports, st));
+    dstat = tmpStat;
+  }
+  FusedArgs a{};
+  a.J = dJ;
+  a.n_supports = n_supports;
+  a.sig = signals;
+  a.B = B;
+  a.ld = ld;
+  a.M = M;
+  a.out = out;
+  a.ld_out = ld_out;
+  a.status = dstat;
+  int rc = (n_supports == 1 && B >= 1) ? dispatch_fused<false>(dtype, s, a, st)
+                                       : dispatch_fused<true>(dtype, s, a, st);
+  if (rc == SFFT_OK && tmpStat) {
+    std::vector<int32_t> h(n_supports);
+    cudaError_t e = cudaMemcpyAsync(h.data(), tmpStat, sizeof(int32_t) * n_supports,
+                                    cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "status readback");
+    for (int64_t i = 0; rc == SFFT_OK && i < n_supports; ++i) {
+      if (h[i] == 2) rc = fail(SFFT_ERR_INVALID, "support " + std::to_string(i) + " is not a valid SupportSet");
+      else if (h[i] == 3) rc = fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a homogeneous support (support " + std::to_string(i) + ")");
+    }
+  }
+  if (tmpJ) cudaFreeAsync(tmpJ, st);
+  if (tmpStat) cudaFreeAsync(tmpStat, st);
+  return rc;
+}

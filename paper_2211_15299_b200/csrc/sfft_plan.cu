@@ -1,0 +1,655 @@
+// Device-side support analysis and ButterflyPlan construction.
+//
+// Reference: congruence.py:76-101 (pivots), congruence.py:235-278 (classify,
+// part-homogeneity, validate_pivot_vector), sampling.py:62-71
+// (pivoted_pattern), hidft.py:69-95 (_build_plan), hidft.py:168-178 (node
+// ordering).  Every index table is bit-exact with the reference.
+//
+// pivots(J): the split levels of the congruence tree are exactly the levels
+// ctz(a ^ b) of ADJACENT pairs when J is sorted by its bit-reversed keys
+// (bit-reversal turns the LSB-first trie into an ordinary sorted order, and
+// every branching node of a trie is witnessed by an adjacent pair).  The
+// keys are distinct M-bit integers, so the sort is a bitmap rank:
+// set bits, prefix-popcount the words, rank = prefix + popc(low bits).
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sfft_common.cuh"
+#include "sfft_plan.h"
+
+namespace sfft {
+
+// ------------------------------------------------------------ errors ---
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return SFFT_ERR_CUDA;
+}
+
+bool is_device_pointer(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged ||
+         (attr.type == cudaMemoryTypeHost && attr.devicePointer == p);
+}
+
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+// --------------------------------------------------------- bitmap rank ---
+constexpr int kScanBlock = 1024;
+
+__global__ void k_support_keys(const int64_t* __restrict__ J, int64_t k, int M,
+                               uint32_t* __restrict__ keys, uint32_t* __restrict__ bitmap,
+                               int* __restrict__ status) {
+  const int64_t N = 1ll << M;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = J[e];
+    if (j < 0 || j >= N || (e > 0 && J[e - 1] >= j)) {
+      atomicMax(status, SFFT_ERR_INVALID);
+      keys[e] = 0;
+      continue;
+    }
+    const uint32_t key = __brev((uint32_t)j) >> (32 - M);
+    keys[e] = key;
+    atomicOr(&bitmap[key >> 5], 1u << (key & 31));
+  }
+}
+
+__global__ void k_set_bits(const uint32_t* __restrict__ keys, const uint8_t* __restrict__ valid,
+                           int64_t n, uint32_t* __restrict__ bitmap) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (valid && !valid[i]) continue;
+    const uint32_t key = keys[i];
+    atomicOr(&bitmap[key >> 5], 1u << (key & 31));
+  }
+}
+
+// block-exclusive prefix of popcounts over kScanBlock words
+__global__ void __launch_bounds__(kScanBlock)
+k_word_scan(const uint32_t* __restrict__ bitmap, int64_t nwords, uint32_t* __restrict__ wprefix,
+            uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t warp_tot[kScanBlock / 32];
+  const int64_t w = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+  const uint32_t c = w < nwords ? __popc(bitmap[w]) : 0u;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t x = warp_tot[lane];
+    uint32_t xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, xi, d);
+      if (lane >= d) xi += y;
+    }
+    warp_tot[lane] = xi - x;  // exclusive warp offsets
+    if (lane == 31) bsum[blockIdx.x] = xi;
+  }
+  __syncthreads();
+  if (w < nwords) wprefix[w] = warp_tot[wid] + incl - c;
+}
+
+// exclusive scan of the block sums on one CTA
+__global__ void __launch_bounds__(kScanBlock) k_bsum_scan(uint32_t* __restrict__ bsum, int64_t nb) {
+  __shared__ uint32_t warp_tot[kScanBlock / 32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t base = 0; base < nb; base += kScanBlock) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t c = i < nb ? bsum[i] : 0u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t x = warp_tot[lane];
+      uint32_t xi = x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, xi, d);
+        if (lane >= d) xi += y;
+      }
+      warp_tot[lane] = xi - x;
+    }
+    __syncthreads();
+    const uint32_t c0 = carry;
+    if (i < nb) bsum[i] = c0 + warp_tot[wid] + incl - c;
+    __syncthreads();
+    if (threadIdx.x == kScanBlock - 1) carry = c0 + warp_tot[wid] + incl;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ uint32_t bit_rank(uint32_t key, const uint32_t* bitmap,
+                                             const uint32_t* wprefix, const uint32_t* bprefix) {
+  const uint32_t w = key >> 5;
+  return bprefix[w / kScanBlock] + wprefix[w] + __popc(bitmap[w] & ((1u << (key & 31)) - 1u));
+}
+
+// sorted[rank(key)] = key, for the pivots
+__global__ void k_rank_scatter(const uint32_t* __restrict__ keys, int64_t n,
+                               const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ wprefix,
+                               const uint32_t* __restrict__ bprefix, uint32_t* __restrict__ sorted) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    sorted[bit_rank(keys[i], bitmap, wprefix, bprefix)] = keys[i];
+}
+
+// pivot mask from adjacent bit-reversed keys: lowest differing bit of J
+__global__ void k_adjacent_levels(const uint32_t* __restrict__ sorted, int64_t n, int M,
+                                  unsigned long long* __restrict__ mask) {
+  unsigned long long m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = sorted[i - 1] ^ sorted[i];
+    const int h = 31 - __clz(x);  // highest differing key bit
+    m |= 1ull << (M - 1 - h);
+  }
+  // warp-reduce then one atomic per warp
+  for (int d = 16; d > 0; d >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, d);
+  if ((threadIdx.x & 31) == 0 && m) atomicOr(mask, m);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+static int alloc(DevBuf& b, size_t bytes, cudaStream_t st) {
+  b.st = st;
+  SFFT_CUDA(cudaMallocAsync(&b.p, std::max<size_t>(bytes, 16), st));
+  return SFFT_OK;
+}
+
+static int grid_1d(int64_t n, int threads = 256) {
+  const int64_t g = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * 16));
+}
+
+// Ranks of n distinct keys < 2^L (optionally only those with valid[i]).
+struct RankCtx {
+  DevBuf bitmap, wprefix, bsum;
+  int64_t nwords = 0, nblocks = 0;
+};
+
+static int rank_prepare(RankCtx& R, const uint32_t* keys, const uint8_t* valid, int64_t n, int L,
+                        cudaStream_t st) {
+  R.nwords = std::max<int64_t>(1, (1ll << L) / 32);
+  R.nblocks = (R.nwords + kScanBlock - 1) / kScanBlock;
+  int rc;
+  if ((rc = alloc(R.bitmap, R.nwords * 4, st))) return rc;
+  if ((rc = alloc(R.wprefix, R.nwords * 4, st))) return rc;
+  if ((rc = alloc(R.bsum, R.nblocks * 4, st))) return rc;
+  SFFT_CUDA(cudaMemsetAsync(R.bitmap.p, 0, R.nwords * 4, st));
+  if (keys) k_set_bits<<<grid_1d(n), 256, 0, st>>>(keys, valid, n, (uint32_t*)R.bitmap.p);
+  return SFFT_OK;
+}
+
+static int rank_scan(RankCtx& R, cudaStream_t st) {
+  k_word_scan<<<(unsigned)R.nblocks, kScanBlock, 0, st>>>((const uint32_t*)R.bitmap.p, R.nwords,
+                                                        (uint32_t*)R.wprefix.p, (uint32_t*)R.bsum.p);
+  k_bsum_scan<<<1, kScanBlock, 0, st>>>((uint32_t*)R.bsum.p, R.nblocks);
+  SFFT_CUDA(cudaGetLastError());
+  return SFFT_OK;
+}
+
+static int to_device_J(const int64_t* J, int64_t k, cudaStream_t st, DevBuf& tmp, const int64_t** dJ) {
+  if (is_device_pointer(J)) {
+    *dJ = J;
+    return SFFT_OK;
+  }
+  int rc = alloc(tmp, sizeof(int64_t) * k, st);
+  if (rc) return rc;
+  SFFT_CUDA(cudaMemcpyAsync(tmp.p, J, sizeof(int64_t) * k, cudaMemcpyHostToDevice, st));
+  *dJ = (const int64_t*)tmp.p;
+  return SFFT_OK;
+}
+
+// pivots(J) on the device; *mask valid after the call (synchronises)
+static int analyze_device(const int64_t* dJ, int64_t k, int M, uint64_t* mask_out, cudaStream_t st) {
+  DevBuf keys, sorted, small;
+  RankCtx R;
+  int rc;
+  if ((rc = alloc(keys, k * 4, st))) return rc;
+  if ((rc = alloc(sorted, k * 4, st))) return rc;
+  if ((rc = alloc(small, 16, st))) return rc;
+  SFFT_CUDA(cudaMemsetAsync(small.p, 0, 16, st));
+  unsigned long long* dmask = (unsigned long long*)small.p;
+  int* dstatus = (int*)((char*)small.p + 8);
+  if ((rc = rank_prepare(R, nullptr, nullptr, k, M, st))) return rc;
+  k_support_keys<<<grid_1d(k), 256, 0, st>>>(dJ, k, M, (uint32_t*)keys.p, (uint32_t*)R.bitmap.p, dstatus);
+  if ((rc = rank_scan(R, st))) return rc;
+  k_rank_scatter<<<grid_1d(k), 256, 0, st>>>((const uint32_t*)keys.p, k, (const uint32_t*)R.bitmap.p,
+                                             (const uint32_t*)R.wprefix.p, (const uint32_t*)R.bsum.p,
+                                             (uint32_t*)sorted.p);
+  k_adjacent_levels<<<grid_1d(k), 256, 0, st>>>((const uint32_t*)sorted.p, k, M, dmask);
+  SFFT_CUDA(cudaGetLastError());
+  unsigned long long h[2] = {0, 0};
+  SFFT_CUDA(cudaMemcpyAsync(h, small.p, 16, cudaMemcpyDeviceToHost, st));
+  SFFT_CUDA(cudaStreamSynchronize(st));
+  const int status = (int)(h[1] & 0xffffffffu);
+  if (status) return fail(SFFT_ERR_INVALID, "support indices must be strictly increasing and lie in [0, N)");
+  *mask_out = h[0];
+  return SFFT_OK;
+}
+
+// --------------------------------------------------------- plan kernels ---
+__global__ void k_plan_elements(const int64_t* __restrict__ J, int64_t k, const int32_t* __restrict__ used,
+                                int s, int32_t* __restrict__ pats, uint32_t* __restrict__ count,
+                                uint32_t* __restrict__ mins) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = (uint32_t)J[e];
+    uint32_t p = 0;
+    for (int i = 0; i < s; ++i) p |= ((j >> used[i]) & 1u) << i;
+    pats[e] = (int32_t)p;
+    atomicAdd(&count[p], 1u);
+    atomicMin(&mins[p], j);
+  }
+}
+
+// reps level kk (2^kk entries at offset 2^kk - 1) = pairwise min of level kk+1
+__global__ void k_min_level(uint32_t* __restrict__ reps, int kk) {
+  const int64_t n = 1ll << kk;
+  uint32_t* lo = reps + (n - 1);
+  const uint32_t* hi = reps + (2 * n - 1);
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    lo[x] = min(hi[x], hi[x + n]);
+}
+
+// empty prefixes inherit parent residue below r with the branch bit set (hidft.py:87-90)
+__global__ void k_fill_level(uint32_t* __restrict__ reps, int kk, int r) {
+  const int64_t n = 1ll << kk;
+  uint32_t* cur = reps + (n - 1);
+  const uint32_t* par = reps + (n / 2 - 1);
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (cur[x] != 0xffffffffu) continue;
+    const uint32_t shared = par[x & (n / 2 - 1)] & ((1u << r) - 1u);
+    cur[x] = shared + ((uint32_t)((x >> (kk - 1)) & 1) << r);
+  }
+}
+
+template <typename T>
+__global__ void k_plan_twiddles(const uint32_t* __restrict__ reps, const int32_t* __restrict__ used,
+                                int64_t A, Cx<T>* __restrict__ tw) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < A - 1;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int beta = 63 - __clzll(idx + 1);
+    const int64_t h = idx + 1 - (1ll << beta);
+    const int rk = used[beta];
+    const uint32_t shared = reps[(1ll << beta) - 1 + h] & ((1u << rk) - 1u);
+    double c, s;
+    twiddle_d(shared, rk, c, s);
+    tw[idx] = Cx<T>{(T)c, (T)s};
+  }
+}
+
+__global__ void k_plan_slots(const uint32_t* __restrict__ reps_s, const uint32_t* __restrict__ count,
+                             int64_t A, int level, int32_t* __restrict__ slot_res,
+                             uint8_t* __restrict__ slot_real, unsigned long long* __restrict__ stats) {
+  const uint32_t lmask = level >= 32 ? 0xffffffffu : ((1u << level) - 1u);
+  unsigned long long nreal = 0, mu = 0;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    slot_res[x] = (int32_t)(reps_s[x] & lmask);
+    const uint32_t c = count[x];
+    slot_real[x] = c > 0;
+    nreal += c > 0;
+    mu = mu > c ? mu : c;
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    nreal += __shfl_xor_sync(0xffffffffu, nreal, d);
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, mu, d);
+    mu = mu > o ? mu : o;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&stats[0], nreal);
+    atomicMax(&stats[1], mu);
+  }
+}
+
+__global__ void k_node_order(const int32_t* __restrict__ slot_res, const uint8_t* __restrict__ slot_real,
+                             int64_t A, const uint32_t* __restrict__ bitmap,
+                             const uint32_t* __restrict__ wprefix, const uint32_t* __restrict__ bprefix,
+                             int32_t* __restrict__ node_slots, int32_t* __restrict__ node_res) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (!slot_real[x]) continue;
+    const uint32_t res = (uint32_t)slot_res[x];
+    const uint32_t rk = bit_rank(res, bitmap, wprefix, bprefix);
+    node_slots[rk] = (int32_t)x;
+    node_res[rk] = (int32_t)res;
+  }
+}
+
+__global__ void k_offsets(const int32_t* __restrict__ used, int s, int M, int64_t A, int64_t* __restrict__ off,
+                          int sorted_order) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < A;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    // slot order: off(a) = sum_i bit_i(a) 2^(M-1-used_i) (hidft.py:155-158);
+    // sorted order (I_r ascending) is the same sum over the bit-reversed index.
+    int64_t v = 0;
+    for (int i = 0; i < s; ++i) {
+      const int bit = sorted_order ? (int)((a >> (s - 1 - i)) & 1) : (int)((a >> i) & 1);
+      v += (int64_t)bit << (M - 1 - used[i]);
+    }
+    off[a] = v;
+  }
+}
+
+__global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+}  // namespace sfft
+
+// ------------------------------------------------------------------ C-ABI ---
+using namespace sfft;
+
+static int validate_r(const int32_t* r, int n_r, int M) {
+  if (n_r < 0 || n_r > 31) return fail(SFFT_ERR_INVALID, "pivot vector too long");
+  if (n_r > 0 && !r) return fail(SFFT_ERR_INVALID, "null pivot vector");
+  for (int i = 0; i + 1 < n_r; ++i)
+    if (r[i] >= r[i + 1]) return fail(SFFT_ERR_INVALID, "pivot vector must be strictly increasing");
+  for (int i = 0; i < n_r; ++i)
+    if (r[i] < 0 || r[i] >= M)
+      return fail(SFFT_ERR_INVALID, "pivots must lie in [0, " + std::to_string(M) + ")");
+  return SFFT_OK;
+}
+
+static std::string tuple_str(const int32_t* r, int n) {
+  std::string s = "(";
+  for (int i = 0; i < n; ++i) s += std::to_string(r[i]) + (n == 1 ? "," : (i + 1 < n ? ", " : ""));
+  return s + ")";
+}
+
+extern "C" const char* sfft_version(void) { return "structfft_b200 0.1.0 (sm_100a)"; }
+extern "C" const char* sfft_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int sfft_device_ok(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major == 10 && minor == 0;
+}
+
+extern "C" int sfft_analyze(const int64_t* J, int64_t k, int M, uint64_t* pivot_mask, int* homogeneous,
+                            sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
+  if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
+  if (!J) return fail(SFFT_ERR_INVALID, "null support");
+  DevBuf tmp;
+  const int64_t* dJ = nullptr;
+  int rc = to_device_J(J, k, st, tmp, &dJ);
+  if (rc) return rc;
+  uint64_t mask = 0;
+  if ((rc = analyze_device(dJ, k, M, &mask, st))) return rc;
+  if (pivot_mask) *pivot_mask = mask;
+  if (homogeneous) *homogeneous = (k & (k - 1)) == 0 && __builtin_popcountll(mask) == 63 - __builtin_clzll(k);
+  return SFFT_OK;
+}
+
+__global__ void k_pattern(const int32_t* __restrict__ r, int n, int M, int64_t* __restrict__ out) {
+  const int64_t A = 1ll << n;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < A;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    // bit j of q (ascending) carries pivot r[n-1-j]: smallest offsets first
+    int64_t v = 0;
+    for (int j = 0; j < n; ++j) v += ((q >> j) & 1) << (M - 1 - r[n - 1 - j]);
+    out[q] = v;
+  }
+}
+
+extern "C" int sfft_pivoted_pattern(const int32_t* r, int n_r, int M, int64_t* out, sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M < 1 || M > 62) return fail(SFFT_ERR_INVALID, "M out of range");
+  int rc = validate_r(r, n_r, M);
+  if (rc) return rc;
+  if (n_r > 30) return fail(SFFT_ERR_UNSUPPORTED, "pattern too large");
+  const int64_t A = 1ll << n_r;
+  DevBuf dr, dout;
+  if ((rc = alloc(dr, sizeof(int32_t) * std::max(n_r, 1), st))) return rc;
+  if (n_r) SFFT_CUDA(cudaMemcpyAsync(dr.p, r, sizeof(int32_t) * n_r, cudaMemcpyHostToDevice, st));
+  const bool dev_out = is_device_pointer(out);
+  int64_t* target = out;
+  if (!dev_out) {
+    if ((rc = alloc(dout, sizeof(int64_t) * A, st))) return rc;
+    target = (int64_t*)dout.p;
+  }
+  k_pattern<<<grid_1d(A), 256, 0, st>>>((const int32_t*)dr.p, n_r, M, target);
+  SFFT_CUDA(cudaGetLastError());
+  if (!dev_out) {
+    SFFT_CUDA(cudaMemcpyAsync(out, target, sizeof(int64_t) * A, cudaMemcpyDeviceToHost, st));
+    SFFT_CUDA(cudaStreamSynchronize(st));
+  }
+  return SFFT_OK;
+}
+
+static void plan_free(sfft_plan* p) {
+  if (!p) return;
+  cudaFree(p->d_element_slots);
+  cudaFree(p->d_slot_residues);
+  cudaFree(p->d_slot_real);
+  cudaFree(p->d_node_slots);
+  cudaFree(p->d_node_residues);
+  cudaFree(p->d_twiddles);
+  delete p;
+}
+
+extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_t* r, int n_r, int height,
+                                int dtype, sfft_stream_t stream, sfft_plan** out_plan) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!out_plan) return fail(SFFT_ERR_INVALID, "null plan output");
+  *out_plan = nullptr;
+  if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
+  if (dtype != SFFT_C64 && dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown dtype");
+  if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
+  int rc = validate_r(r, n_r, M);  // congruence.py:272-278
+  if (rc) return rc;
+  DevBuf tmpJ;
+  const int64_t* dJ = nullptr;
+  if ((rc = to_device_J(J, k, st, tmpJ, &dJ))) return rc;
+  uint64_t mask = 0;
+  if ((rc = analyze_device(dJ, k, M, &mask, st))) return rc;
+  if (n_r > 0) {  // assert_part_homogeneous, congruence.py:259-269
+    const int rmax = r[n_r - 1];
+    uint64_t rmask = 0;
+    for (int i = 0; i < n_r; ++i) rmask |= 1ull << r[i];
+    const uint64_t bad = mask & ((2ull << rmax) - 1) & ~rmask;
+    if (bad)
+      return fail(SFFT_ERR_CONTRACT, "support is not " + tuple_str(r, n_r) + "-part-homogeneous: pivot " +
+                                         std::to_string(__builtin_ctzll(bad)) + " <= " + std::to_string(rmax) +
+                                         " missing from r");
+  }
+  if (height < 0 || height > n_r)
+    return fail(SFFT_ERR_INVALID, "height must be in [0, " + std::to_string(n_r) + "]");
+  const int s = n_r - height;
+  if (s > 26) return fail(SFFT_ERR_UNSUPPORTED, "more than 2^26 slots");
+  const int64_t A = 1ll << s;
+  const int level = s ? r[s - 1] + 1 : 0;
+
+  sfft_plan* p = new sfft_plan();
+  std::memset(p, 0, sizeof(*p));
+  SFFT_CUDA(cudaGetDevice(&p->device));
+  p->M = M;
+  p->dtype = dtype;
+  p->n_r = n_r;
+  p->height = height;
+  p->s = s;
+  p->level = level;
+  p->k = k;
+  p->A = A;
+  p->pivot_mask = mask;
+  p->homogeneous = (k & (k - 1)) == 0 && __builtin_popcountll(mask) == 63 - __builtin_clzll(k);
+  for (int i = 0; i < n_r; ++i) p->r[i] = r[i];
+  for (int i = 0; i < s; ++i) p->used[i] = r[i];
+  const size_t csz = dtype == SFFT_C64 ? 8 : 16;
+  cudaError_t e = cudaSuccess;
+  auto M_ = [&](void** ptr, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+  };
+  M_((void**)&p->d_element_slots, 4 * k);
+  M_((void**)&p->d_slot_residues, 4 * A);
+  M_((void**)&p->d_slot_real, A);
+  M_((void**)&p->d_node_slots, 4 * std::min<int64_t>(A, k));
+  M_((void**)&p->d_node_residues, 4 * std::min<int64_t>(A, k));
+  M_(&p->d_twiddles, csz * std::max<int64_t>(A - 1, 1));
+  if (e != cudaSuccess) {
+    plan_free(p);
+    return cuda_fail(e, "plan allocation");
+  }
+  auto done = [&](int code) {
+    if (code) plan_free(p);
+    return code;
+  };
+  DevBuf dused, count, reps, stats;
+  if ((rc = alloc(dused, 4 * 32, st))) return done(rc);
+  if ((rc = alloc(count, 4 * A, st))) return done(rc);
+  if ((rc = alloc(reps, 4 * (2 * A - 1), st))) return done(rc);
+  if ((rc = alloc(stats, 16, st))) return done(rc);
+  if (cudaMemcpyAsync(dused.p, p->used, 4 * 32, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemsetAsync(count.p, 0, 4 * A, st) != cudaSuccess ||
+      cudaMemsetAsync(reps.p, 0xff, 4 * (2 * A - 1), st) != cudaSuccess ||
+      cudaMemsetAsync(stats.p, 0, 16, st) != cudaSuccess)
+    return done(cuda_fail(cudaGetLastError(), "plan init"));
+  uint32_t* dreps = (uint32_t*)reps.p;
+  const int32_t* du = (const int32_t*)dused.p;
+  k_plan_elements<<<grid_1d(k), 256, 0, st>>>(dJ, k, du, s, p->d_element_slots, (uint32_t*)count.p,
+                                              dreps + (A - 1));
+  for (int kk = s - 1; kk >= 0; --kk) k_min_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk);
+  for (int kk = 1; kk <= s; ++kk) k_fill_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk, p->used[kk - 1]);
+  if (A > 1) {
+    if (dtype == SFFT_C64)
+      k_plan_twiddles<float><<<grid_1d(A), 256, 0, st>>>(dreps, du, A, (Cx<float>*)p->d_twiddles);
+    else
+      k_plan_twiddles<double><<<grid_1d(A), 256, 0, st>>>(dreps, du, A, (Cx<double>*)p->d_twiddles);
+  }
+  k_plan_slots<<<grid_1d(A), 256, 0, st>>>(dreps + (A - 1), (const uint32_t*)count.p, A, level,
+                                           p->d_slot_residues, p->d_slot_real,
+                                           (unsigned long long*)stats.p);
+  {
+    RankCtx R;
+    if ((rc = rank_prepare(R, nullptr, nullptr, A, level, st))) return done(rc);
+    // residues of real slots are distinct: set their bits, then rank
+    k_set_bits<<<grid_1d(A), 256, 0, st>>>((const uint32_t*)p->d_slot_residues, p->d_slot_real, A,
+                                           (uint32_t*)R.bitmap.p);
+    if ((rc = rank_scan(R, st))) return done(rc);
+    k_node_order<<<grid_1d(A), 256, 0, st>>>(p->d_slot_residues, p->d_slot_real, A,
+                                             (const uint32_t*)R.bitmap.p, (const uint32_t*)R.wprefix.p,
+                                             (const uint32_t*)R.bsum.p, p->d_node_slots, p->d_node_residues);
+  }
+  unsigned long long h[2];
+  if (cudaGetLastError() != cudaSuccess ||
+      cudaMemcpyAsync(h, stats.p, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return done(cuda_fail(cudaGetLastError(), "plan build"));
+  p->n_nodes = (int64_t)h[0];
+  p->mu_star = (int64_t)h[1];
+  *out_plan = p;
+  return SFFT_OK;
+}
+
+extern "C" int sfft_plan_destroy(sfft_plan* plan) {
+  plan_free(plan);
+  return SFFT_OK;
+}
+
+extern "C" int sfft_plan_get_info(const sfft_plan* p, sfft_plan_info* info) {
+  if (!p || !info) return fail(SFFT_ERR_INVALID, "null plan or info");
+  std::memset(info, 0, sizeof(*info));
+  info->M = p->M;
+  info->dtype = p->dtype;
+  info->n_r = p->n_r;
+  info->height = p->height;
+  info->s = p->s;
+  info->level = p->level;
+  info->homogeneous = p->homogeneous;
+  info->k = p->k;
+  info->A = p->A;
+  info->n_nodes = p->n_nodes;
+  info->mu_star = p->mu_star;
+  info->pivot_mask = p->pivot_mask;
+  for (int i = 0; i < 32; ++i) info->used[i] = i < p->s ? p->used[i] : 0;
+  return SFFT_OK;
+}
+
+static int copy_out(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  SFFT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+  return SFFT_OK;
+}
+
+extern "C" int sfft_plan_tables(const sfft_plan* p, int64_t* element_slots, int64_t* slot_residues,
+                                uint8_t* slot_real, int64_t* node_residues, int64_t* offsets, void* twiddles,
+                                sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!p) return fail(SFFT_ERR_INVALID, "null plan");
+  int rc;
+  DevBuf w, du;
+  const int64_t big = std::max(std::max(p->k, p->A), p->n_nodes);
+  if ((rc = alloc(w, 8 * big, st))) return rc;
+  int64_t* dw = (int64_t*)w.p;
+  auto widen = [&](const int32_t* src, int64_t n, int64_t* dst) -> int {
+    if (!dst) return SFFT_OK;
+    k_widen<<<grid_1d(n), 256, 0, st>>>(src, n, dw);
+    return copy_out(dst, dw, 8 * n, st) ? SFFT_ERR_CUDA : (cudaStreamSynchronize(st) == cudaSuccess ? SFFT_OK : SFFT_ERR_CUDA);
+  };
+  if ((rc = widen(p->d_element_slots, p->k, element_slots))) return rc;
+  if ((rc = widen(p->d_slot_residues, p->A, slot_residues))) return rc;
+  if ((rc = widen(p->d_node_residues, p->n_nodes, node_residues))) return rc;
+  if (slot_real && (rc = copy_out(slot_real, p->d_slot_real, p->A, st))) return rc;
+  if (twiddles && p->A > 1 &&
+      (rc = copy_out(twiddles, p->d_twiddles, (p->dtype == SFFT_C64 ? 8 : 16) * (p->A - 1), st)))
+    return rc;
+  if (offsets) {
+    if ((rc = alloc(du, 4 * 32, st))) return rc;
+    SFFT_CUDA(cudaMemcpyAsync(du.p, p->used, 4 * 32, cudaMemcpyHostToDevice, st));
+    k_offsets<<<grid_1d(p->A), 256, 0, st>>>((const int32_t*)du.p, p->s, p->M, p->A, dw, 0);
+    if ((rc = copy_out(offsets, dw, 8 * p->A, st))) return rc;
+  }
+  SFFT_CUDA(cudaStreamSynchronize(st));
+  return SFFT_OK;
+}

@@ -1,0 +1,28 @@
+// Internal plan object shared by the plan builder and the transform launchers.
+#pragma once
+
+#include <stdint.h>
+
+struct sfft_plan {
+  int device;
+  int M, dtype, n_r, height, s, level, homogeneous;
+  int64_t k, A, n_nodes, mu_star;
+  uint64_t pivot_mask;
+  int32_t r[32];
+  int32_t used[32];
+  // device tables (int32 indices: N <= 2^31)
+  int32_t* d_element_slots;  // k   slot of each support element (pats)
+  int32_t* d_slot_residues;  // A   residue mod 2^level, virtual slots inherit
+  uint8_t* d_slot_real;      // A
+  int32_t* d_node_slots;     // n_nodes  real slots in ascending residue order
+  int32_t* d_node_residues;  // n_nodes
+  void* d_twiddles;          // A-1 complex (dtype), stage-major
+};
+
+namespace sfft {
+// transform launchers (sfft_hidft.cu)
+int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld, int64_t shift,
+                      const int32_t* map1, int64_t n1, double scale1, void* out1, int64_t ld1,
+                      void* out2, int64_t ld2, int identity, cudaStream_t st);
+int max_supported_s(int dtype);
+}  // namespace sfft

@@ -1,0 +1,390 @@
+"""The Hi-DFT on B200: reference hidft.py's API over the CUDA C-ABI.
+
+`hidft(source, J, r, height, shift)` and `hidft_to_dft(res)` keep the
+reference signatures and results (hidft.py:135-207); a source may now also be
+a (B, N) batch.  `hidft_to_dft_batched` is the fused hot path: one kernel
+launch derives the plan on chip, gathers the 2^s samples of every signal,
+runs the butterfly and writes (Ff)_J in ascending-J order.
+
+Sources (hidft.py:34-49):
+  * CUDA tensor (N,) or (B, N), complex64 / complex128 -> computed in that
+    precision (complex64 signals run the float32 kernels);
+  * page-locked CPU tensor -> zero-copy gather over PCIe (only the 2^s
+    samples per signal cross the bus);
+  * pageable numpy / CPU tensor -> copied to the device once;
+  * callable loc -> samples, or an object with `sample_block(loc)` (e.g. the
+    reference's BandlimitedSignal) -> evaluated at the plan's offsets on the
+    host, then transformed on the device.
+Results are CUDA tensors for CUDA sources and numpy arrays otherwise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Any, Sequence
+
+import numpy as np
+
+from . import _lib
+from .congruence import (SupportSet, as_support, classify, validate_pivot_vector)
+from .errors import ContractViolationError, InvalidInputError
+
+_DT = {}  # filled lazily: torch dtype -> C dtype code
+
+
+def _torch():
+    import torch
+    if not _DT:
+        _DT[torch.complex64] = _lib.C64
+        _DT[torch.complex128] = _lib.C128
+    return torch
+
+
+# ------------------------------------------------------------------ plans ---
+
+class ButterflyPlan:
+    """Device ButterflyPlan (hidft.py:52-95) for one (J, used pivots, dtype).
+
+    Built by sfft_plan_create; the tables stay in HBM.  Host copies of the
+    index tables are made on demand (bit-exact with the reference)."""
+
+    def __init__(self, J: SupportSet, r: tuple[int, ...], height: int, dtype_code: int, device):
+        lib = _lib.load()
+        self.support = J
+        self.device = device
+        self.dtype_code = dtype_code
+        self._lib = lib
+        self.handle = ctypes.c_void_p(0)
+        rr = np.asarray(r if r else [0], dtype=np.int32)
+        dj = J.device_tensor(device)
+        _lib.check(lib.sfft_plan_create(dj.data_ptr(), len(J), J.M, rr.ctypes.data, len(r), int(height),
+                                        dtype_code, _lib.stream_ptr(device), ctypes.byref(self.handle)))
+        info = _lib.PlanInfo()
+        _lib.check(lib.sfft_plan_get_info(self.handle, ctypes.byref(info)))
+        self.r = tuple(r)
+        self.height = int(height)
+        self.s = info.s
+        self.used = tuple(int(info.used[i]) for i in range(info.s))
+        self.level = info.level
+        self.A = int(info.A)
+        self.k = int(info.k)
+        self.n_nodes = int(info.n_nodes)
+        self.mu_star = int(info.mu_star)
+        self.homogeneous = bool(info.homogeneous)
+        self.pivot_mask = int(info.pivot_mask)
+        self._tables = None
+
+    @property
+    def n_slots(self) -> int:
+        return self.A
+
+    def tables(self) -> dict[str, np.ndarray]:
+        """element_slots, slot_residues, slot_real, node_residues, offsets,
+        twiddles -- copied from the device."""
+        if self._tables is None:
+            k, A, n = self.k, self.A, self.n_nodes
+            es = np.empty(k, np.int64)
+            sr = np.empty(A, np.int64)
+            real = np.empty(A, np.uint8)
+            nr = np.empty(max(n, 1), np.int64)
+            off = np.empty(A, np.int64)
+            tw = np.empty(max(A - 1, 1), np.complex64 if self.dtype_code == _lib.C64 else np.complex128)
+            _lib.check(self._lib.sfft_plan_tables(self.handle, es.ctypes.data, sr.ctypes.data,
+                                                  real.ctypes.data, nr.ctypes.data, off.ctypes.data,
+                                                  tw.ctypes.data, _lib.stream_ptr(self.device)))
+            self._tables = {"element_slots": es, "slot_residues": sr, "slot_real": real.astype(bool),
+                            "node_residues": nr[:n], "offsets": off, "twiddles": tw[: A - 1]}
+        return self._tables
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.sfft_plan_destroy(h)
+            except Exception:
+                pass
+            h.value = None
+
+
+def get_plan(J: SupportSet, r: tuple[int, ...], height: int, dtype_code: int, device) -> ButterflyPlan:
+    """Plan cache on the immutable support (SPEC.md:342 allows caching)."""
+    key = (tuple(r), int(height), dtype_code, str(device))
+    plan = J._plans.get(key)
+    if plan is None:
+        plan = ButterflyPlan(J, tuple(r), height, dtype_code, device)
+        J._plans[key] = plan
+    return plan
+
+
+# ---------------------------------------------------------------- sources ---
+
+@dataclass
+class _Src:
+    kind: str               # "device" | "pinned" | "host" | "callable"
+    tensor: Any = None      # 2-D (B, N) view for device/pinned/host
+    batched: bool = False
+    dtype_code: int = _lib.C128
+    device: Any = None
+    fn: Any = None
+
+
+def _prepare_source(source, N: int) -> _Src:
+    torch = _torch()
+    dev = _lib.require_device()
+    if isinstance(source, torch.Tensor):
+        t = source
+        if not t.is_complex():
+            t = t.to(torch.complex128)
+        if t.dtype not in _DT:
+            raise InvalidInputError(f"unsupported signal dtype {t.dtype}")
+        if t.dim() not in (1, 2) or t.shape[-1] != N:
+            raise InvalidInputError("dense signal must be a length-N vector or a (B, N) batch")
+        batched = t.dim() == 2
+        t2 = t if batched else t.unsqueeze(0)
+        if t2.stride(-1) != 1:
+            t2 = t2.contiguous()
+        if t2.is_cuda:
+            return _Src("device", t2, batched, _DT[t2.dtype], t2.device)
+        if t2.is_pinned():
+            return _Src("pinned", t2, batched, _DT[t2.dtype], dev)
+        return _Src("host", t2.to(dev), batched, _DT[t2.dtype], dev)
+    if callable(source) or hasattr(source, "sample_block"):
+        if hasattr(source, "N") and int(getattr(source, "N")) != N:
+            raise InvalidInputError("signal modulus does not match support")
+        fn = source.sample_block if hasattr(source, "sample_block") else source
+        return _Src("callable", None, False, _lib.C128, dev, fn)
+    arr = np.asarray(source)
+    if arr.dtype != np.complex64:
+        arr = np.asarray(arr, dtype=np.complex128)
+    if arr.ndim not in (1, 2) or arr.shape[-1] != N:
+        raise InvalidInputError("dense signal must be a length-N vector or a (B, N) batch")
+    batched = arr.ndim == 2
+    t = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1, N))).to(dev)
+    return _Src("host", t, batched, _DT[t.dtype], dev)
+
+
+def _signal_ptr(src: _Src) -> int:
+    return src.tensor.data_ptr()
+
+
+# ----------------------------------------------------------------- result ---
+
+@dataclass
+class HiDftResult:
+    """Per-node transform values at one height (hidft.py:98-132).
+
+    node_values / slot_values are (n,) for a single signal or (B, n) for a
+    batch; torch CUDA tensors for CUDA sources, numpy otherwise."""
+
+    support: SupportSet
+    pivots: tuple[int, ...]
+    height: int
+    shift: int
+    level: int
+    node_residues: tuple[int, ...]
+    node_values: Any
+    slot_values: Any
+    slot_residues: np.ndarray
+    slot_real: np.ndarray
+    ops_adds: int
+    ops_mults: int
+    plan: ButterflyPlan | None = field(default=None, repr=False)
+    on_device: bool = field(default=False, repr=False)
+
+    def _host(self, x) -> np.ndarray:
+        return x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+
+    @property
+    def values(self) -> dict:
+        vals = self._host(self.node_values)
+        if vals.ndim == 1:
+            return {int(r): complex(v) for r, v in zip(self.node_residues, vals)}
+        return {int(r): vals[:, i] for i, r in enumerate(self.node_residues)}
+
+    def value_at_index(self, j: int):
+        res = int(j) % (1 << self.level)
+        vals = self.values
+        if res not in vals:
+            raise InvalidInputError(f"index {j} belongs to no stored node")
+        return vals[res]
+
+    def _element_nodes(self) -> np.ndarray:
+        res = self.support.as_array() & ((1 << self.level) - 1)
+        return np.searchsorted(np.asarray(self.node_residues, np.int64), res)
+
+    def values_by_index(self):
+        """One value per support element, in support order (hidft.py:127-132)."""
+        idx = self._element_nodes()
+        if self.on_device:
+            torch = _torch()
+            return self.node_values[..., torch.as_tensor(idx, device=self.node_values.device)]
+        return np.asarray(self._host(self.node_values))[..., idx].astype(np.complex128)
+
+
+def _count(counter, A: int, stages: int) -> None:
+    if counter is not None and stages:
+        for _ in range(stages):  # per stage, as hidft.py:165-167
+            counter.mul(A // 2, phase="hidft")
+            counter.add(A, phase="hidft")
+
+
+def _finish(x, src: _Src):
+    """Drop the batch axis for single signals; host sources get numpy."""
+    if not src.batched:
+        x = x[0]
+    if src.kind == "device":
+        return x
+    return x.cpu().numpy()
+
+
+def hidft(source, J, r: Sequence[int], height: int = 0, shift: int = 0, counter=None) -> HiDftResult:
+    """Generalised radix-2 transform of tau^shift f (hidft.py:135-185).
+
+    Output equals F(node representatives, I_{r^{n-}}) applied to the shifted
+    samples, unscaled; exactly 1.5*A*log2(A) complex operations are counted."""
+    torch = _torch()
+    J = as_support(J)
+    rt = validate_pivot_vector(r, J.M)
+    src = _prepare_source(source, J.N)
+    plan = get_plan(J, rt, height, src.dtype_code, src.device)
+    cdt = torch.complex64 if src.dtype_code == _lib.C64 else torch.complex128
+    lib = _lib.load()
+    stream = _lib.stream_ptr(src.device)
+    if src.kind == "callable":
+        off = plan.tables()["offsets"]
+        loc = (off - int(shift)) % J.N
+        vals = np.asarray(src.fn(loc), dtype=np.complex128)
+        if vals.shape != loc.shape:
+            raise InvalidInputError("sample callback returned wrong shape")
+        samples = torch.from_numpy(vals.reshape(1, -1)).to(src.device)
+        B = 1
+        nodes = torch.empty((B, max(plan.n_nodes, 1)), dtype=cdt, device=src.device)
+        slots = torch.empty((B, plan.A), dtype=cdt, device=src.device)
+        _lib.check(lib.sfft_hidft_gathered(plan.handle, samples.data_ptr(), B, plan.A, _lib.OUT_NODES,
+                                           nodes.data_ptr(), nodes.shape[1], slots.data_ptr(), plan.A,
+                                           stream))
+    else:
+        sig = src.tensor
+        B = sig.shape[0]
+        nodes = torch.empty((B, max(plan.n_nodes, 1)), dtype=cdt, device=src.device)
+        slots = torch.empty((B, plan.A), dtype=cdt, device=src.device)
+        _lib.check(lib.sfft_hidft(plan.handle, _signal_ptr(src), B, sig.stride(0), int(shift),
+                                  _lib.OUT_NODES, nodes.data_ptr(), nodes.shape[1], slots.data_ptr(),
+                                  plan.A, stream))
+    nodes = nodes[:, : plan.n_nodes]
+    _count(counter, plan.A, plan.s)
+    tabs = plan.tables()
+    return HiDftResult(
+        support=J, pivots=rt, height=int(height), shift=int(shift), level=plan.level,
+        node_residues=tuple(int(x) for x in tabs["node_residues"]),
+        node_values=_finish(nodes, src), slot_values=_finish(slots, src),
+        slot_residues=tabs["slot_residues"].copy(), slot_real=tabs["slot_real"].copy(),
+        ops_adds=plan.A * plan.s, ops_mults=(plan.A // 2) * plan.s,
+        plan=plan, on_device=src.kind == "device")
+
+
+def hidft_to_dft(res: HiDftResult, counter=None):
+    """(F f)_J from a height-0 transform of a homogeneous support
+    (hidft.py:188-207): node values x N/|J| in ascending-J order."""
+    torch = _torch()
+    J = res.support
+    if not classify(J).is_homogeneous:
+        raise ContractViolationError("hidft_to_dft requires a homogeneous support")
+    if res.height != 0:
+        raise ContractViolationError("hidft_to_dft requires a height-0 transform")
+    plan = res.plan
+    if plan is None:
+        raise InvalidInputError("result was not produced by this package's hidft")
+    slots = res.slot_values
+    host = not torch.is_tensor(slots)
+    if host:
+        slots = torch.from_numpy(np.ascontiguousarray(slots)).to(plan.device)
+    single = slots.dim() == 1
+    s2 = slots.unsqueeze(0) if single else slots
+    s2 = s2.contiguous()
+    out = torch.empty((s2.shape[0], len(J)), dtype=s2.dtype, device=s2.device)
+    _lib.check(_lib.load().sfft_plan_apply_map(plan.handle, _lib.OUT_DFT, s2.data_ptr(), s2.shape[0],
+                                               s2.shape[1], out.data_ptr(), len(J),
+                                               _lib.stream_ptr(plan.device)))
+    if counter is not None and J.N != len(J):
+        counter.mul(len(J), phase="read")
+    if single:
+        out = out[0]
+    return out.cpu().numpy() if host else out
+
+
+def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
+    """Fused hidft(f_b, J_b, pivots(J_b)) + hidft_to_dft for a batch.
+
+    signals: (B, N) complex64/complex128 CUDA tensor, or a page-locked CPU
+    tensor (zero-copy gather; the result is then returned on the host).
+    J: one SupportSet shared by all rows, or a (B, k) int64 tensor with one
+    sorted support per row (config 4).  Per-row statuses land in `status`
+    (int32 device tensor) when given; with check=True a non-homogeneous or
+    invalid support raises like the reference would."""
+    torch = _torch()
+    dev = _lib.require_device()
+    if not torch.is_tensor(signals):
+        signals = torch.from_numpy(np.ascontiguousarray(np.asarray(signals))).to(dev)
+    single = signals.dim() == 1
+    sig = signals.unsqueeze(0) if single else signals
+    if sig.dtype not in (torch.complex64, torch.complex128):
+        raise InvalidInputError("signals must be complex64 or complex128")
+    if sig.stride(-1) != 1:
+        sig = sig.contiguous()
+    B, N = sig.shape
+    M = N.bit_length() - 1
+    if N & (N - 1):
+        raise InvalidInputError(f"N={N} is not a power of two")
+    host_out = not sig.is_cuda
+    if host_out and not sig.is_pinned():
+        sig = sig.to(dev)
+        host_out = True
+    run_dev = sig.device if sig.is_cuda else dev
+    if isinstance(J, (SupportSet,)) or hasattr(J, "indices"):
+        Js = as_support(J)
+        if Js.N != N:
+            raise InvalidInputError("signal modulus does not match support")
+        jt = Js.device_tensor(run_dev)
+        nsup, k = 1, len(Js)
+    else:
+        jt = J if torch.is_tensor(J) else torch.as_tensor(np.asarray(J, dtype=np.int64))
+        if jt.dim() != 2 or jt.shape[0] != B:
+            raise InvalidInputError("per-signal supports must be a (B, k) tensor")
+        jt = jt.to(run_dev, dtype=torch.int64).contiguous()
+        nsup, k = B, jt.shape[1]
+        Js = None
+    code = _DT[sig.dtype]
+    if out is None:
+        out = torch.empty((B, k), dtype=sig.dtype, device=run_dev)
+    st = status
+    if st is None and check:
+        st = torch.zeros(nsup, dtype=torch.int32, device=run_dev)
+    lib = _lib.load()
+    stream = _lib.stream_ptr(run_dev)
+    rc = lib.sfft_hidft_to_dft_fused(jt.data_ptr(), k, nsup, M, sig.data_ptr(), B, sig.stride(0), code,
+                                     out.data_ptr(), out.stride(0),
+                                     st.data_ptr() if st is not None else None, stream)
+    if rc == _lib.ERR_UNSUPPORTED and Js is not None:
+        # 2^s beyond the fused single-CTA size: plan once, then the plan kernel
+        r = classify(Js).pivots
+        if not classify(Js).is_homogeneous:
+            raise ContractViolationError("hidft_to_dft requires a homogeneous support")
+        plan = get_plan(Js, r, 0, code, run_dev)
+        rc = lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_DFT,
+                            out.data_ptr(), out.stride(0), None, 0, stream)
+        _lib.check(rc)
+        if st is not None:
+            st.zero_()
+    else:
+        _lib.check(rc)
+    if check and st is not None:
+        bad = st.cpu().numpy()
+        if (bad == 2).any():
+            raise InvalidInputError(f"support row {int(np.argmax(bad == 2))} is not a valid SupportSet")
+        if (bad == 3).any():
+            raise ContractViolationError(
+                f"hidft_to_dft requires a homogeneous support (row {int(np.argmax(bad == 3))})")
+    res = out[0] if single else out
+    return res.cpu() if host_out else res

@@ -1,0 +1,143 @@
+"""Seeded synthetic workloads for BASELINE.json's five configs (harness only).
+
+Recipe: SURVEY.md 8(d).  Streams follow the reference's generator
+discipline (families.py:35-37, Philox keyed by SeedSequence(seed,
+spawn_key)), and supports use its homogeneous construction
+(families.py:61-80), so the same seed yields the same support as the
+reference (pinned by tests/test_oracle_golden.py::test_config_supports and
+tests/test_workloads.py).  Signals are the inverse DFT of an i.i.d. complex
+Gaussian spectrum on J, synthesised on the GPU in complex128 and cast.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+CONFIGS = {
+    1: dict(M=16, p=8, P_hi=16, B=16, dtype="complex128"),
+    2: dict(M=20, p=10, P_hi=16, B=1024, dtype="complex64"),
+    3: dict(M=22, p=14, P_hi=22, B=512, dtype="complex64", k=4096),
+    4: dict(M=20, p=10, P_hi=16, B=8192, dtype="complex64"),
+    5: dict(M=26, p=16, P_hi=26, B=256, dtype="complex64"),
+    6: dict(M=26, p=16, P_hi=26, B=32, dtype="complex128"),  # config 5's complex128 pass
+}
+
+
+def rng_from_seed(seed: int, *streams: int) -> np.random.Generator:
+    ss = np.random.SeedSequence(entropy=int(seed), spawn_key=tuple(int(s) for s in streams))
+    return np.random.Generator(np.random.Philox(seed=ss))
+
+
+def homogeneous_support(pivs, M: int, seed: int) -> np.ndarray:
+    """{a + sum_i b_i c_i 2^{r_i} mod N}: offset a then one odd multiplier per
+    pivot, drawn in that order from stream (seed, 1)."""
+    N = 1 << M
+    rng = rng_from_seed(seed, 1)
+    a = int(rng.integers(0, N))
+    vals = np.array([a], dtype=np.int64)
+    for ri in pivs:
+        c = 1 + 2 * int(rng.integers(0, max(1 << (M - ri - 1), 1)))
+        vals = np.concatenate([vals, (vals + (c << ri)) % N])
+    return np.unique(vals)
+
+
+def config_support(cfg: int, b: int = 0) -> tuple[np.ndarray, int]:
+    c = 5 if cfg == 6 else cfg
+    spec = CONFIGS[cfg]
+    M = spec["M"]
+    if c in (1, 2, 5):
+        piv = sorted(int(x) for x in rng_from_seed(c, 7).choice(spec["P_hi"], size=spec["p"], replace=False))
+        return homogeneous_support(piv, M, c), M
+    if c == 3:
+        piv = sorted(int(x) for x in rng_from_seed(3, 7).choice(22, size=14, replace=False))
+        H = homogeneous_support(piv, M, 3)
+        pick = np.sort(rng_from_seed(3, 8).choice(1 << 14, size=1 << 12, replace=False))
+        return H[pick], M
+    if c == 4:
+        piv = sorted(int(x) for x in rng_from_seed(4, 9, b).choice(16, size=10, replace=False))
+        seed_b = int(rng_from_seed(4, 10, b).integers(0, 2 ** 62))
+        return homogeneous_support(piv, M, seed_b), M
+    raise ValueError(cfg)
+
+
+def config_pivots(cfg: int, b: int = 0) -> tuple[int, ...]:
+    """The pivot vector the generator planted (config 3: that of H)."""
+    c = 5 if cfg == 6 else cfg
+    if c == 4:
+        return tuple(sorted(int(x) for x in rng_from_seed(4, 9, b).choice(16, size=10, replace=False)))
+    spec = CONFIGS[cfg]
+    return tuple(sorted(int(x) for x in rng_from_seed(c, 7).choice(spec["P_hi"], size=spec["p"], replace=False)))
+
+
+def pattern_of(pivs, M: int) -> np.ndarray:
+    """I_r ascending (sampling.py:47-51), host copy for byte accounting."""
+    vals = np.zeros(1, dtype=np.int64)
+    for ri in pivs:
+        vals = np.concatenate([vals, vals + (1 << (M - 1 - ri))])
+    return np.sort(vals)
+
+
+def config_supports_batch(cfg: int, B: int) -> np.ndarray:
+    """(B, k) per-signal supports (config 4)."""
+    rows = [config_support(cfg, b)[0] for b in range(B)]
+    return np.stack(rows)
+
+
+def coefficients(cfg: int, b: int, k: int) -> np.ndarray:
+    c = 5 if cfg == 6 else cfg
+    rng = rng_from_seed(c, 200, b)
+    return rng.normal(size=k) + 1j * rng.normal(size=k)
+
+
+def synthesize_into(out, supports, coeffs, chunk: int = 16):
+    """out[b] = ifft(zero-padded spectrum_b) computed in complex128 on the
+    device and cast to out.dtype.  supports: (k,) or (B, k) int64 array;
+    coeffs: (B, k) complex128 array.  Harness only (torch.fft)."""
+    import torch
+    B, N = out.shape
+    dev = out.device
+    sup = np.asarray(supports, dtype=np.int64)
+    for s0 in range(0, B, chunk):
+        s1 = min(B, s0 + chunk)
+        spec = torch.zeros((s1 - s0, N), dtype=torch.complex128, device=dev)
+        idx = sup if sup.ndim == 1 else sup[s0:s1]
+        it = torch.as_tensor(idx, device=dev)
+        ct = torch.as_tensor(np.asarray(coeffs[s0:s1]), device=dev)
+        if it.dim() == 1:
+            spec[:, it] = ct
+        else:
+            spec.scatter_(1, it, ct)
+        out[s0:s1] = torch.fft.ifft(spec, dim=1).to(out.dtype)
+        del spec
+    return out
+
+
+@dataclass
+class Workload:
+    cfg: int
+    M: int
+    B: int
+    k: int
+    dtype: str
+    support: np.ndarray          # (k,) shared or (B, k) per-signal
+    coeffs: np.ndarray           # (B, k)
+
+    @property
+    def N(self) -> int:
+        return 1 << self.M
+
+
+def make_workload(cfg: int, B: int | None = None, b0: int = 0) -> Workload:
+    """Config `cfg` restricted to signals [b0, b0+B) (default: the full batch)."""
+    spec = CONFIGS[cfg]
+    B = spec["B"] if B is None else B
+    if cfg == 4:
+        sup = np.stack([config_support(4, b0 + b)[0] for b in range(B)])
+        k = sup.shape[1]
+    else:
+        sup, _ = config_support(cfg)
+        k = sup.size
+    coef = np.stack([coefficients(cfg, b0 + b, k) for b in range(B)])
+    return Workload(cfg, spec["M"], B, k, spec["dtype"], sup, coef)
