@@ -112,7 +112,7 @@ class SupportSet:
         key = str(device)
         t = self._dev.get(key)
         if t is None:
-            t = torch.from_numpy(np.ascontiguousarray(self._arr)).to(device, non_blocking=False)
+            t = torch.from_numpy(self._arr.copy()).to(device, non_blocking=False)
             self._dev[key] = t
         return t
 
@@ -122,6 +122,8 @@ def as_support(J) -> SupportSet:
     reference's SupportSet)."""
     if isinstance(J, SupportSet):
         return J
+    if type(J).__module__.startswith("torch"):
+        raise InvalidInputError("expected a SupportSet, got a tensor")
     if hasattr(J, "N") and hasattr(J, "indices"):
         return SupportSet(J.N, np.asarray(J.indices, dtype=np.int64))
     raise InvalidInputError("expected a SupportSet")

@@ -17,6 +17,8 @@
 // double2) with row stride ld; outputs are rows of n_out complex.
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -37,11 +39,11 @@ struct Geo {
   static constexpr int E = A < EMax<T>::v ? A : EMax<T>::v;  // slots per thread
   static constexpr int LE = ilog2c(E);
   static constexpr int TPS = A / E;                           // threads per signal
-  static constexpr int NT = TPS > 256 ? TPS : 256;            // threads per CTA
+  static constexpr int NT = TPS > 64 ? TPS : 64;              // threads per CTA
   static constexpr int SPC = NT / TPS;                        // signals per CTA
   static constexpr int NPASS = S == 0 ? 1 : (S + LE - 1) / LE;
-  static constexpr int NTAB = S <= 8 ? 1 : (S + 7) / 8;       // offset tables
-  static constexpr int TABW = S < 8 ? A : 256;                // entries per table
+  // occupancy hint: >= 16 resident warps per SM where the register file allows
+  static constexpr int MINB = NT >= 1024 ? 1 : (512 / NT > 1 ? 512 / NT : 1);
 };
 
 // Bank-conflict-free shared-memory slot position: XOR the low SWZ bits with
@@ -110,35 +112,26 @@ __device__ __forceinline__ void butterfly(Cx<T> (&v)[Geo<T, S>::E], int t, Cx<T>
   }
 }
 
-// Pass-0 gather: slot a = x + t*E reads sample (off(a) - shift) mod N.
+// Pass-0 gather: slot a = x + t*E reads sample (off(a) + base) mod N with
+// off(a) = sum_i bit_i(a) d_i, d_i = 2^(M-1-used_i) (hidft.py:155-158).  The
+// low LE bits of a come from the unrolled register index x, so their part
+// of the offset is a compile-time selection of d_0..d_{LE-1}.  All E loads
+// are issued back to back before any use.
 template <typename T, int S>
-__device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S>::E], int t, const Cx<T>* row,
-                                       const int* tab, uint32_t negshift, uint32_t nmask) {
+__device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S>::E], int t, const Cx<T>* __restrict__ row,
+                                       const uint32_t (&d)[S > 0 ? S : 1], uint32_t base, uint32_t nmask) {
   using G = Geo<T, S>;
-  uint32_t idx[G::E];
+  uint32_t hi = base;
+#pragma unroll
+  for (int i = G::LE; i < S; ++i)
+    if ((t >> (i - G::LE)) & 1) hi += d[i];
 #pragma unroll
   for (int x = 0; x < G::E; ++x) {
-    const int a = x + t * G::E;
-    uint32_t off = (uint32_t)tab[a & (G::TABW - 1)];
-    if (G::NTAB > 1) off += (uint32_t)tab[256 + ((a >> 8) & 255)];
-    if (G::NTAB > 2) off += (uint32_t)tab[512 + ((a >> 16) & 255)];
-    idx[x] = (off + negshift) & nmask;
-  }
+    uint32_t off = hi;
 #pragma unroll
-  for (int x = 0; x < G::E; ++x) v[x] = load_sample(row + idx[x]);
-}
-
-// offset tables: tab[q][v] = sum over bits b of v of 2^(M-1-piv[8q+b])
-__device__ __forceinline__ void build_offset_tables(int* tab, int ntab, int tabw, const int* piv, int s,
-                                                    int M, int tid, int nthr) {
-  for (int i = tid; i < ntab * tabw; i += nthr) {
-    const int q = i / tabw, v = i % tabw;
-    uint32_t off = 0;
-    for (int b = 0; b < 8; ++b) {
-      const int pi = 8 * q + b;
-      if (pi < s && ((v >> b) & 1)) off += 1u << (M - 1 - piv[pi]);
-    }
-    tab[i] = (int)off;
+    for (int i = 0; i < G::LE; ++i)
+      if ((x >> i) & 1) off += d[i];
+    v[x] = load_sample(row + (off & nmask));
   }
 }
 
@@ -150,7 +143,7 @@ struct PlanArgs {
   int M;
   uint32_t negshift;
   int32_t used[32];
-  const void* tw;
+  const void* tw;       // A-1 twiddles in HBM, read through L1 (shared by all CTAs of an SM)
   const int32_t* map1;  // NULL => identity
   int64_t n1;
   double scale1;
@@ -161,71 +154,49 @@ struct PlanArgs {
   int identity;  // samples already gathered in slot order (row[a] = slot a)
 };
 
-template <typename T, int S> constexpr bool plan_tw_in_smem() {
-  return (size_t)(Geo<T, S>::SPC + 1) * Geo<T, S>::A * sizeof(Cx<T>) <= 160 * 1024;
-}
 template <typename T, int S> constexpr size_t plan_smem() {
-  using G = Geo<T, S>;
-  return (size_t)G::SPC * G::A * sizeof(Cx<T>) +
-         (plan_tw_in_smem<T, S>() ? (size_t)(G::A > 1 ? G::A - 1 : 1) * sizeof(Cx<T>) : 0) +
-         (size_t)G::NTAB * G::TABW * sizeof(int);
+  return (size_t)Geo<T, S>::SPC * Geo<T, S>::A * sizeof(Cx<T>);
 }
 
+// One CTA per SPC signals, no per-CTA setup: the gather is the first thing
+// every thread does, the butterfly reads the plan's twiddles through L1,
+// and the block scheduler balances the grid over the 148 SMs.
 template <typename T, int S>
-__global__ void __launch_bounds__(Geo<T, S>::NT)
+__global__ void __launch_bounds__(Geo<T, S>::NT, Geo<T, S>::MINB)
 k_hidft_plan(const PlanArgs args) {
   using G = Geo<T, S>;
-  constexpr bool TWS = plan_tw_in_smem<T, S>();  // twiddles staged in smem, else read via L1/L2
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);
-  Cx<T>* stw = sdata + G::SPC * G::A;
-  int* stab = reinterpret_cast<int*>(stw + (TWS ? (G::A > 1 ? G::A - 1 : 1) : 0));
-  __shared__ int spiv[32];
-
   const int tid = threadIdx.x;
   const int g = tid / G::TPS, t = tid % G::TPS;
-  if (tid < 32) spiv[tid] = args.used[tid];
-  const Cx<T>* gtw = reinterpret_cast<const Cx<T>*>(args.tw);
-  if (TWS)
-    for (int i = tid; i < G::A - 1; i += G::NT) stw[i] = gtw[i];
-  const Cx<T>* tw = TWS ? stw : gtw;
-  __syncthreads();
-  if (args.identity) {  // off(a) = a: table q maps v -> v << 8q
-    for (int i = tid; i < G::NTAB * G::TABW; i += G::NT) stab[i] = (i % G::TABW) << (8 * (i / G::TABW));
-  } else {
-    build_offset_tables(stab, G::NTAB, G::TABW, spiv, S, args.M, tid, G::NT);
-  }
-  __syncthreads();
-
+  const int64_t b = (int64_t)blockIdx.x * G::SPC + g;
+  const bool live = b < args.B;
+  uint32_t d[S > 0 ? S : 1];
+#pragma unroll
+  for (int i = 0; i < S; ++i) d[i] = args.identity ? (1u << i) : (1u << (args.M - 1 - args.used[i]));
   const uint32_t nmask = args.identity ? (uint32_t)(G::A - 1)
                                         : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
-  const int64_t ngroups = (args.B + G::SPC - 1) / G::SPC;
-  const T scale = (T)args.scale1;
-  Cx<T>* sd = sdata + g * G::A;
-  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int64_t b = grp * G::SPC + g;
-    const bool live = b < args.B;
-    Cx<T> v[G::E];
-    if (live) {
-      const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
-      gather<T, S>(v, t, row, stab, args.negshift, nmask);
-    } else {
+  Cx<T> v[G::E];
+  if (live) {
+    const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
+    gather<T, S>(v, t, row, d, args.identity ? 0u : args.negshift, nmask);
+  } else {
 #pragma unroll
-      for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
+    for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
+  }
+  Cx<T>* sd = sdata + g * G::A;
+  butterfly<T, S>(v, t, sd, reinterpret_cast<const Cx<T>*>(args.tw));
+  if (live) {
+    const T scale = (T)args.scale1;
+    Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
+    for (int64_t i = t; i < args.n1; i += G::TPS) {
+      const int a = args.map1 ? __ldg(args.map1 + i) : (int)i;
+      o1[i] = cscale(sd[swz<T, S>(a)], scale);
     }
-    butterfly<T, S>(v, t, sd, tw);
-    if (live) {
-      Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
-      for (int64_t i = t; i < args.n1; i += G::TPS) {
-        const int a = args.map1 ? args.map1[i] : (int)i;
-        o1[i] = cscale(sd[swz<T, S>(a)], scale);
-      }
-      if (args.out2) {
-        Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2;
-        for (int i = t; i < G::A; i += G::TPS) o2[i] = sd[swz<T, S>(i)];
-      }
+    if (args.out2) {
+      Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2;
+      for (int i = t; i < G::A; i += G::TPS) o2[i] = sd[swz<T, S>(i)];
     }
-    __syncthreads();
   }
 }
 
@@ -255,11 +226,11 @@ struct FusedArgs {
 // Plan for one support on `nthr` threads (tid in [0, nthr)).  Every thread
 // of the CTA must call it at the same time (it uses CTA barriers); several
 // thread groups may build several plans concurrently.  Writes spats
-// (element -> slot), stw (A-1 twiddles) and stab (offset tables).
+// (element -> slot), stw (A-1 twiddles) and the pivots (sctl + 2).
 // scratch: 2*A ints.  Returns 0 ok, 2 invalid support, 3 not homogeneous.
 template <typename T, int S>
 __device__ int fused_plan(const int64_t* __restrict__ Jrow, bool live, int M, int tid, int nthr,
-                          int* spats, Cx<T>* stw, int* stab, int* scratch, int* sctl) {
+                          int* spats, Cx<T>* stw, int* scratch, int* sctl) {
   using G = Geo<T, S>;
   constexpr int A = G::A;
   int* sJ = scratch;
@@ -293,7 +264,8 @@ __device__ int fused_plan(const int64_t* __restrict__ Jrow, bool live, int M, in
   __syncthreads();
   mask = (uint32_t)sctl[0];
   const bool go = live && sctl[1] == 0 && __popc(mask) == S;
-  if (go && tid < S) spiv[tid] = (int)__fns(mask, 0, tid + 1);
+  if (go)
+    for (int i = tid; i < S; i += nthr) spiv[i] = (int)__fns(mask, 0, i + 1);
   __syncthreads();
   int piv[S > 0 ? S : 1];
   if (go) {
@@ -315,18 +287,17 @@ __device__ int fused_plan(const int64_t* __restrict__ Jrow, bool live, int M, in
       if (sElem[spats[e]] != sJ[e]) bad = 3;  // two elements share a pattern
     for (int x = tid + 1; x < A; x += nthr) {
       const int top = 31 - __clz(x);
-      const uint32_t d = (uint32_t)(sElem[x] ^ sElem[x ^ (1 << top)]);
-      if (d == 0 || __ffs(d) - 1 != piv[top]) bad = 3;  // v2 outside P0
+      const uint32_t dd = (uint32_t)(sElem[x] ^ sElem[x ^ (1 << top)]);
+      if (dd == 0 || __ffs(dd) - 1 != spiv[top]) bad = 3;  // v2 outside P0
     }
     if (bad) atomicMax(&sctl[1], bad);
     for (int idx = tid; idx < A - 1; idx += nthr) {
       const int beta = 31 - __clz(idx + 1);
       const int h = idx + 1 - (1 << beta);
-      const int rk = piv[beta];
+      const int rk = spiv[beta];
       const uint32_t shared = (uint32_t)sElem[h] & ((1u << rk) - 1u);
       stw[idx] = twiddle<T>(shared, rk);
     }
-    build_offset_tables(stab, G::NTAB, G::TABW, spiv, S, M, tid, nthr);
   }
   __syncthreads();
   if (!live) return 0;
@@ -334,54 +305,65 @@ __device__ int fused_plan(const int64_t* __restrict__ Jrow, bool live, int M, in
   return __popc(mask) == S ? 0 : 3;
 }
 
+template <typename T, int S, bool PS> constexpr size_t fused_smem() {
+  using G = Geo<T, S>;
+  constexpr size_t NP = PS ? G::SPC : 1;
+  return (size_t)G::SPC * G::A * sizeof(Cx<T>) + NP * (G::A > 1 ? G::A - 1 : 1) * sizeof(Cx<T>) +
+         NP * G::A * sizeof(int);
+}
+
+// PER_SIGNAL: one CTA per SPC signals, each group derives its own support's
+// plan on chip, then gathers, transforms and stores.  Shared support: CTAs
+// are persistent, build the one plan once and loop over signal groups.
 template <typename T, int S, bool PER_SIGNAL>
-__global__ void __launch_bounds__(Geo<T, S>::NT)
+__global__ void __launch_bounds__(Geo<T, S>::NT, Geo<T, S>::MINB)
 k_fused_to_dft(const FusedArgs args) {
   using G = Geo<T, S>;
   constexpr int A = G::A;
   constexpr int NP = PER_SIGNAL ? G::SPC : 1;  // plans held per CTA
   constexpr int TWN = A > 1 ? A - 1 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);          // SPC * A
-  Cx<T>* stw_all = sdata + G::SPC * A;                        // NP * TWN
+  Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);            // SPC * A
+  Cx<T>* stw_all = sdata + G::SPC * A;                          // NP * TWN
   int* spats_all = reinterpret_cast<int*>(stw_all + NP * TWN);  // NP * A
-  int* stab_all = spats_all + NP * A;                         // NP * NTAB*TABW
   __shared__ int sctl[NP][2 + (S > 0 ? S : 1)];
 
   const int tid = threadIdx.x;
   const int g = tid / G::TPS, t = tid % G::TPS;
   const uint32_t nmask = (args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u);
   const T scale = (T)((double)(1ll << args.M) / (double)A);
-  const int64_t ngroups = (args.B + G::SPC - 1) / G::SPC;
   Cx<T>* sd = sdata + g * A;
   const int pg = PER_SIGNAL ? g : 0;
   int* pats = spats_all + pg * A;
   Cx<T>* tw = stw_all + pg * TWN;
-  int* tab = stab_all + pg * G::NTAB * G::TABW;
+  const int* spiv = &sctl[pg][2];
 
+  int64_t grp = blockIdx.x, step = gridDim.x;
+  const int64_t ngroups = (args.B + G::SPC - 1) / G::SPC;
   if (!PER_SIGNAL) {
     // one plan per CTA, built by all its threads; scratch aliases the data area
-    const int st = fused_plan<T, S>(args.J, true, args.M, tid, G::NT, pats, tw, tab,
+    const int st = fused_plan<T, S>(args.J, true, args.M, tid, G::NT, pats, tw,
                                     reinterpret_cast<int*>(sdata), &sctl[0][0]);
     if (blockIdx.x == 0 && tid == 0 && args.status) args.status[0] = st;
     if (st != 0) return;  // uniform across the CTA
   }
-
-  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  for (; grp < ngroups; grp += step) {
     const int64_t b = grp * G::SPC + g;
     const bool live = b < args.B;
     int st = 0;
     if (PER_SIGNAL) {
-      // every group builds the plan of its own signal's support, concurrently
-      st = fused_plan<T, S>(args.J + (live ? b : 0) * (int64_t)A, live, args.M, t, G::TPS,
-                            pats, tw, tab, reinterpret_cast<int*>(sd), &sctl[g][0]);
+      st = fused_plan<T, S>(args.J + (live ? b : 0) * (int64_t)A, live, args.M, t, G::TPS, pats, tw,
+                            reinterpret_cast<int*>(sd), &sctl[g][0]);
       if (live && t == 0 && args.status) args.status[b] = st;
     }
     const bool ok = live && st == 0;
     Cx<T> v[G::E];
     if (ok) {
+      uint32_t d[S > 0 ? S : 1];
+#pragma unroll
+      for (int i = 0; i < S; ++i) d[i] = 1u << (args.M - 1 - spiv[i]);
       const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
-      gather<T, S>(v, t, row, tab, 0u, nmask);
+      gather<T, S>(v, t, row, d, 0u, nmask);
     } else {
 #pragma unroll
       for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
@@ -397,22 +379,31 @@ k_fused_to_dft(const FusedArgs args) {
 
 // ------------------------------------------------------------ launchers ---
 
-template <typename T, int S, bool PS> constexpr size_t fused_smem() {
-  using G = Geo<T, S>;
-  constexpr size_t NP = PS ? G::SPC : 1;
-  return (size_t)G::SPC * G::A * sizeof(Cx<T>) + NP * (G::A > 1 ? G::A - 1 : 1) * sizeof(Cx<T>) +
-         NP * G::A * sizeof(int) + NP * G::NTAB * G::TABW * sizeof(int);
-}
+// Per (kernel, device): opt in to the full dynamic shared memory and cache
+// the occupancy (resident CTAs per SM).
+static std::mutex g_kmu;
+static std::map<std::pair<const void*, int>, int> g_occ;
 
 template <typename K>
-static int prep_grid(K kernel, int nt, size_t smem, int64_t ngroups, int* grid) {
-  if (smem > 48 * 1024)
-    SFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  SFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, smem));
-  if (occ < 1) return fail(SFFT_ERR_UNSUPPORTED, "kernel does not fit on an SM");
-  const int64_t cap = (int64_t)num_sms() * occ;
-  *grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, ngroups));
+static int kernel_occupancy(K kernel, int nt, size_t smem, int* occ) {
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  {
+    std::lock_guard<std::mutex> lk(g_kmu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) {
+      *occ = it->second;
+      return SFFT_OK;
+    }
+  }
+  SFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int o = 0;
+  SFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, nt, smem));
+  if (o < 1) return fail(SFFT_ERR_UNSUPPORTED, "kernel does not fit on an SM");
+  std::lock_guard<std::mutex> lk(g_kmu);
+  g_occ[key] = o;
+  *occ = o;
   return SFFT_OK;
 }
 
@@ -422,11 +413,12 @@ static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {
   constexpr size_t smem = plan_smem<T, S>();
   static_assert(smem <= 227 * 1024, "plan kernel smem");
   auto kern = k_hidft_plan<T, S>;
-  int grid = 0;
-  const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
-  int rc = prep_grid(kern, G::NT, smem, ngroups, &grid);
+  int occ = 0;
+  int rc = kernel_occupancy(kern, G::NT, smem, &occ);
   if (rc) return rc;
-  kern<<<grid, G::NT, smem, st>>>(a);
+  const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
+  if (ngroups > 0x7fffffff) return fail(SFFT_ERR_UNSUPPORTED, "batch too large for one launch");
+  kern<<<(unsigned)ngroups, G::NT, smem, st>>>(a);
   SFFT_CUDA(cudaGetLastError());
   return SFFT_OK;
 }
@@ -437,11 +429,13 @@ static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
   constexpr size_t smem = fused_smem<T, S, PS>();
   static_assert(smem <= 227 * 1024, "fused kernel smem");
   auto kern = k_fused_to_dft<T, S, PS>;
-  int grid = 0;
-  const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
-  int rc = prep_grid(kern, G::NT, smem, ngroups, &grid);
+  int occ = 0;
+  int rc = kernel_occupancy(kern, G::NT, smem, &occ);
   if (rc) return rc;
-  kern<<<grid, G::NT, smem, st>>>(a);
+  const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
+  int64_t grid = PS ? ngroups : std::min<int64_t>(ngroups, (int64_t)num_sms() * occ);
+  if (grid > 0x7fffffff) return fail(SFFT_ERR_UNSUPPORTED, "batch too large for one launch");
+  kern<<<(unsigned)std::max<int64_t>(grid, 1), G::NT, smem, st>>>(a);
   SFFT_CUDA(cudaGetLastError());
   return SFFT_OK;
 }

@@ -342,7 +342,7 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         sig = sig.to(dev)
         host_out = True
     run_dev = sig.device if sig.is_cuda else dev
-    if isinstance(J, (SupportSet,)) or hasattr(J, "indices"):
+    if not torch.is_tensor(J) and (isinstance(J, SupportSet) or hasattr(J, "indices")):
         Js = as_support(J)
         if Js.N != N:
             raise InvalidInputError("signal modulus does not match support")
@@ -358,27 +358,27 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
     code = _DT[sig.dtype]
     if out is None:
         out = torch.empty((B, k), dtype=sig.dtype, device=run_dev)
-    st = status
-    if st is None and check:
-        st = torch.zeros(nsup, dtype=torch.int32, device=run_dev)
     lib = _lib.load()
     stream = _lib.stream_ptr(run_dev)
-    rc = lib.sfft_hidft_to_dft_fused(jt.data_ptr(), k, nsup, M, sig.data_ptr(), B, sig.stride(0), code,
-                                     out.data_ptr(), out.stride(0),
-                                     st.data_ptr() if st is not None else None, stream)
-    if rc == _lib.ERR_UNSUPPORTED and Js is not None:
-        # 2^s beyond the fused single-CTA size: plan once, then the plan kernel
-        r = classify(Js).pivots
-        if not classify(Js).is_homogeneous:
+    st = status
+    if Js is not None:
+        # shared support: plan once (cached on J), then one gather+butterfly
+        # launch per batch with the plan's tables read through L1
+        cls = classify(Js)
+        if not cls.is_homogeneous:
             raise ContractViolationError("hidft_to_dft requires a homogeneous support")
-        plan = get_plan(Js, r, 0, code, run_dev)
-        rc = lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_DFT,
-                            out.data_ptr(), out.stride(0), None, 0, stream)
-        _lib.check(rc)
+        plan = get_plan(Js, cls.pivots, 0, code, run_dev)
+        _lib.check(lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_DFT,
+                                  out.data_ptr(), out.stride(0), None, 0, stream))
         if st is not None:
             st.zero_()
-    else:
-        _lib.check(rc)
+        res = out[0] if single else out
+        return res.cpu() if host_out else res
+    if st is None and check:
+        st = torch.zeros(nsup, dtype=torch.int32, device=run_dev)
+    _lib.check(lib.sfft_hidft_to_dft_fused(jt.data_ptr(), k, nsup, M, sig.data_ptr(), B, sig.stride(0),
+                                           code, out.data_ptr(), out.stride(0),
+                                           st.data_ptr() if st is not None else None, stream))
     if check and st is not None:
         bad = st.cpu().numpy()
         if (bad == 2).any():

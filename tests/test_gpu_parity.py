@@ -179,7 +179,7 @@ def test_contract_errors(S):
         S.hidft(f, J, (3, 1))
     with pytest.raises(S.ContractViolationError):  # tests/test_hidft.py:141-145
         S.hidft_to_dft(S.hidft(f, J, (1, 3)))
-    res = S.hidft(f, S.SupportSet.make(32, [3, 17, 25, 27]), (1, 3), height=1)
+    res = S.hidft(np.zeros(32, complex), S.SupportSet.make(32, [3, 17, 25, 27]), (1, 3), height=1)
     with pytest.raises(S.ContractViolationError):
         S.hidft_to_dft(res)
     with pytest.raises(S.InvalidInputError):
