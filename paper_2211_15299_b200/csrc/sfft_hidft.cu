@@ -22,8 +22,12 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "sfft_common.cuh"
 #include "sfft_plan.h"
+
+namespace cg = cooperative_groups;
 
 namespace sfft {
 
@@ -198,6 +202,106 @@ k_hidft_plan(const PlanArgs args) {
       for (int i = t; i < G::A; i += G::TPS) o2[i] = sd[swz<T, S>(i)];
     }
   }
+}
+
+// ------------------------------------------ cluster kernel for large A ---
+//
+// 2^s slots beyond one SM's shared memory (config 5: A = 65536) are spread
+// over a thread-block cluster of C CTAs; CTA q owns the slots whose top
+// log2(C) bits equal q (so stages 1..s-log2(C) are CTA-local).
+//  0. gather: CTA q loads the q-th contiguous chunk of the SORTED sample set
+//     I_r (coalesced whenever the pattern has contiguous runs), and stores
+//     each sample straight into its owner CTA's shared memory over DSMEM
+//     (sorted index qs holds slot brev_s(qs)).
+//  1. every CTA runs the local stages on its slice (the single-CTA code).
+//  2. the last log2(C) stages: each CTA takes 1/C of the local indices,
+//     reads the C partners of each from the C slices over DSMEM, finishes
+//     the butterfly in registers and stores straight to the output row
+//     through the plan's slot -> output-position map.
+template <typename T, int S, int C>
+__global__ void __launch_bounds__(Geo<T, S - ilog2c(C)>::NT, 1)
+k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
+  constexpr int LC = ilog2c(C), SL = S - LC, AL = 1 << SL;
+  using G = Geo<T, SL>;
+  static_assert(G::SPC == 1, "one signal slice per CTA");
+  constexpr int NT = G::NT, LNT = ilog2c(NT);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* sd = reinterpret_cast<Cx<T>*>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = (int)cluster.block_rank();
+  const int64_t b = blockIdx.x / C;
+  const int t = threadIdx.x;
+  const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(args.tw);
+  uint32_t d[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) d[i] = 1u << (args.M - 1 - args.used[i]);
+  const uint32_t nmask = (args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u);
+  const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
+
+  // 0. coalesced gather of sorted positions qs = q*AL + x*NT + t
+  uint32_t offt = args.negshift;
+#pragma unroll
+  for (int j = 0; j < LNT; ++j)
+    if ((t >> j) & 1) offt += d[S - 1 - j];
+#pragma unroll
+  for (int j = 0; j < LC; ++j)
+    if ((q >> j) & 1) offt += d[S - 1 - (SL + j)];
+  Cx<T> v[G::E];
+#pragma unroll
+  for (int x = 0; x < G::E; ++x) {
+    uint32_t off = offt;
+#pragma unroll
+    for (int j = 0; j < G::LE; ++j)
+      if ((x >> j) & 1) off += d[S - 1 - (LNT + j)];
+    v[x] = load_sample(row + (off & nmask));
+  }
+#pragma unroll
+  for (int x = 0; x < G::E; ++x) {
+    const uint32_t qs = (uint32_t)(q * AL + x * NT + t);
+    const uint32_t a = __brev(qs) >> (32 - S);
+    Cx<T>* dst = cluster.map_shared_rank(sd, (int)(a >> SL));
+    dst[swz<T, SL>((int)(a & (AL - 1)))] = v[x];
+  }
+  cluster.sync();
+
+  // 1. local stages 1..SL
+#pragma unroll
+  for (int x = 0; x < G::E; ++x) v[x] = sd[swz<T, SL>(slot_of<SL, G::LE>(0, t, x))];
+  butterfly<T, SL>(v, t, sd, tw);
+  cluster.sync();
+
+  // 2. stages SL+1..S across the cluster
+  constexpr int PER = AL / C;
+  const T scale = (T)args.scale1;
+  Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
+  Cx<T>* o2 = args.out2 ? reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2 : nullptr;
+  for (int i = t; i < PER; i += NT) {
+    const int al = q * PER + i;
+    Cx<T> w[C];
+#pragma unroll
+    for (int x = 0; x < C; ++x) w[x] = cluster.map_shared_rank(sd, x)[swz<T, SL>(al)];
+#pragma unroll
+    for (int j = 0; j < LC; ++j) {
+      const int beta = SL + j;
+#pragma unroll
+      for (int x = 0; x < C; ++x) {
+        if (x & (1 << j)) continue;
+        const int h = al + ((x & ((1 << j) - 1)) << SL);
+        const Cx<T> u = w[x];
+        const Cx<T> z = cmul(tw[(1 << beta) - 1 + h], w[x | (1 << j)]);
+        w[x] = csub(u, z);
+        w[x | (1 << j)] = cadd(u, z);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < C; ++x) {
+      const int a = al + x * AL;
+      const int pos = inv1 ? __ldg(inv1 + a) : a;
+      if (pos >= 0) o1[pos] = cscale(w[x], scale);
+      if (o2) o2[a] = w[x];
+    }
+  }
+  cluster.sync();  // keep every slice alive until all remote reads are done
 }
 
 // -------------------------------------------- fused homogeneous to_dft ---
@@ -440,11 +544,48 @@ static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
   return SFFT_OK;
 }
 
+template <typename T, int S, int C>
+static int run_cluster_kernel(const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
+  constexpr int SL = S - ilog2c(C);
+  using G = Geo<T, SL>;
+  constexpr size_t smem = (size_t)G::A * sizeof(Cx<T>);
+  auto kern = k_hidft_cluster<T, S, C>;
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(g_kmu);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+    if (!g_occ.count(key)) {
+      SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (C > 8) SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      g_occ[key] = 1;
+    }
+  }
+  if (a.B * C > 0x7fffffffll) return fail(SFFT_ERR_UNSUPPORTED, "batch too large for one launch");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.B * C));
+  cfg.blockDim = dim3(G::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, a, inv1));
+  return SFFT_OK;
+}
+
 // largest s handled on one CTA (data for one signal resident in shared memory)
 constexpr int kMaxPlanS_c64 = 14, kMaxPlanS_c128 = 13;
 constexpr int kMaxFusedS_c64 = 13, kMaxFusedS_c128 = 12;
 
-int max_supported_s(int dtype) { return dtype == SFFT_C64 ? kMaxPlanS_c64 : kMaxPlanS_c128; }
+// cluster path: slices of 2^13 (c64) / 2^12 (c128) slots, C = 4..16 CTAs
+constexpr int kMaxClusterS_c64 = 17, kMaxClusterS_c128 = 16;
+
+int max_supported_s(int dtype) { return dtype == SFFT_C64 ? kMaxClusterS_c64 : kMaxClusterS_c128; }
 
 #define SFFT_CASES_12(M_, ...) \
   M_(0, __VA_ARGS__) M_(1, __VA_ARGS__) M_(2, __VA_ARGS__) M_(3, __VA_ARGS__) M_(4, __VA_ARGS__) \
@@ -454,18 +595,24 @@ int max_supported_s(int dtype) { return dtype == SFFT_C64 ? kMaxPlanS_c64 : kMax
 #define PLAN_CASE(S_, T_) case S_: return run_plan_kernel<T_, S_>(a, st);
 #define FUSED_CASE(S_, T_, PS_) case S_: return run_fused_kernel<T_, S_, PS_>(a, st);
 
-static int dispatch_plan(int dtype, int s, const PlanArgs& a, cudaStream_t st) {
+static int dispatch_plan(int dtype, int s, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
   if (dtype == SFFT_C64) {
     switch (s) {
       SFFT_CASES_12(PLAN_CASE, float)
       PLAN_CASE(13, float)
       PLAN_CASE(14, float)
+      case 15: return run_cluster_kernel<float, 15, 4>(a, inv1, st);
+      case 16: return run_cluster_kernel<float, 16, 8>(a, inv1, st);
+      case 17: return run_cluster_kernel<float, 17, 16>(a, inv1, st);
       default: break;
     }
   } else {
     switch (s) {
       SFFT_CASES_12(PLAN_CASE, double)
       PLAN_CASE(13, double)
+      case 14: return run_cluster_kernel<double, 14, 4>(a, inv1, st);
+      case 15: return run_cluster_kernel<double, 15, 8>(a, inv1, st);
+      case 16: return run_cluster_kernel<double, 16, 16>(a, inv1, st);
       default: break;
     }
   }
@@ -492,8 +639,8 @@ static int dispatch_fused(int dtype, int s, const FusedArgs& a, cudaStream_t st)
 }
 
 int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld, int64_t shift,
-                      const int32_t* map1, int64_t n1, double scale1, void* out1, int64_t ld1,
-                      void* out2, int64_t ld2, int identity, cudaStream_t st) {
+                      const int32_t* map1, const int32_t* inv1, int64_t n1, double scale1, void* out1,
+                      int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st) {
   PlanArgs a{};
   a.identity = identity;
   a.sig = sig;
@@ -512,7 +659,9 @@ int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld
   a.ld1 = ld1;
   a.out2 = out2;
   a.ld2 = ld2;
-  return dispatch_plan(p->dtype, p->s, a, st);
+  if (identity && p->s > (p->dtype == SFFT_C64 ? kMaxPlanS_c64 : kMaxPlanS_c128))
+    return fail(SFFT_ERR_UNSUPPORTED, "pre-gathered samples need 2^s within one CTA");
+  return dispatch_plan(p->dtype, p->s, a, inv1, st);
 }
 
 template <typename T>
@@ -529,11 +678,15 @@ __global__ void k_apply_map(const Cx<T>* __restrict__ in, int64_t B, int64_t ld_
 
 // resolve (map, n_out, scale) for an output kind, checking its contract
 static int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, int64_t* n_out,
-                    double* scale) {
+                    double* scale, const int32_t** inv = nullptr) {
   const double N = (double)(1ll << plan->M);
   *scale = 1.0;
+  const int32_t* dummy;
+  if (!inv) inv = &dummy;
+  *inv = nullptr;
   switch (out_kind) {
     case SFFT_OUT_NODES:
+      *inv = plan->d_inv_node;
       *map = plan->d_node_slots;
       *n_out = plan->n_nodes;
       return SFFT_OK;
@@ -547,6 +700,7 @@ static int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, in
       if (plan->height != 0)
         return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a height-0 transform");
       *map = plan->d_element_slots;
+      *inv = plan->d_inv_elem;
       *n_out = plan->k;
       *scale = N / (double)plan->k;
       return SFFT_OK;
@@ -555,6 +709,7 @@ static int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, in
         return fail(SFFT_ERR_CONTRACT, "mu* > 1: node systems need Vandermonde decoding");
       if (plan->height != 0) return fail(SFFT_ERR_CONTRACT, "sas decode needs height 0");
       *map = plan->d_element_slots;
+      *inv = plan->d_inv_elem;
       *n_out = plan->k;
       *scale = N / (double)plan->A;
       return SFFT_OK;
@@ -574,9 +729,10 @@ static int hidft_common(const sfft_plan* plan, const void* signals, int64_t B, i
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   if (B < 0) return fail(SFFT_ERR_INVALID, "negative batch");
   const int32_t* map = nullptr;
+  const int32_t* inv = nullptr;
   int64_t n_out = 0;
   double scale = 1.0;
-  int rc = out_spec(plan, out_kind, &map, &n_out, &scale);
+  int rc = out_spec(plan, out_kind, &map, &n_out, &scale, &inv);
   if (rc) return rc;
   if (B == 0) return SFFT_OK;
   if (!signals || !out) return fail(SFFT_ERR_INVALID, "null signal or output pointer");
@@ -586,7 +742,7 @@ static int hidft_common(const sfft_plan* plan, const void* signals, int64_t B, i
   int dev = 0;
   SFFT_CUDA(cudaGetDevice(&dev));
   if (dev != plan->device) return fail(SFFT_ERR_INVALID, "plan belongs to another device");
-  return launch_hidft_plan(plan, signals, B, ld, shift, map, n_out, scale, out, ld_out, slot_out,
+  return launch_hidft_plan(plan, signals, B, ld, shift, map, inv, n_out, scale, out, ld_out, slot_out,
                            ld_slot, identity, st);
 }
 

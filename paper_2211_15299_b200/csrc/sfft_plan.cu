@@ -270,7 +270,7 @@ static int analyze_device(const int64_t* dJ, int64_t k, int M, uint64_t* mask_ou
 // --------------------------------------------------------- plan kernels ---
 __global__ void k_plan_elements(const int64_t* __restrict__ J, int64_t k, const int32_t* __restrict__ used,
                                 int s, int32_t* __restrict__ pats, uint32_t* __restrict__ count,
-                                uint32_t* __restrict__ mins) {
+                                uint32_t* __restrict__ mins, int32_t* __restrict__ inv_elem) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k;
        e += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t j = (uint32_t)J[e];
@@ -279,6 +279,7 @@ __global__ void k_plan_elements(const int64_t* __restrict__ J, int64_t k, const 
     pats[e] = (int32_t)p;
     atomicAdd(&count[p], 1u);
     atomicMin(&mins[p], j);
+    atomicMax(&inv_elem[p], (int32_t)e);  // the one member when mu* = 1
   }
 }
 
@@ -347,7 +348,8 @@ __global__ void k_plan_slots(const uint32_t* __restrict__ reps_s, const uint32_t
 __global__ void k_node_order(const int32_t* __restrict__ slot_res, const uint8_t* __restrict__ slot_real,
                              int64_t A, const uint32_t* __restrict__ bitmap,
                              const uint32_t* __restrict__ wprefix, const uint32_t* __restrict__ bprefix,
-                             int32_t* __restrict__ node_slots, int32_t* __restrict__ node_res) {
+                             int32_t* __restrict__ node_slots, int32_t* __restrict__ node_res,
+                             int32_t* __restrict__ inv_node) {
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A;
        x += (int64_t)gridDim.x * blockDim.x) {
     if (!slot_real[x]) continue;
@@ -355,6 +357,7 @@ __global__ void k_node_order(const int32_t* __restrict__ slot_res, const uint8_t
     const uint32_t rk = bit_rank(res, bitmap, wprefix, bprefix);
     node_slots[rk] = (int32_t)x;
     node_res[rk] = (int32_t)res;
+    inv_node[x] = (int32_t)rk;
   }
 }
 
@@ -477,6 +480,8 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_node_slots);
   cudaFree(p->d_node_residues);
   cudaFree(p->d_twiddles);
+  cudaFree(p->d_inv_elem);
+  cudaFree(p->d_inv_node);
   delete p;
 }
 
@@ -538,6 +543,8 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   M_((void**)&p->d_node_slots, 4 * std::min<int64_t>(A, k));
   M_((void**)&p->d_node_residues, 4 * std::min<int64_t>(A, k));
   M_(&p->d_twiddles, csz * std::max<int64_t>(A - 1, 1));
+  M_((void**)&p->d_inv_elem, 4 * A);
+  M_((void**)&p->d_inv_node, 4 * A);
   if (e != cudaSuccess) {
     plan_free(p);
     return cuda_fail(e, "plan allocation");
@@ -554,12 +561,14 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   if (cudaMemcpyAsync(dused.p, p->used, 4 * 32, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemsetAsync(count.p, 0, 4 * A, st) != cudaSuccess ||
       cudaMemsetAsync(reps.p, 0xff, 4 * (2 * A - 1), st) != cudaSuccess ||
-      cudaMemsetAsync(stats.p, 0, 16, st) != cudaSuccess)
+      cudaMemsetAsync(stats.p, 0, 16, st) != cudaSuccess ||
+      cudaMemsetAsync(p->d_inv_elem, 0xff, 4 * A, st) != cudaSuccess ||
+      cudaMemsetAsync(p->d_inv_node, 0xff, 4 * A, st) != cudaSuccess)
     return done(cuda_fail(cudaGetLastError(), "plan init"));
   uint32_t* dreps = (uint32_t*)reps.p;
   const int32_t* du = (const int32_t*)dused.p;
   k_plan_elements<<<grid_1d(k), 256, 0, st>>>(dJ, k, du, s, p->d_element_slots, (uint32_t*)count.p,
-                                              dreps + (A - 1));
+                                              dreps + (A - 1), p->d_inv_elem);
   for (int kk = s - 1; kk >= 0; --kk) k_min_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk);
   for (int kk = 1; kk <= s; ++kk) k_fill_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk, p->used[kk - 1]);
   if (A > 1) {
@@ -580,7 +589,8 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     if ((rc = rank_scan(R, st))) return done(rc);
     k_node_order<<<grid_1d(A), 256, 0, st>>>(p->d_slot_residues, p->d_slot_real, A,
                                              (const uint32_t*)R.bitmap.p, (const uint32_t*)R.wprefix.p,
-                                             (const uint32_t*)R.bsum.p, p->d_node_slots, p->d_node_residues);
+                                             (const uint32_t*)R.bsum.p, p->d_node_slots, p->d_node_residues,
+                                             p->d_inv_node);
   }
   unsigned long long h[2];
   if (cudaGetLastError() != cudaSuccess ||

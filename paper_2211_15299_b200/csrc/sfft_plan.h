@@ -17,12 +17,14 @@ struct sfft_plan {
   int32_t* d_node_slots;     // n_nodes  real slots in ascending residue order
   int32_t* d_node_residues;  // n_nodes
   void* d_twiddles;          // A-1 complex (dtype), stage-major
+  int32_t* d_inv_elem;       // A   slot -> support element (-1: virtual); unique when mu* = 1
+  int32_t* d_inv_node;       // A   slot -> node rank (-1: virtual)
 };
 
 namespace sfft {
 // transform launchers (sfft_hidft.cu)
 int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld, int64_t shift,
-                      const int32_t* map1, int64_t n1, double scale1, void* out1, int64_t ld1,
-                      void* out2, int64_t ld2, int identity, cudaStream_t st);
+                      const int32_t* map1, const int32_t* inv1, int64_t n1, double scale1, void* out1,
+                      int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st);
 int max_supported_s(int dtype);
 }  // namespace sfft

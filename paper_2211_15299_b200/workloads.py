@@ -91,13 +91,15 @@ def coefficients(cfg: int, b: int, k: int) -> np.ndarray:
     return rng.normal(size=k) + 1j * rng.normal(size=k)
 
 
-def synthesize_into(out, supports, coeffs, chunk: int = 16):
+def synthesize_into(out, supports, coeffs, chunk: int = 0):
     """out[b] = ifft(zero-padded spectrum_b) computed in complex128 on the
     device and cast to out.dtype.  supports: (k,) or (B, k) int64 array;
     coeffs: (B, k) complex128 array.  Harness only (torch.fft)."""
     import torch
     B, N = out.shape
     dev = out.device
+    if chunk <= 0:  # bound the complex128 temporaries to ~2 GiB
+        chunk = max(1, min(16, (2 << 30) // (N * 16)))
     sup = np.asarray(supports, dtype=np.int64)
     for s0 in range(0, B, chunk):
         s1 = min(B, s0 + chunk)

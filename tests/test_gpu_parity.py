@@ -323,3 +323,68 @@ def test_config3_sas(S, torch, golden_configs):
     _check_rows(wl, sig, got, [0, 1, 7, 300, 511], O.sas_mu1, 1e-5)
     for b in (0, 1):
         assert rel_l2(got[b], golden_configs[f"cfg3_b{b}_out"]) < 1e-5
+
+
+# ----------------------------------------------- cluster path (large A) ---
+
+@pytest.mark.parametrize("dt,s", [(np.complex64, 15), (np.complex64, 16), (np.complex64, 17),
+                                  (np.complex128, 14), (np.complex128, 15), (np.complex128, 16)])
+def test_cluster_homogeneous(S, torch, dt, s):
+    rng = np.random.default_rng(1000 + s)
+    M, B = 22, 3
+    piv = sorted(rng.choice(M, size=s, replace=False).tolist())
+    J = O.gen_homogeneous(piv, M, int(rng.integers(0, 2 ** 62)))
+    coef = rng.normal(size=(B, J.size)) + 1j * rng.normal(size=(B, J.size))
+    f = np.stack([O.synthesize(J, coef[b], M) for b in range(B)]).astype(dt)
+    Js = S.SupportSet(1 << M, J)
+    got = S.hidft_to_dft_batched(torch.from_numpy(f).cuda(), Js).cpu().numpy()
+    for b in range(B):
+        want = O.hidft_to_dft(f[b], J, M)
+        assert rel_l2(got[b], want) < TOL[dt], (b, rel_l2(got[b], want))
+    # node / slot outputs with a shift through the generic hidft entry
+    res = S.hidft(torch.from_numpy(f[:1]).cuda(), Js, tuple(piv), shift=12345)
+    o = O.hidft(f[0], J, M, piv, 0, 12345)
+    assert res.node_residues == tuple(int(x) for x in o.node_residues)
+    assert rel_l2(res.node_values[0].cpu().numpy(), o.node_values) < TOL[dt]
+    assert rel_l2(res.slot_values[0].cpu().numpy(), o.slot_values) < TOL[dt]
+
+
+def test_cluster_part_homogeneous_sas(S, torch):
+    # config-3 shape at larger scale: a 2^13 subset of a 2^16 homogeneous set
+    rng = np.random.default_rng(77)
+    M = 24
+    piv = sorted(rng.choice(M, size=16, replace=False).tolist())
+    H = O.gen_homogeneous(piv, M, 5)
+    J = np.sort(H[rng.choice(H.size, size=1 << 13, replace=False)])
+    r = O.pivots(J, M)
+    coef = rng.normal(size=J.size) + 1j * rng.normal(size=J.size)
+    f = O.synthesize(J, coef, M).astype(np.complex64)
+    Js = S.SupportSet(1 << M, J)
+    assert S.pivots(Js) == r
+    out = S.sas_transform(torch.from_numpy(f).cuda(), Js, r=r)
+    want = O.sas_mu1(f, J, M)
+    if len(r) > 14:
+        assert S.get_plan(Js, r, 0, 0, S._lib.require_device()).A == 1 << len(r)
+    assert rel_l2(out.coeffs.cpu().numpy(), want) < 1e-5
+    assert rel_l2(out.coeffs.cpu().numpy(), coef) < 1e-5
+    res = S.hidft(torch.from_numpy(f).cuda(), Js, r, height=1)
+    o = O.hidft(f, J, M, r, 1, 0)
+    assert res.node_residues == tuple(int(x) for x in o.node_residues)
+    assert rel_l2(res.node_values.cpu().numpy(), o.node_values) < 1e-5
+
+
+@pytest.mark.parametrize("cfg", [5, 6])
+def test_config5_full_batch(S, torch, golden_configs, cfg):
+    from paper_2211_15299_b200 import workloads as W
+    B = W.CONFIGS[cfg]["B"]
+    wl, sig = _synth(torch, S, cfg, B)
+    J = S.SupportSet(wl.N, wl.support)
+    got = S.hidft_to_dft_batched(sig, J).cpu().numpy()
+    tol = TOL[np.complex64 if wl.dtype == "complex64" else np.complex128]
+    err = np.linalg.norm(got - wl.coeffs, axis=1) / np.linalg.norm(wl.coeffs, axis=1)
+    assert err.max() < tol
+    _check_rows(wl, sig, got, [0, B - 1], O.hidft_to_dft, tol)
+    head = golden_configs["cfg5_b0_head"]
+    assert rel_l2(got[0][: head.size], head) < max(tol, 1e-6)
+    del sig
+    torch.cuda.empty_cache()
