@@ -317,8 +317,9 @@ def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
 
 # ------------------------------------------------------- CPU reference ---
 
-def _cpu_worker(args):
-    cfg, rows, barrier_path, deadline = args
+def _cpu_worker(cfg, rows, steps, barrier, queue):
+    """One host process: synthesise its rows (untimed), then time `steps`
+    passes of the reference call over them, each pass starting on a barrier."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import structfft_oracle as O
@@ -331,37 +332,59 @@ def _cpu_worker(args):
         coef = W.coefficients(cfg, b, J.size)
         sigs.append((J, M, O.synthesize(J, coef, M).astype(dt)))
     fn = O.reference_sas_call if cfg == 3 else O.reference_call
-    t0 = time.perf_counter()
-    done = 0
-    for J, M, f in sigs:
-        fn(f, J, M)
-        done += 1
-        if time.perf_counter() - t0 > deadline:
-            break
-    return done, sum(s[0].size for s in sigs[:done]), time.perf_counter() - t0
+    ncoef = sum(J.size for J, _, _ in sigs)
+    for step in range(steps):
+        barrier.wait()
+        t0 = time.perf_counter()
+        for J, M, f in sigs:
+            fn(f, J, M)
+        queue.put((step, time.perf_counter() - t0, ncoef))
 
 
-def run_cpu_reference(cfg: int, seconds: float) -> dict:
-    """The reference algorithm (oracle port) on all host cores, bounded sample."""
+def cpu_reference_steps(cfg: int, steps: int, seconds: float) -> tuple[list, dict]:
+    """The reference algorithm (oracle port, cost-faithful to the reference
+    call) on every host core, one process per core (the reference's own
+    process-pool mechanism, bench.py:261-263).  Each step is a bounded
+    sample: every worker runs its rows once; step value = coefficients /
+    slowest worker's time."""
     import multiprocessing as mp
-    P = os.cpu_count() or 1
-    # per-signal cost probe, then size the sample for ~`seconds` of wall time
-    probe = _cpu_worker((cfg, [0], None, 1e9))
-    per_sig = max(probe[2], 1e-4)
-    n_per = max(1, min(16, int(seconds / per_sig)))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import structfft_oracle as O
     from paper_2211_15299_b200 import workloads as W
-    Bmax = W.CONFIGS[cfg]["B"]
-    total = min(Bmax, n_per * P) if cfg != 5 else min(Bmax, 2 * P)
-    rows = list(range(total))
-    chunks = [rows[i::P] for i in range(P) if rows[i::P]]
-    ctx = mp.get_context("fork")
+    P = os.cpu_count() or 1
+    spec = W.CONFIGS[cfg]
+    J, M = W.config_support(cfg, 0)
+    esz = 8 if spec["dtype"] == "complex64" else 16
+    f0 = O.synthesize(J, W.coefficients(cfg, 0, J.size), M).astype(
+        np.complex64 if esz == 8 else np.complex128)
+    fn = O.reference_sas_call if cfg == 3 else O.reference_call
+    fn(f0, J, M)
     t0 = time.perf_counter()
-    with ctx.Pool(len(chunks)) as pool:
-        res = pool.map(_cpu_worker, [(cfg, c, None, 2 * seconds) for c in chunks])
-    wall = time.perf_counter() - t0
-    # workers synthesise before timing; report the slowest worker's timed span
-    span = max(r[2] for r in res)
-    coeffs = sum(r[1] for r in res)
+    fn(f0, J, M)
+    per_sig = time.perf_counter() - t0
+    del f0
+    mem_rows = max(1, (1 << 30) // ((1 << M) * esz))          # <= 1 GiB of signals per worker
+    time_rows = max(1, int(seconds / max(steps, 1) / per_sig))  # bounded step time
+    per_worker = max(1, min(mem_rows, time_rows, -(-spec["B"] // P)))
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(P)
+    queue = ctx.Queue()
+    procs = []
+    for w in range(P):
+        rows = [(w * per_worker + i) % spec["B"] for i in range(per_worker)]
+        procs.append(ctx.Process(target=_cpu_worker, args=(cfg, rows, steps, barrier, queue)))
+    t_wall = time.perf_counter()
+    for p in procs:
+        p.start()
+    per_step = {}
+    for _ in range(P * steps):
+        step, dt, n = queue.get(timeout=3600)
+        slot = per_step.setdefault(step, [0.0, 0])
+        slot[0] = max(slot[0], dt)
+        slot[1] += n
+    for p in procs:
+        p.join(timeout=60)
+    vals = [per_step[s][1] / per_step[s][0] for s in range(steps)]
     model = ""
     try:
         with open("/proc/cpuinfo") as fh:
@@ -371,10 +394,18 @@ def run_cpu_reference(cfg: int, seconds: float) -> dict:
                     break
     except OSError:
         pass
-    return {"value": coeffs / span, "unit": UNIT, "cores": len(chunks), "kind": "port",
-            "sample": f"{sum(r[0] for r in res)} signals of config {cfg} (oracle port of hidft+hidft_to_dft"
-                      f"{' / sas_transform' if cfg == 3 else ''}, dense host arrays, per-call plan), "
-                      f"{len(chunks)} worker processes on {model or 'host CPU'}; wall incl. synthesis {wall:.1f}s"}
+    info = {"unit": UNIT, "cores": P, "kind": "port",
+            "sample": f"{P * per_worker} signals of config {cfg} per step ({per_worker} per worker process, "
+                      f"{P} processes on {model or 'host CPU'}); oracle port of "
+                      f"{'sas_transform(f, J, r=pivots(J))' if cfg == 3 else 'hidft(f, J, pivots(J)) + hidft_to_dft'}"
+                      f" on dense host arrays, per-call plan and c64->c128 upcast as the reference; "
+                      f"single-call probe {per_sig * 1e3:.2f} ms/signal; total wall {time.perf_counter() - t_wall:.1f} s"}
+    return vals, info
+
+
+def run_cpu_reference(cfg: int, seconds: float) -> dict:
+    vals, info = cpu_reference_steps(cfg, 2, seconds)
+    return {"value": vals[-1], **info}
 
 
 def run_reference(args) -> None:
@@ -384,11 +415,7 @@ def run_reference(args) -> None:
     world = env_int("WORLD_SIZE", 1)
     cfg = args.config
     from paper_2211_15299_b200 import workloads as W
-    vals = []
-    cpu = None
-    for _ in range(args.warmup + args.steps):
-        cpu = run_cpu_reference(cfg, args.cpu_seconds / 3)
-        vals.append(cpu["value"])
+    vals, info = cpu_reference_steps(cfg, args.warmup + args.steps, args.ref_seconds)
     timed = vals[args.warmup:]
     value = statistics.median(timed)
     spec = W.CONFIGS[cfg]
@@ -401,7 +428,7 @@ def run_reference(args) -> None:
             "data": "synthetic, same seeds as the b200 arm",
             "config": {"workload": f"config {cfg}: N=2^{spec['M']}, k={k}, B={B}", "global_batch": B,
                        "parallelism": "host process pool"},
-            "cpu_baseline": {**cpu, "value": value},
+            "cpu_baseline": {"value": value, **info},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -417,7 +444,8 @@ def main() -> None:
     ap.add_argument("--max-sets", type=int, default=8)
     ap.add_argument("--soak", type=float, default=1.0)
     ap.add_argument("--e2e-steps", type=int, default=20)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU-baseline budget (b200 arm)")
+    ap.add_argument("--ref-seconds", type=float, default=150.0, help="whole --impl reference run budget")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

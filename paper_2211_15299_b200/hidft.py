@@ -370,8 +370,6 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         plan = get_plan(Js, cls.pivots, 0, code, run_dev)
         _lib.check(lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_DFT,
                                   out.data_ptr(), out.stride(0), None, 0, stream))
-        if st is not None:
-            st.zero_()
         res = out[0] if single else out
         return res.cpu() if host_out else res
     if st is None and check:
