@@ -115,6 +115,12 @@ def gather_bytes(pattern: np.ndarray, esz: int) -> tuple[int, int]:
     return 32 * sectors, pattern.size * esz
 
 
+def line_bytes(pattern: np.ndarray, esz: int) -> int:
+    """HBM bytes at the measured access granularity: every touched 128 B line
+    (profiles/r01_gather_granularity.md)."""
+    return 128 * np.unique((pattern * esz) // 128).size
+
+
 def measured_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -152,12 +158,14 @@ def run_b200(args) -> None:
     L2 = 126 * 2 ** 20
     pattern_bytes = None
     per_sig_sector = []
+    lines = 0
     if wl.support.ndim == 1:
         piv = S.pivots(S.SupportSet(N, wl.support))
         pat = S.pivoted_pattern(piv, wl.M).as_array()
         gb, ub = gather_bytes(pat, esz)
         per_sig_sector = [gb] * B
         pattern_bytes = (gb, ub)
+        lines = B * line_bytes(pat, esz)
     else:
         ub_sum = 0
         for b in range(B):
@@ -165,6 +173,7 @@ def run_b200(args) -> None:
             gb, ub = gather_bytes(pat, esz)
             per_sig_sector.append(gb)
             ub_sum += ub
+            lines += line_bytes(pat, esz)
         pattern_bytes = (None, ub_sum / B)
     footprint = sum(per_sig_sector)
     R = max(2, math.ceil(4 * L2 / max(footprint, 1)))
@@ -243,6 +252,12 @@ def run_b200(args) -> None:
             "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": int(G),
             "element_bytes_per_launch": int(B * (pattern_bytes[1] if pattern_bytes else 0) + B * wl.k * esz)}
+    # the same kernel against HBM bytes at the measured 128 B access granularity
+    G_line = lines + B * wl.k * esz + wl.support.size * 8
+    roof["at_measured_granularity"] = {
+        "bytes_per_launch": int(G_line), "achieved": round(G_line / (ms_per_step / 1e3) / 1e9, 1),
+        "frac": round(G_line / (ms_per_step / 1e3) / 1e9 / hbm, 4),
+        "note": "every isolated HBM read moves a 128 B line on this B200 (profiles/r01_gather_granularity.md)"}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:

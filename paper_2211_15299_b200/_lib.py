@@ -15,7 +15,7 @@ from .errors import (BudgetExceededError, ContractViolationError, DeviceError,
                      InvalidInputError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsfft_b200.so")
+LIB_PATH = os.environ.get("SFFT_LIB") or os.path.join(_HERE, "libsfft_b200.so")
 
 OK, ERR_INVALID, ERR_CONTRACT, ERR_BUDGET, ERR_CUDA, ERR_UNSUPPORTED = 0, 2, 3, 4, 5, 6
 C64, C128 = 0, 1

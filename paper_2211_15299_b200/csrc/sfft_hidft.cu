@@ -52,12 +52,14 @@ struct Geo {
 
 // Bank-conflict-free shared-memory slot position: XOR the low SWZ bits with
 // the XOR-fold of the higher bits.  A bijection inside each aligned block,
-// conflict-free for every power-of-two lane stride used below.
+// conflict-free for every power-of-two lane stride used below, and LINEAR
+// over GF(2): swz(a ^ b) = swz(a) ^ swz(b), so a slot split into a thread
+// part and a register part costs one XOR per access (the register part is
+// a compile-time constant after unrolling).
 template <typename T, int S>
-__device__ __forceinline__ int swz(int a) {
+__host__ __device__ constexpr int swz(int a) {
   constexpr int B = EMax<T>::SWZ;
   int y = a >> B, f = 0;
-#pragma unroll
   for (int i = 0; i < (S + B - 1) / B; ++i) {
     f ^= y & ((1 << B) - 1);
     y >>= B;
@@ -67,11 +69,16 @@ __device__ __forceinline__ int swz(int a) {
 
 // Slot owned by thread t (within its signal) for register x in pass p:
 // bits [w0, w0+LE) come from x, the rest from t.
+__host__ __device__ constexpr int pass_w0(int p, int S, int LE) { return (p * LE < S - LE) ? p * LE : S - LE; }
 template <int S, int LE>
-__device__ __forceinline__ int slot_of(int p, int t, int x) {
-  const int w0 = (p * LE < S - LE) ? p * LE : S - LE;
-  return (t & ((1 << w0) - 1)) | (x << w0) | ((t >> w0) << (w0 + LE));
+__device__ __forceinline__ int slot_t(int p, int t) {
+  const int w0 = pass_w0(p, S, LE);
+  return (t & ((1 << w0) - 1)) | ((t >> w0) << (w0 + LE));
 }
+template <int S, int LE>
+__host__ __device__ constexpr int slot_x(int p, int x) { return x << pass_w0(p, S, LE); }
+template <int S, int LE>
+__device__ __forceinline__ int slot_of(int p, int t, int x) { return slot_t<S, LE>(p, t) | slot_x<S, LE>(p, x); }
 
 // Stages [p*LE, min(p*LE+LE, S)) of pass p, in registers.
 template <typename T, int S, int E, int LE>
@@ -97,21 +104,22 @@ __device__ __forceinline__ void pass_stages(Cx<T> (&v)[E], int p, int t, const C
 }
 
 // Whole butterfly for one signal per thread group.  On entry v holds the
-// pass-0 slots (x + t*E); on exit the slot values sit in sd (swizzled) and
-// the CTA has passed a barrier.
-template <typename T, int S>
+// pass-0 slots (x + t*E) unless LOAD0 (then they are read from sd); on exit
+// the slot values sit in sd (swizzled) and the CTA has passed a barrier.
+template <typename T, int S, bool LOAD0 = false>
 __device__ __forceinline__ void butterfly(Cx<T> (&v)[Geo<T, S>::E], int t, Cx<T>* sd,
                                           const Cx<T>* __restrict__ tw) {
   using G = Geo<T, S>;
 #pragma unroll
   for (int p = 0; p < G::NPASS; ++p) {
-    if (p > 0) {
+    const int tb = swz<T, S>(slot_t<S, G::LE>(p, t));
+    if (p > 0 || LOAD0) {
 #pragma unroll
-      for (int x = 0; x < G::E; ++x) v[x] = sd[swz<T, S>(slot_of<S, G::LE>(p, t, x))];
+      for (int x = 0; x < G::E; ++x) v[x] = sd[tb ^ swz<T, S>(slot_x<S, G::LE>(p, x))];
     }
     pass_stages<T, S, G::E, G::LE>(v, p, t, tw);
 #pragma unroll
-    for (int x = 0; x < G::E; ++x) sd[swz<T, S>(slot_of<S, G::LE>(p, t, x))] = v[x];
+    for (int x = 0; x < G::E; ++x) sd[tb ^ swz<T, S>(slot_x<S, G::LE>(p, x))] = v[x];
     __syncthreads();
   }
 }
@@ -218,8 +226,22 @@ k_hidft_plan(const PlanArgs args) {
 //     reads the C partners of each from the C slices over DSMEM, finishes
 //     the butterfly in registers and stores straight to the output row
 //     through the plan's slot -> output-position map.
+template <int S>
+__device__ __forceinline__ uint32_t brev_s(uint32_t x) { return __brev(x) >> (32 - S); }
+
+#ifdef SFFT_PHASE_TIMING
+// debug build only: per-CTA clock64 stamps at phase boundaries
+__device__ unsigned long long g_phase_stamps[1 << 20][8];
+#define SFFT_STAMP(i)                                                               \
+  do {                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < (1u << 20)) g_phase_stamps[blockIdx.x][i] = clock64(); \
+  } while (0)
+#else
+#define SFFT_STAMP(i) do {} while (0)
+#endif
+
 template <typename T, int S, int C>
-__global__ void __launch_bounds__(Geo<T, S - ilog2c(C)>::NT, 1)
+__global__ void __launch_bounds__(Geo<T, S - ilog2c(C)>::NT, (C <= 8 ? 2 : 1))
 k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
   constexpr int LC = ilog2c(C), SL = S - LC, AL = 1 << SL;
   using G = Geo<T, SL>;
@@ -232,76 +254,96 @@ k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
   const int64_t b = blockIdx.x / C;
   const int t = threadIdx.x;
   const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(args.tw);
-  uint32_t d[S];
-#pragma unroll
-  for (int i = 0; i < S; ++i) d[i] = 1u << (args.M - 1 - args.used[i]);
   const uint32_t nmask = (args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u);
   const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
+#define SFFT_D(i) (1u << (args.M - 1 - args.used[(i)]))
+  SFFT_STAMP(0);
 
-  // 0. coalesced gather of sorted positions qs = q*AL + x*NT + t
+  // 0. coalesced gather of sorted positions qs = q*AL + x*NT + t; sorted
+  //    index bit j carries pivot S-1-j.  Slot = brev_S(qs), linear in qs.
   uint32_t offt = args.negshift;
 #pragma unroll
   for (int j = 0; j < LNT; ++j)
-    if ((t >> j) & 1) offt += d[S - 1 - j];
+    if ((t >> j) & 1) offt += SFFT_D(S - 1 - j);
 #pragma unroll
   for (int j = 0; j < LC; ++j)
-    if ((q >> j) & 1) offt += d[S - 1 - (SL + j)];
+    if ((q >> j) & 1) offt += SFFT_D(S - 1 - (SL + j));
+  uint32_t dx[G::LE > 0 ? G::LE : 1];
+#pragma unroll
+  for (int j = 0; j < G::LE; ++j) dx[j] = SFFT_D(S - 1 - (LNT + j));
   Cx<T> v[G::E];
 #pragma unroll
   for (int x = 0; x < G::E; ++x) {
     uint32_t off = offt;
 #pragma unroll
     for (int j = 0; j < G::LE; ++j)
-      if ((x >> j) & 1) off += d[S - 1 - (LNT + j)];
+      if ((x >> j) & 1) off += dx[j];
     v[x] = load_sample(row + (off & nmask));
   }
+  SFFT_STAMP(1);
+  {
+    const uint32_t at = brev_s<S>((uint32_t)t) ^ brev_s<S>((uint32_t)(q * AL));
 #pragma unroll
-  for (int x = 0; x < G::E; ++x) {
-    const uint32_t qs = (uint32_t)(q * AL + x * NT + t);
-    const uint32_t a = __brev(qs) >> (32 - S);
-    Cx<T>* dst = cluster.map_shared_rank(sd, (int)(a >> SL));
-    dst[swz<T, SL>((int)(a & (AL - 1)))] = v[x];
+    for (int x = 0; x < G::E; ++x) {
+      const uint32_t a = at ^ brev_s<S>((uint32_t)(x * NT));
+      Cx<T>* dst = cluster.map_shared_rank(sd, (int)(a >> SL));
+      dst[swz<T, SL>((int)(a & (AL - 1)))] = v[x];
+    }
   }
+  SFFT_STAMP(2);
   cluster.sync();
+  SFFT_STAMP(3);
 
-  // 1. local stages 1..SL
-#pragma unroll
-  for (int x = 0; x < G::E; ++x) v[x] = sd[swz<T, SL>(slot_of<SL, G::LE>(0, t, x))];
-  butterfly<T, SL>(v, t, sd, tw);
+  // 1. local stages 1..SL on this CTA's slice
+  butterfly<T, SL, true>(v, t, sd, tw);
+  SFFT_STAMP(4);
   cluster.sync();
+  SFFT_STAMP(5);
 
-  // 2. stages SL+1..S across the cluster
+  // 2. stages SL+1..S across the cluster: all loads first, then math, then stores
   constexpr int PER = AL / C;
+  constexpr int RPT = PER >= NT ? PER / NT : 1;  // local indices per thread
   const T scale = (T)args.scale1;
   Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
   Cx<T>* o2 = args.out2 ? reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2 : nullptr;
-  for (int i = t; i < PER; i += NT) {
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const int i = t + rr * NT;
+    if (i >= PER) break;
     const int al = q * PER + i;
+    const int sl = swz<T, SL>(al);
     Cx<T> w[C];
 #pragma unroll
-    for (int x = 0; x < C; ++x) w[x] = cluster.map_shared_rank(sd, x)[swz<T, SL>(al)];
+    for (int x = 0; x < C; ++x) w[x] = cluster.map_shared_rank(sd, x)[sl];
+    Cx<T> tws[C - 1];  // stage j twiddles at x < 2^j: index (1<<(SL+j))-1 + al + (x << SL)
+#pragma unroll
+    for (int j = 0; j < LC; ++j)
+#pragma unroll
+      for (int x = 0; x < (1 << j); ++x) tws[(1 << j) - 1 + x] = tw[(1 << (SL + j)) - 1 + al + (x << SL)];
+    int pos[C];
+#pragma unroll
+    for (int x = 0; x < C; ++x) pos[x] = inv1 ? __ldg(inv1 + al + x * AL) : al + x * AL;
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
-      const int beta = SL + j;
 #pragma unroll
       for (int x = 0; x < C; ++x) {
         if (x & (1 << j)) continue;
-        const int h = al + ((x & ((1 << j) - 1)) << SL);
         const Cx<T> u = w[x];
-        const Cx<T> z = cmul(tw[(1 << beta) - 1 + h], w[x | (1 << j)]);
+        const Cx<T> z = cmul(tws[(1 << j) - 1 + (x & ((1 << j) - 1))], w[x | (1 << j)]);
         w[x] = csub(u, z);
         w[x | (1 << j)] = cadd(u, z);
       }
     }
 #pragma unroll
     for (int x = 0; x < C; ++x) {
-      const int a = al + x * AL;
-      const int pos = inv1 ? __ldg(inv1 + a) : a;
-      if (pos >= 0) o1[pos] = cscale(w[x], scale);
-      if (o2) o2[a] = w[x];
+      if (pos[x] >= 0) o1[pos[x]] = cscale(w[x], scale);
+      if (o2) o2[al + x * AL] = w[x];
     }
   }
+#undef SFFT_D
+  SFFT_STAMP(6);
   cluster.sync();  // keep every slice alive until all remote reads are done
+  SFFT_STAMP(7);
 }
 
 // -------------------------------------------- fused homogeneous to_dft ---
@@ -849,3 +891,11 @@ extern "C" int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_su
   if (tmpStat) cudaFreeAsync(tmpStat, st);
   return rc;
 }
+
+#ifdef SFFT_PHASE_TIMING
+extern "C" SFFT_API int sfft_debug_stamps(unsigned long long* out, int nblocks) {
+  SFFT_CUDA(cudaDeviceSynchronize());
+  SFFT_CUDA(cudaMemcpyFromSymbol(out, sfft::g_phase_stamps, sizeof(unsigned long long) * 8 * nblocks));
+  return SFFT_OK;
+}
+#endif
