@@ -17,6 +17,7 @@
 // double2) with row stride ld; outputs are rows of n_out complex.
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -94,11 +95,7 @@ __device__ __forceinline__ void pass_stages(Cx<T> (&v)[E], int p, int t, const C
       if (x & (1 << lb)) continue;
       const int a = slot_of<S, LE>(p, t, x);
       const int h = a & ((1 << beta) - 1);
-      const Cx<T> w = tw[(1 << beta) - 1 + h];
-      const Cx<T> u = v[x];
-      const Cx<T> z = cmul(w, v[x | (1 << lb)]);
-      v[x] = csub(u, z);
-      v[x | (1 << lb)] = cadd(u, z);
+      bfly(v[x], v[x | (1 << lb)], tw[(1 << beta) - 1 + h]);
     }
   }
 }
@@ -164,6 +161,7 @@ struct PlanArgs {
   void* out2;  // optional slot values (identity map)
   int64_t ld2;
   int identity;  // samples already gathered in slot order (row[a] = slot a)
+  int debug_skip;  // timing build only: bit0 gather, bit1 scatter, bit2 local stages, bit3 phase 2
 };
 
 template <typename T, int S> constexpr size_t plan_smem() {
@@ -229,6 +227,53 @@ k_hidft_plan(const PlanArgs args) {
 template <int S>
 __device__ __forceinline__ uint32_t brev_s(uint32_t x) { return __brev(x) >> (32 - S); }
 
+// --- DSMEM helpers (PTX): shared::cluster addresses, async remote stores that
+// complete on the destination CTA's mbarrier, and the cluster barrier halves.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async(uint32_t addr, Cx<float> v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+               :: "r"(addr), "f"(v.x), "f"(v.y), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t addr, Cx<double> v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               :: "r"(addr), "d"(v.x), "d"(v.y), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive_tx_local(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+#ifdef SFFT_PHASE_TIMING
+#define SFFT_SKIP(bit) (args.debug_skip & (1 << (bit)))
+#else
+#define SFFT_SKIP(bit) 0
+#endif
 #ifdef SFFT_PHASE_TIMING
 // debug build only: per-CTA clock64 stamps at phase boundaries
 __device__ unsigned long long g_phase_stamps[1 << 20][8];
@@ -240,27 +285,75 @@ __device__ unsigned long long g_phase_stamps[1 << 20][8];
 #define SFFT_STAMP(i) do {} while (0)
 #endif
 
+// 16-byte remote async store into another CTA's shared memory, completing on
+// that CTA's mbarrier (two complex64 or one complex128)
+__device__ __forceinline__ void st_async16(uint32_t addr, Cx<float> a, Cx<float> b, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+               :: "r"(addr), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void st_async16(uint32_t addr, Cx<double> a, Cx<double>, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               :: "r"(addr), "d"(a.x), "d"(a.y), "r"(mbar) : "memory");
+}
+
 template <typename T, int S, int C>
-__global__ void __launch_bounds__(Geo<T, S - ilog2c(C)>::NT, (C <= 8 ? 2 : 1))
-k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
-  constexpr int LC = ilog2c(C), SL = S - LC, AL = 1 << SL;
+struct ClusterGeo {
+  static constexpr int LC = ilog2c(C), SL = S - LC, AL = 1 << SL, PER = AL / C;
   using G = Geo<T, SL>;
-  static_assert(G::SPC == 1, "one signal slice per CTA");
-  constexpr int NT = G::NT, LNT = ilog2c(NT);
+  static constexpr int NT = G::NT;
+  static constexpr int EPU = 16 / (int)sizeof(Cx<T>);  // elements per 16-byte unit
+  static constexpr size_t SMEM = 3 * (size_t)AL * sizeof(Cx<T>);  // W, R1, R2
+  static constexpr int MINB = (int)((200 * 1024) / SMEM) >= 2 ? 2 : 1;
+};
+
+// Persistent cluster kernel (C CTAs per signal, clusters loop over signals).
+// Per signal, two all-to-all exchanges of contiguous 16-byte blocks pushed
+// with st.async into the receiver's buffer and counted by its mbarrier; no
+// cluster-wide barrier inside the loop (a sender can only run ahead into
+// the next signal after the receiver has released the buffer, see below).
+//   0. CTA q gathers the q-th contiguous chunk of the SORTED sample set
+//      (coalesced over runs; prefetched during the previous signal), stages
+//      it in W grouped by owner CTA, and pushes block r to CTA r's R1
+//      (layout [source q][i]).
+//   1. CTA r transforms its slice (slots with top log2(C) bits = r, the
+//      local stages 1..SL) reading pass 0 straight from R1, result in W.
+//   2. CTA r pushes local slot range [q'*PER, (q'+1)*PER) to CTA q''s R2.
+//   3. CTA q' finishes stages SL+1..S for its PER local indices (all C
+//      partners in R2) and stores through the slot -> output map.
+// Buffer reuse: R1 of signal n+1 is written by a sender only after that
+// sender finished step 3 of signal n, which needed this CTA's step-2 data,
+// which this CTA sends after its step 1 (the last reader of R1).  Likewise
+// R2.  Each mbarrier is re-armed right after its wait, before this CTA
+// sends anything that could let a sender run ahead.  (A two-buffer variant
+// with register-staged pushes measured 7% slower at the same occupancy.)
+template <typename T, int S, int C>
+__global__ void __launch_bounds__(ClusterGeo<T, S, C>::NT, ClusterGeo<T, S, C>::MINB)
+k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
+  using CG = ClusterGeo<T, S, C>;
+  constexpr int LC = CG::LC, SL = CG::SL, AL = CG::AL, PER = CG::PER, NT = CG::NT, EPU = CG::EPU;
+  using G = typename CG::G;
+  constexpr int LNT = ilog2c(NT);
+  constexpr uint32_t BYTES = AL * sizeof(Cx<T>);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Cx<T>* sd = reinterpret_cast<Cx<T>*>(smem_raw);
+  Cx<T>* W = reinterpret_cast<Cx<T>*>(smem_raw);
+  Cx<T>* R1 = W + AL;
+  Cx<T>* R2 = R1 + AL;
+  __shared__ __align__(8) unsigned long long s_mbar[2];
   cg::cluster_group cluster = cg::this_cluster();
   const int q = (int)cluster.block_rank();
-  const int64_t b = blockIdx.x / C;
   const int t = threadIdx.x;
   const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(args.tw);
   const uint32_t nmask = (args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u);
-  const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
+  const uint32_t mb0 = smem_addr(&s_mbar[0]), mb1 = smem_addr(&s_mbar[1]);
+  const uint32_t r1_addr = smem_addr(R1), r2_addr = smem_addr(R2);
+  if (t == 0) {
+    mbar_init(mb0, 1);
+    mbar_init(mb1, 1);
+    mbar_expect_tx(mb0, BYTES);
+    mbar_expect_tx(mb1, BYTES);
+  }
+  cluster.sync();  // barrier inits visible cluster-wide
 #define SFFT_D(i) (1u << (args.M - 1 - args.used[(i)]))
-  SFFT_STAMP(0);
-
-  // 0. coalesced gather of sorted positions qs = q*AL + x*NT + t; sorted
-  //    index bit j carries pivot S-1-j.  Slot = brev_S(qs), linear in qs.
   uint32_t offt = args.negshift;
 #pragma unroll
   for (int j = 0; j < LNT; ++j)
@@ -271,79 +364,103 @@ k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
   uint32_t dx[G::LE > 0 ? G::LE : 1];
 #pragma unroll
   for (int j = 0; j < G::LE; ++j) dx[j] = SFFT_D(S - 1 - (LNT + j));
-  Cx<T> v[G::E];
-#pragma unroll
-  for (int x = 0; x < G::E; ++x) {
-    uint32_t off = offt;
-#pragma unroll
-    for (int j = 0; j < G::LE; ++j)
-      if ((x >> j) & 1) off += dx[j];
-    v[x] = load_sample(row + (off & nmask));
-  }
-  SFFT_STAMP(1);
-  {
-    const uint32_t at = brev_s<S>((uint32_t)t) ^ brev_s<S>((uint32_t)(q * AL));
+#undef SFFT_D
+  const T scale = (T)args.scale1;
+  const int64_t ncl = gridDim.x / C;
+  // gather sorted positions u = x*NT + t of signal bb into v
+  auto gather_sorted = [&](Cx<T>(&v)[G::E], int64_t bb) {
+    const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + bb * args.ld;
 #pragma unroll
     for (int x = 0; x < G::E; ++x) {
-      const uint32_t a = at ^ brev_s<S>((uint32_t)(x * NT));
-      Cx<T>* dst = cluster.map_shared_rank(sd, (int)(a >> SL));
-      dst[swz<T, SL>((int)(a & (AL - 1)))] = v[x];
+      uint32_t off = offt;
+#pragma unroll
+      for (int j = 0; j < G::LE; ++j)
+        if ((x >> j) & 1) off += dx[j];
+      v[x] = load_sample(row + (off & nmask));
     }
-  }
-  SFFT_STAMP(2);
-  cluster.sync();
-  SFFT_STAMP(3);
-
-  // 1. local stages 1..SL on this CTA's slice
-  butterfly<T, SL, true>(v, t, sd, tw);
-  SFFT_STAMP(4);
-  cluster.sync();
-  SFFT_STAMP(5);
-
-  // 2. stages SL+1..S across the cluster: all loads first, then math, then stores
-  constexpr int PER = AL / C;
-  constexpr int RPT = PER >= NT ? PER / NT : 1;  // local indices per thread
-  const T scale = (T)args.scale1;
-  Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
-  Cx<T>* o2 = args.out2 ? reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2 : nullptr;
+  };
+  Cx<T> v[G::E];
+  if (blockIdx.x / C < args.B) gather_sorted(v, blockIdx.x / C);
+  uint32_t par = 0;
+  for (int64_t b = blockIdx.x / C; b < args.B; b += ncl, par ^= 1u) {
+    SFFT_STAMP(0);
+    // ---- 0. stage by owner (XOR by owner: conflict-free), push to R1s
 #pragma unroll
-  for (int rr = 0; rr < RPT; ++rr) {
-    const int i = t + rr * NT;
-    if (i >= PER) break;
-    const int al = q * PER + i;
-    const int sl = swz<T, SL>(al);
-    Cx<T> w[C];
+    for (int x = 0; x < G::E; ++x) {
+      const uint32_t u = (uint32_t)(x * NT + t);
+      const uint32_t r = brev_s<LC>(u & (C - 1));
+      const uint32_t i = brev_s<SL>(u) & (PER - 1);
+      W[r * PER + (i ^ r)] = v[x];
+    }
+    __syncthreads();
+    for (int w = t; w < AL / EPU; w += NT) {
+      const int j0 = w * EPU;
+      const int r = j0 / PER, jj = j0 % PER;
+      const int i0 = jj ^ r;  // staged element i0 (and its pair partner i0^1)
+      Cx<T> e0 = W[j0], e1 = W[j0 + EPU - 1];
+      if (EPU == 2 && (i0 & 1)) { const Cx<T> tmp = e0; e0 = e1; e1 = tmp; }
+      const uint32_t dst = r1_addr + (uint32_t)((q * PER + (i0 & ~(EPU - 1))) * sizeof(Cx<T>));
+      st_async16(cluster_addr(dst, r), e0, e1, cluster_addr(mb0, r));
+    }
+    __syncthreads();  // W free for the local stages
+    SFFT_STAMP(1);
+    mbar_wait(mb0, par);
+    SFFT_STAMP(2);
+    if (t == 0) mbar_expect_tx(mb0, BYTES);  // arm for the next signal
+    // ---- 1. local stages; pass 0 reads R1[src][i] for local slot (i << LC) | brev(src)
 #pragma unroll
-    for (int x = 0; x < C; ++x) w[x] = cluster.map_shared_rank(sd, x)[sl];
-    Cx<T> tws[C - 1];  // stage j twiddles at x < 2^j: index (1<<(SL+j))-1 + al + (x << SL)
+    for (int x = 0; x < G::E; ++x) {
+      const int al = x + t * G::E;
+      v[x] = R1[brev_s<LC>((uint32_t)(al & (C - 1))) * PER + (al >> LC)];
+    }
+    butterfly<T, SL>(v, t, W, tw);
+    SFFT_STAMP(3);
+    // ---- 2. push local range [q'*PER, (q'+1)*PER) to CTA q'
+    for (int w = t; w < AL / EPU; w += NT) {
+      const int j0 = w * EPU;
+      const int qd = j0 / PER, ii = j0 % PER;
+      const int p0 = swz<T, SL>(j0);
+      const Cx<T> e0 = W[p0], e1 = W[p0 ^ (EPU - 1)];
+      const uint32_t dst = r2_addr + (uint32_t)((q * PER + ii) * sizeof(Cx<T>));
+      st_async16(cluster_addr(dst, qd), e0, e1, cluster_addr(mb1, qd));
+    }
+    // prefetch the next signal's samples: their latency hides behind steps 2-3
+    if (b + ncl < args.B) gather_sorted(v, b + ncl);
+    mbar_wait(mb1, par);
+    SFFT_STAMP(4);
+    if (t == 0) mbar_expect_tx(mb1, BYTES);
+    // ---- 3. stages SL+1..S for local indices al = q*PER + i
+    Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
+    Cx<T>* o2 = args.out2 ? reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2 : nullptr;
+    for (int i = t; i < PER; i += NT) {
+      const int al = q * PER + i;
+      Cx<T> w[C];
 #pragma unroll
-    for (int j = 0; j < LC; ++j)
+      for (int x = 0; x < C; ++x) w[x] = R2[x * PER + i];
 #pragma unroll
-      for (int x = 0; x < (1 << j); ++x) tws[(1 << j) - 1 + x] = tw[(1 << (SL + j)) - 1 + al + (x << SL)];
-    int pos[C];
+      for (int j = 0; j < LC; ++j) {
+        Cx<T> twj[C / 2];
 #pragma unroll
-    for (int x = 0; x < C; ++x) pos[x] = inv1 ? __ldg(inv1 + al + x * AL) : al + x * AL;
+        for (int x = 0; x < C / 2; ++x)
+          if (x < (1 << j)) twj[x] = tw[(1 << (SL + j)) - 1 + al + (x << SL)];
 #pragma unroll
-    for (int j = 0; j < LC; ++j) {
+        for (int x = 0; x < C; ++x) {
+          if (x & (1 << j)) continue;
+          bfly(w[x], w[x | (1 << j)], twj[x & ((1 << j) - 1)]);
+        }
+      }
 #pragma unroll
       for (int x = 0; x < C; ++x) {
-        if (x & (1 << j)) continue;
-        const Cx<T> u = w[x];
-        const Cx<T> z = cmul(tws[(1 << j) - 1 + (x & ((1 << j) - 1))], w[x | (1 << j)]);
-        w[x] = csub(u, z);
-        w[x | (1 << j)] = cadd(u, z);
+        const int a = al + x * AL;
+        const int pos = inv1 ? __ldg(inv1 + a) : a;
+        if (pos >= 0) o1[pos] = cscale(w[x], scale);
+        if (o2) o2[a] = w[x];
       }
     }
-#pragma unroll
-    for (int x = 0; x < C; ++x) {
-      if (pos[x] >= 0) o1[pos[x]] = cscale(w[x], scale);
-      if (o2) o2[al + x * AL] = w[x];
-    }
+    __syncthreads();  // W staging of the next signal after every push read W
+    SFFT_STAMP(5);
   }
-#undef SFFT_D
-  SFFT_STAMP(6);
-  cluster.sync();  // keep every slice alive until all remote reads are done
-  SFFT_STAMP(7);
+  cluster.sync();  // no CTA leaves while peers may still push into it
 }
 
 // -------------------------------------------- fused homogeneous to_dft ---
@@ -588,25 +705,14 @@ static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
 
 template <typename T, int S, int C>
 static int run_cluster_kernel(const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
-  constexpr int SL = S - ilog2c(C);
-  using G = Geo<T, SL>;
-  constexpr size_t smem = (size_t)G::A * sizeof(Cx<T>);
+  using CG = ClusterGeo<T, S, C>;
+  constexpr size_t smem = CG::SMEM;
+  static_assert(smem <= 227 * 1024, "cluster kernel smem");
   auto kern = k_hidft_cluster<T, S, C>;
   int dev = 0;
   SFFT_CUDA(cudaGetDevice(&dev));
-  {
-    std::lock_guard<std::mutex> lk(g_kmu);
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
-    if (!g_occ.count(key)) {
-      SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      if (C > 8) SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      g_occ[key] = 1;
-    }
-  }
-  if (a.B * C > 0x7fffffffll) return fail(SFFT_ERR_UNSUPPORTED, "batch too large for one launch");
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a.B * C));
-  cfg.blockDim = dim3(G::NT);
+  cfg.blockDim = dim3(CG::NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -616,6 +722,24 @@ static int run_cluster_kernel(const PlanArgs& a, const int32_t* inv1, cudaStream
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  int max_clusters = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_kmu);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+    auto it = g_occ.find(key);
+    if (it == g_occ.end()) {
+      SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (C > 8) SFFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cfg.gridDim = dim3(C);
+      SFFT_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+      if (max_clusters < 1) return fail(SFFT_ERR_UNSUPPORTED, "cluster does not fit on the device");
+      g_occ[key] = max_clusters;
+    } else {
+      max_clusters = it->second;
+    }
+  }
+  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(a.B, max_clusters));
+  cfg.gridDim = dim3((unsigned)(ncl * C));
   SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, a, inv1));
   return SFFT_OK;
 }
@@ -643,8 +767,12 @@ static int dispatch_plan(int dtype, int s, const PlanArgs& a, const int32_t* inv
       SFFT_CASES_12(PLAN_CASE, float)
       PLAN_CASE(13, float)
       PLAN_CASE(14, float)
-      case 15: return run_cluster_kernel<float, 15, 4>(a, inv1, st);
+      case 15: return run_cluster_kernel<float, 15, 8>(a, inv1, st);
+#ifdef SFFT_C8_FOR_S16
       case 16: return run_cluster_kernel<float, 16, 8>(a, inv1, st);
+#else
+      case 16: return run_cluster_kernel<float, 16, 16>(a, inv1, st);
+#endif
       case 17: return run_cluster_kernel<float, 17, 16>(a, inv1, st);
       default: break;
     }
@@ -685,6 +813,9 @@ int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld
                       int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st) {
   PlanArgs a{};
   a.identity = identity;
+#ifdef SFFT_PHASE_TIMING
+  if (const char* e = getenv("SFFT_DEBUG_SKIP")) a.debug_skip = atoi(e);
+#endif
   a.sig = sig;
   a.B = B;
   a.ld = ld;

@@ -25,17 +25,19 @@ torch.cuda.synchronize()
 lib = _lib.load()
 lib.sfft_debug_stamps.argtypes = [ctypes.c_void_p, ctypes.c_int]
 plan = S.get_plan(J, S.pivots(J), 0, 0 if cdt == torch.complex64 else 1, torch.device("cuda", 0))
-C = {16: 8, 15: 4, 17: 16}.get(plan.s, 16) if cdt == torch.complex64 else {14: 4, 15: 8, 16: 16}[plan.s]
-nb = B * C
+C = {16: 16, 15: 8, 17: 16}.get(plan.s, 16) if cdt == torch.complex64 else {14: 4, 15: 8, 16: 16}[plan.s]
+nb = min(B * C, 148 * 4)
 st = np.zeros((nb, 8), np.uint64)
 _lib.check(lib.sfft_debug_stamps(st.ctypes.data, nb))
 st = st.astype(np.int64)
+st = st[st[:, 0] != 0]
 rel = st - st[:, :1]
-names = ["gather issued", "dsmem scatter", "cluster.sync#1", "local butterfly", "cluster.sync#2", "phase 2", "final sync"]
-d = np.diff(st, axis=1)
+names = ["gather+stage", "push R1 + wait", "local stages", "push R2 + wait", "last stages+store"]
+d = np.diff(st[:, :6], axis=1)
 print(f"cfg{cfg} B={B} s={plan.s} C={C}: per-CTA cycles by phase (median / p90)")
 for i, n in enumerate(names):
     print(f"  {n:18s} {np.median(d[:, i]):9.0f} {np.percentile(d[:, i], 90):9.0f}")
-print(f"  {'total':18s} {np.median(rel[:, 7]):9.0f}")
-span = st[:, 7].max() - st[:, 0].min()
+print(f"  {'total (last signal)':18s} {np.median(rel[:, 5]):9.0f}")
+span = st[:, 5].max() - st[:, 0].min()
 print(f"kernel span (cycles, SM clocks differ per SM -> indicative) {span}")
+
