@@ -136,6 +136,12 @@ SFFT_API int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const void
                                  int64_t B, int64_t ld, void* out, int64_t ld_out,
                                  sfft_stream_t stream);
 
+/* BandlimitedSignal.sample_block (core.py:164-173) on the device:
+ * out[i] = (1/N) sum_e coeffs[e] exp(+2 pi i (locations[i] * J[e] mod N) / N),
+ * complex128, J / coeffs / locations / out device pointers. */
+SFFT_API int sfft_synthesize(const int64_t* J, const void* coeffs, int64_t k, int M,
+                             const int64_t* locations, int64_t n, void* out, sfft_stream_t stream);
+
 /* Fused hidft(f_b, J_b, pivots(J_b)) + hidft_to_dft for homogeneous supports:
  * pivots, pattern, tables and twiddles are derived on chip per CTA, so one
  * launch does plan + gather + butterfly + scaled, ascending-J store.

@@ -15,6 +15,7 @@ from .errors import (BudgetExceededError, ContractViolationError, DeviceError, I
                      StructFFTError)
 from .hidft import ButterflyPlan, HiDftResult, get_plan, hidft, hidft_to_dft, hidft_to_dft_batched
 from .sampling import SamplingPattern, pivoted_pattern, pivoted_pattern_tensor
+from .signals import BandlimitedSignal
 from .sas import SasPlan, SasResult, predicted_cost, sas_transform, select_pivots
 
 __version__ = "0.1.0"

@@ -121,7 +121,7 @@ def get_plan(J: SupportSet, r: tuple[int, ...], height: int, dtype_code: int, de
 
 @dataclass
 class _Src:
-    kind: str               # "device" | "pinned" | "host" | "callable"
+    kind: str               # "device" | "pinned" | "host" | "callable" | "synth"
     tensor: Any = None      # 2-D (B, N) view for device/pinned/host
     batched: bool = False
     dtype_code: int = _lib.C128
@@ -149,6 +149,12 @@ def _prepare_source(source, N: int) -> _Src:
         if t2.is_pinned():
             return _Src("pinned", t2, batched, _DT[t2.dtype], dev)
         return _Src("host", t2.to(dev), batched, _DT[t2.dtype], dev)
+    if hasattr(source, "support") and hasattr(source, "coeffs") and hasattr(source, "sample_block"):
+        # BandlimitedSignal (ours or the reference's): synthesise on the device
+        from .signals import BandlimitedSignal
+        if int(source.N) != N:
+            raise InvalidInputError("signal modulus does not match support")
+        return _Src("synth", None, False, _lib.C128, dev, BandlimitedSignal.from_reference(source))
     if callable(source) or hasattr(source, "sample_block"):
         if hasattr(source, "N") and int(getattr(source, "N")) != N:
             raise InvalidInputError("signal modulus does not match support")
@@ -166,6 +172,22 @@ def _prepare_source(source, N: int) -> _Src:
 
 def _signal_ptr(src: _Src) -> int:
     return src.tensor.data_ptr()
+
+
+def _gathered_samples(src: _Src, plan: "ButterflyPlan", shift: int):
+    """(1, A) complex128 device tensor of the samples at (I - shift) mod N in
+    slot order, for sources that are evaluated rather than stored
+    (hidft.py:36-45): synthesised on the device for a BandlimitedSignal, or
+    the callable's values otherwise."""
+    torch = _torch()
+    N = plan.support.N
+    loc = (plan.tables()["offsets"] - int(shift)) % N
+    if src.kind == "synth":
+        return src.fn.sample_block_tensor(torch.as_tensor(loc, device=src.device)).view(1, -1)
+    vals = np.asarray(src.fn(loc), dtype=np.complex128)
+    if vals.shape != loc.shape:
+        raise InvalidInputError("sample callback returned wrong shape")
+    return torch.from_numpy(vals.reshape(1, -1)).to(src.device)
 
 
 # ----------------------------------------------------------------- result ---
@@ -251,13 +273,8 @@ def hidft(source, J, r: Sequence[int], height: int = 0, shift: int = 0, counter=
     cdt = torch.complex64 if src.dtype_code == _lib.C64 else torch.complex128
     lib = _lib.load()
     stream = _lib.stream_ptr(src.device)
-    if src.kind == "callable":
-        off = plan.tables()["offsets"]
-        loc = (off - int(shift)) % J.N
-        vals = np.asarray(src.fn(loc), dtype=np.complex128)
-        if vals.shape != loc.shape:
-            raise InvalidInputError("sample callback returned wrong shape")
-        samples = torch.from_numpy(vals.reshape(1, -1)).to(src.device)
+    if src.kind in ("callable", "synth"):
+        samples = _gathered_samples(src, plan, shift)
         B = 1
         nodes = torch.empty((B, max(plan.n_nodes, 1)), dtype=cdt, device=src.device)
         slots = torch.empty((B, plan.A), dtype=cdt, device=src.device)

@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from .congruence import SupportSet, as_support, pivots as support_pivots, validate_pivot_vector
 from .errors import InvalidInputError
-from .hidft import _count, _finish, _prepare_source, _torch, get_plan
+from .hidft import _count, _finish, _gathered_samples, _prepare_source, _torch, get_plan
 
 C1 = 1.5  # per-stage butterfly constant (sas.py:38)
 C2 = 6.0  # Vandermonde constant (sas.py:39)
@@ -135,14 +135,19 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
         raise NotImplementedError(
             f"mu*={plan.mu_star} > 1 needs per-node Vandermonde decoding (sas.py:372-398), "
             "not on the device path yet; use r=pivots(J)")
-    if src.kind == "callable":
-        raise InvalidInputError("sas_transform on the device needs a dense signal source")
     cdt = torch.complex64 if src.dtype_code == _lib.C64 else torch.complex128
-    sig = src.tensor
-    B = sig.shape[0]
-    out = torch.empty((B, len(J)), dtype=cdt, device=src.device)
-    _lib.check(_lib.load().sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_SAS,
-                                      out.data_ptr(), len(J), None, 0, _lib.stream_ptr(src.device)))
+    stream = _lib.stream_ptr(src.device)
+    if src.kind in ("callable", "synth"):
+        samples = _gathered_samples(src, plan, 0)
+        out = torch.empty((1, len(J)), dtype=cdt, device=src.device)
+        _lib.check(_lib.load().sfft_hidft_gathered(plan.handle, samples.data_ptr(), 1, plan.A, _lib.OUT_SAS,
+                                                   out.data_ptr(), len(J), None, 0, stream))
+    else:
+        sig = src.tensor
+        B = sig.shape[0]
+        out = torch.empty((B, len(J)), dtype=cdt, device=src.device)
+        _lib.check(_lib.load().sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_SAS,
+                                          out.data_ptr(), len(J), None, 0, stream))
     _count(counter, plan.A, plan.s)
     scale = J.N / plan.A
     if counter is not None and scale != 1.0:
