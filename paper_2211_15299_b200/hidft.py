@@ -369,7 +369,7 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         jt = J if torch.is_tensor(J) else torch.as_tensor(np.asarray(J, dtype=np.int64))
         if jt.dim() != 2 or jt.shape[0] != B:
             raise InvalidInputError("per-signal supports must be a (B, k) tensor")
-        jt = jt.to(run_dev, dtype=torch.int64).contiguous()
+        jt = jt.to(run_dev, dtype=torch.int64, non_blocking=True).contiguous()
         nsup, k = B, jt.shape[1]
         Js = None
     code = _DT[sig.dtype]
