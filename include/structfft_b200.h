@@ -142,6 +142,33 @@ SFFT_API int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const void
 SFFT_API int sfft_synthesize(const int64_t* J, const void* coeffs, int64_t k, int M,
                              const int64_t* locations, int64_t n, void* out, sfft_stream_t stream);
 
+/* Node membership of a plan's decode level (congruence tree, congruence.py:134-214):
+ * offsets[n_nodes+1] and member element indices (ascending J within each node),
+ * host or device buffers, either may be NULL (builds and caches the table). */
+SFFT_API int sfft_plan_nodes(sfft_plan* plan, int32_t* offsets, int32_t* members, sfft_stream_t stream);
+
+/* hidft of shift0 + j for j < nshift (sas.py:343-345) in one launch: output row
+ * b*nshift + j.  in_dtype may be SFFT_C64 with a complex128 plan (promoted on
+ * load, as the reference's float64 path does). */
+SFFT_API int sfft_hidft_shifts(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int in_dtype,
+                               int64_t shift0, int64_t nshift, int out_kind, void* out, int64_t ld_out,
+                               sfft_stream_t stream);
+
+/* Shift-and-sample node decoding for mu* > 1 (sas.py:358-399): nodevals are the
+ * nshift = mu* node outputs per signal (rows b*mu + j); per aliased node a
+ * Bjorck-Pereyra solve with Leja order in float64, the reference's error
+ * estimate, double-double re-measure/re-solve above tol/20, dense LU fallback
+ * above max(tol, 1e-9) residual.  Escalation samples come from the dense
+ * signals (sig), a float64 table in pattern order (table: B x mu x A), or the
+ * band-limited spectra (bl_J[k_src], bl_c[B x k_src] complex128).  out: B x k
+ * complex128 in ascending-J order; flags (1 escalated, 2 dense fallback) and
+ * residuals per (signal, node). */
+SFFT_API int sfft_sas_decode(sfft_plan* plan, const void* nodevals, int64_t ld_nv, int nv_dtype, int64_t B,
+                             int64_t mu, double tol, const void* sig, int64_t ld_sig, int sig_dtype,
+                             const void* table, const int64_t* bl_J, const void* bl_c, int64_t k_src,
+                             const int64_t* J_dev, void* out, int64_t ld_out, int32_t* flags, double* resid,
+                             int64_t* n_escalated, int64_t* n_fallback, sfft_stream_t stream);
+
 /* Fused hidft(f_b, J_b, pivots(J_b)) + hidft_to_dft for homogeneous supports:
  * pivots, pattern, tables and twiddles are derived on chip per CTA, so one
  * launch does plan + gather + butterfly + scaled, ascending-J store.

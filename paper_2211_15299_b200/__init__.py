@@ -16,6 +16,7 @@ from .errors import (BudgetExceededError, ContractViolationError, DeviceError, I
 from .hidft import ButterflyPlan, HiDftResult, get_plan, hidft, hidft_to_dft, hidft_to_dft_batched
 from .sampling import SamplingPattern, pivoted_pattern, pivoted_pattern_tensor
 from .signals import BandlimitedSignal
-from .sas import SasPlan, SasResult, predicted_cost, sas_transform, select_pivots
+from .sas import (CostReport, NodeSystem, SasPlan, SasResult, predicted_cost, sas_transform,
+                  select_pivots)
 
 __version__ = "0.1.0"

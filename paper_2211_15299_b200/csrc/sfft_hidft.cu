@@ -126,8 +126,8 @@ __device__ __forceinline__ void butterfly(Cx<T> (&v)[Geo<T, S>::E], int t, Cx<T>
 // low LE bits of a come from the unrolled register index x, so their part
 // of the offset is a compile-time selection of d_0..d_{LE-1}.  All E loads
 // are issued back to back before any use.
-template <typename T, int S>
-__device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S>::E], int t, const Cx<T>* __restrict__ row,
+template <typename T, int S, typename In = T>
+__device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S>::E], int t, const Cx<In>* __restrict__ row,
                                        const uint32_t (&d)[S > 0 ? S : 1], uint32_t base, uint32_t nmask) {
   using G = Geo<T, S>;
   uint32_t hi = base;
@@ -140,7 +140,8 @@ __device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S>::E], int t, const Cx
 #pragma unroll
     for (int i = 0; i < G::LE; ++i)
       if ((x >> i) & 1) off += d[i];
-    v[x] = load_sample(row + (off & nmask));
+    const Cx<In> s = load_sample(row + (off & nmask));
+    v[x] = Cx<T>{(T)s.x, (T)s.y};  // complex64 input into the fp64 path promotes exactly
   }
 }
 
@@ -161,6 +162,8 @@ struct PlanArgs {
   void* out2;  // optional slot values (identity map)
   int64_t ld2;
   int identity;  // samples already gathered in slot order (row[a] = slot a)
+  int in_c64;    // fp64 plan reading complex64 signals (promoted on load, as hidft.py:46 does)
+  int64_t nshift;  // rows per signal: row r transforms signal r / nshift at shift shift0 + r % nshift
   int debug_skip;  // timing build only: bit0 gather, bit1 scatter, bit2 local stages, bit3 phase 2
 };
 
@@ -179,8 +182,8 @@ k_hidft_plan(const PlanArgs args) {
   Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);
   const int tid = threadIdx.x;
   const int g = tid / G::TPS, t = tid % G::TPS;
-  const int64_t b = (int64_t)blockIdx.x * G::SPC + g;
-  const bool live = b < args.B;
+  const int64_t b = (int64_t)blockIdx.x * G::SPC + g;  // output row
+  const bool live = b < args.B * args.nshift;
   uint32_t d[S > 0 ? S : 1];
 #pragma unroll
   for (int i = 0; i < S; ++i) d[i] = args.identity ? (1u << i) : (1u << (args.M - 1 - args.used[i]));
@@ -188,8 +191,12 @@ k_hidft_plan(const PlanArgs args) {
                                         : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
   Cx<T> v[G::E];
   if (live) {
-    const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
-    gather<T, S>(v, t, row, d, args.identity ? 0u : args.negshift, nmask);
+    const int64_t bs = b / args.nshift;
+    const uint32_t base = args.identity ? 0u : ((args.negshift - (uint32_t)(b % args.nshift)) & nmask);
+    if (sizeof(T) == 8 && args.in_c64)
+      gather<T, S, float>(v, t, reinterpret_cast<const Cx<float>*>(args.sig) + bs * args.ld, d, base, nmask);
+    else
+      gather<T, S>(v, t, reinterpret_cast<const Cx<T>*>(args.sig) + bs * args.ld, d, base, nmask);
   } else {
 #pragma unroll
     for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
@@ -367,22 +374,30 @@ k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
 #undef SFFT_D
   const T scale = (T)args.scale1;
   const int64_t ncl = gridDim.x / C;
-  // gather sorted positions u = x*NT + t of signal bb into v
+  const int64_t nrows = args.B * args.nshift;
+  // gather sorted positions u = x*NT + t of output row bb (signal bb / nshift,
+  // shift shift0 + bb % nshift) into v
   auto gather_sorted = [&](Cx<T>(&v)[G::E], int64_t bb) {
-    const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + bb * args.ld;
+    const int64_t bs = bb / args.nshift;
+    const uint32_t sh = (uint32_t)(bb % args.nshift);
 #pragma unroll
     for (int x = 0; x < G::E; ++x) {
-      uint32_t off = offt;
+      uint32_t off = offt - sh;
 #pragma unroll
       for (int j = 0; j < G::LE; ++j)
         if ((x >> j) & 1) off += dx[j];
-      v[x] = load_sample(row + (off & nmask));
+      if (sizeof(T) == 8 && args.in_c64) {
+        const Cx<float> s = load_sample(reinterpret_cast<const Cx<float>*>(args.sig) + bs * args.ld + (off & nmask));
+        v[x] = Cx<T>{(T)s.x, (T)s.y};
+      } else {
+        v[x] = load_sample(reinterpret_cast<const Cx<T>*>(args.sig) + bs * args.ld + (off & nmask));
+      }
     }
   };
   Cx<T> v[G::E];
-  if (blockIdx.x / C < args.B) gather_sorted(v, blockIdx.x / C);
+  if (blockIdx.x / C < nrows) gather_sorted(v, blockIdx.x / C);
   uint32_t par = 0;
-  for (int64_t b = blockIdx.x / C; b < args.B; b += ncl, par ^= 1u) {
+  for (int64_t b = blockIdx.x / C; b < nrows; b += ncl, par ^= 1u) {
     SFFT_STAMP(0);
     // ---- 0. stage by owner (XOR by owner: conflict-free), push to R1s
 #pragma unroll
@@ -425,7 +440,7 @@ k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
       st_async16(cluster_addr(dst, qd), e0, e1, cluster_addr(mb1, qd));
     }
     // prefetch the next signal's samples: their latency hides behind steps 2-3
-    if (b + ncl < args.B) gather_sorted(v, b + ncl);
+    if (b + ncl < nrows) gather_sorted(v, b + ncl);
     mbar_wait(mb1, par);
     SFFT_STAMP(4);
     if (t == 0) mbar_expect_tx(mb1, BYTES);
@@ -679,7 +694,7 @@ static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {
   int occ = 0;
   int rc = kernel_occupancy(kern, G::NT, smem, &occ);
   if (rc) return rc;
-  const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
+  const int64_t ngroups = (a.B * a.nshift + G::SPC - 1) / G::SPC;
   if (ngroups > 0x7fffffff) return fail(SFFT_ERR_UNSUPPORTED, "batch too large for one launch");
   kern<<<(unsigned)ngroups, G::NT, smem, st>>>(a);
   SFFT_CUDA(cudaGetLastError());
@@ -738,7 +753,7 @@ static int run_cluster_kernel(const PlanArgs& a, const int32_t* inv1, cudaStream
       max_clusters = it->second;
     }
   }
-  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(a.B, max_clusters));
+  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(a.B * a.nshift, max_clusters));
   cfg.gridDim = dim3((unsigned)(ncl * C));
   SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, a, inv1));
   return SFFT_OK;
@@ -810,8 +825,11 @@ static int dispatch_fused(int dtype, int s, const FusedArgs& a, cudaStream_t st)
 
 int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld, int64_t shift,
                       const int32_t* map1, const int32_t* inv1, int64_t n1, double scale1, void* out1,
-                      int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st) {
+                      int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st,
+                      int64_t nshift, int in_c64) {
   PlanArgs a{};
+  a.nshift = nshift > 0 ? nshift : 1;
+  a.in_c64 = in_c64;
   a.identity = identity;
 #ifdef SFFT_PHASE_TIMING
   if (const char* e = getenv("SFFT_DEBUG_SKIP")) a.debug_skip = atoi(e);
@@ -850,8 +868,8 @@ __global__ void k_apply_map(const Cx<T>* __restrict__ in, int64_t B, int64_t ld_
 }
 
 // resolve (map, n_out, scale) for an output kind, checking its contract
-static int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, int64_t* n_out,
-                    double* scale, const int32_t** inv = nullptr) {
+int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, int64_t* n_out, double* scale,
+             const int32_t** inv) {
   const double N = (double)(1ll << plan->M);
   *scale = 1.0;
   const int32_t* dummy;

@@ -482,6 +482,8 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_twiddles);
   cudaFree(p->d_inv_elem);
   cudaFree(p->d_inv_node);
+  cudaFree(p->d_node_off);
+  cudaFree(p->d_node_mem);
   delete p;
 }
 

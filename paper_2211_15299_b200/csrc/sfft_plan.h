@@ -19,12 +19,17 @@ struct sfft_plan {
   void* d_twiddles;          // A-1 complex (dtype), stage-major
   int32_t* d_inv_elem;       // A   slot -> support element (-1: virtual); unique when mu* = 1
   int32_t* d_inv_node;       // A   slot -> node rank (-1: virtual)
+  int32_t* d_node_off;       // n_nodes+1  node membership CSR (built on first SAS decode)
+  int32_t* d_node_mem;       // k          member element indices, ascending per node
 };
 
 namespace sfft {
 // transform launchers (sfft_hidft.cu)
 int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld, int64_t shift,
                       const int32_t* map1, const int32_t* inv1, int64_t n1, double scale1, void* out1,
-                      int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st);
+                      int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st,
+                      int64_t nshift = 1, int in_c64 = 0);
 int max_supported_s(int dtype);
+int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, int64_t* n_out, double* scale,
+             const int32_t** inv = nullptr);
 }  // namespace sfft

@@ -1,0 +1,683 @@
+// Shift-and-sample decoding on the device for mu* > 1 (reference sas.py).
+//
+//   (N/|I|) * Hidft(tau^j f)(v) = sum_{l in v} Ff(l) x_l^j,  x_l = e^{-2 pi i l/N}
+//
+// for j < m_v (the node's weight), one Vandermonde system per aliased node v
+// at the decode level (sas.py:1-12).  The mu* shifted Hi-DFTs run as one
+// launch of the transform kernels (B*mu* rows).  This file decodes:
+//   * Bjorck-Pereyra with Leja ordering in float64 (sas.py:135-203), the
+//     reference's forward-error estimate (sas.py:214-235);
+//   * nodes estimated above tolerance/20 are re-measured and re-solved in
+//     double-double (sas.py:290-310, _ddc.py), with double-double roots
+//     computed on the device (Taylor series after exact reduction) in the
+//     reference's coarse x fine table layout (_ddc.py:151-205);
+//   * non-escalated nodes whose residual exceeds max(tol, 1e-9) fall back to
+//     a dense LU solve with partial pivoting (sas.py:386-395).
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "sfft_common.cuh"
+#include "sfft_plan.h"
+
+namespace sfft {
+
+constexpr int kMaxMu = 64;  // largest node weight the device decoder handles
+
+// ------------------------------------------------------ double-double ---
+// Same formulas as _ddc.py (no FMA contraction: explicit _rn intrinsics);
+// two_prod uses the exact FMA error term (equal to Dekker's split result).
+struct dd {
+  double hi, lo;
+};
+struct cdd {
+  dd re, im;
+};
+
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  const double err = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, err};
+}
+__device__ __forceinline__ dd quick_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+  const double p = __dmul_rn(a, b);
+  return {p, fma(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add(dd x, dd y) {
+  const dd s = two_sum(x.hi, y.hi);
+  const double e = __dadd_rn(__dadd_rn(s.lo, x.lo), y.lo);
+  return quick_two_sum(s.hi, e);
+}
+__device__ __forceinline__ dd dd_neg(dd x) { return {-x.hi, -x.lo}; }
+__device__ __forceinline__ dd dd_sub(dd x, dd y) { return dd_add(x, dd_neg(y)); }
+__device__ __forceinline__ dd dd_mul(dd x, dd y) {
+  const dd p = two_prod(x.hi, y.hi);
+  const double e = __dadd_rn(__dadd_rn(p.lo, __dmul_rn(x.hi, y.lo)), __dmul_rn(x.lo, y.hi));
+  return quick_two_sum(p.hi, e);
+}
+__device__ __forceinline__ dd dd_mul_f(dd x, double f) {
+  const dd p = two_prod(x.hi, f);
+  return quick_two_sum(p.hi, __dadd_rn(p.lo, __dmul_rn(x.lo, f)));
+}
+__device__ __forceinline__ dd dd_div(dd x, dd y) {
+  const double q1 = __ddiv_rn(x.hi, y.hi);
+  dd r = dd_sub(x, dd_mul_f(y, q1));
+  const double q2 = __ddiv_rn(r.hi, y.hi);
+  r = dd_sub(r, dd_mul_f(y, q2));
+  const double q3 = __ddiv_rn(r.hi, y.hi);
+  return dd_add(quick_two_sum(q1, q2), dd{q3, 0.0});
+}
+__device__ __forceinline__ cdd cdd_add(cdd u, cdd v) { return {dd_add(u.re, v.re), dd_add(u.im, v.im)}; }
+__device__ __forceinline__ cdd cdd_sub(cdd u, cdd v) { return {dd_sub(u.re, v.re), dd_sub(u.im, v.im)}; }
+__device__ __forceinline__ cdd cdd_mul(cdd u, cdd v) {
+  return {dd_sub(dd_mul(u.re, v.re), dd_mul(u.im, v.im)), dd_add(dd_mul(u.re, v.im), dd_mul(u.im, v.re))};
+}
+__device__ __forceinline__ cdd cdd_mul_complex(cdd u, double a, double b) {
+  return {dd_sub(dd_mul_f(u.re, a), dd_mul_f(u.im, b)), dd_add(dd_mul_f(u.re, b), dd_mul_f(u.im, a))};
+}
+__device__ __forceinline__ cdd cdd_div(cdd u, cdd v) {
+  const dd den = dd_add(dd_mul(v.re, v.re), dd_mul(v.im, v.im));
+  const dd re = dd_add(dd_mul(u.re, v.re), dd_mul(u.im, v.im));
+  const dd im = dd_sub(dd_mul(u.im, v.re), dd_mul(u.re, v.im));
+  return {dd_div(re, den), dd_div(im, den)};
+}
+
+// e^{+2 pi i t / D} in double-double, D a power of two, 0 <= t < D.
+// Exact reduction: 4t/D = q + r exactly; angle = q*pi/2 + r*pi/2, reflected
+// to phi = (pi/2) * min(r, 1-r) in [0, pi/4]; Taylor series to 1e-33.
+__device__ cdd dd_root(uint64_t t, int logD) {
+  const dd PIO2 = {1.5707963267948966, 6.123233995736766e-17};
+  const double v4 = ldexp((double)t, 2 - logD);  // 4t/D, exact
+  const int q = (int)floor(v4);
+  double r = v4 - (double)q;
+  const bool refl = r > 0.5;
+  if (refl) r = 1.0 - r;
+  const dd phi = dd_mul_f(PIO2, r);
+  const dd x2 = dd_mul(phi, phi);
+  dd s = phi, c = {1.0, 0.0}, ts = phi, tc = {1.0, 0.0};
+  for (int n = 1; n <= 15; ++n) {
+    ts = dd_div(dd_mul(ts, x2), dd{(double)((2 * n) * (2 * n + 1)), 0.0});
+    tc = dd_div(dd_mul(tc, x2), dd{(double)((2 * n - 1) * (2 * n)), 0.0});
+    if (n & 1) {
+      s = dd_sub(s, ts);
+      c = dd_sub(c, tc);
+    } else {
+      s = dd_add(s, ts);
+      c = dd_add(c, tc);
+    }
+  }
+  dd cs = refl ? s : c, sn = refl ? c : s;  // cos/sin of (pi/2) r
+  switch (q & 3) {
+    case 0: return {cs, sn};
+    case 1: return {dd_neg(sn), cs};
+    case 2: return {dd_neg(cs), dd_neg(sn)};
+    default: return {sn, dd_neg(cs)};
+  }
+}
+
+// root table of _ddc.py:151-205: fine[s] = e^{2 pi i s / N}, s < 2^h;
+// coarse[q] = e^{2 pi i q / 2^(M-h)}; root(t) = coarse[t >> h] * fine[t & (2^h-1)]
+__global__ void k_root_tables(cdd* __restrict__ fine, cdd* __restrict__ coarse, int M) {
+  const int h = M / 2;
+  const int64_t nf = 1ll << h, nc = 1ll << (M - h);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf + nc; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nf) fine[i] = dd_root((uint64_t)i, M);
+    else coarse[i - nf] = dd_root((uint64_t)(i - nf), M - h);
+  }
+}
+
+struct RootTab {
+  const cdd* fine;
+  const cdd* coarse;
+  int h;
+  uint64_t nmask;
+  __device__ __forceinline__ cdd get(uint64_t t) const {
+    t &= nmask;
+    return cdd_mul(coarse[t >> h], fine[t & ((1ull << h) - 1)]);
+  }
+};
+
+// ------------------------------------------------ float64 node decoding ---
+struct C64x {  // complex double with plain arithmetic (reference numpy complex128)
+  double x, y;
+};
+__device__ __forceinline__ C64x cm(C64x a, C64x b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ C64x cs(C64x a, C64x b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ C64x cdv(C64x a, C64x b) {
+  // numpy complex division (Smith's algorithm)
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double rat = b.y / b.x, scl = 1.0 / (b.x + b.y * rat);
+    return {(a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl};
+  }
+  const double rat = b.x / b.y, scl = 1.0 / (b.y + b.x * rat);
+  return {(a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl};
+}
+__device__ __forceinline__ double cabs2(C64x a) { return hypot(a.x, a.y); }
+
+// sas.py:153-163 on nodes x[perm]
+__device__ void bp_core(const C64x* x, const int* perm, C64x* c, int n) {
+  for (int k = 0; k < n - 1; ++k)
+    for (int j = n - 1; j > k; --j) c[j] = cs(c[j], cm(x[perm[k]], c[j - 1]));
+  for (int k = n - 2; k >= 0; --k) {
+    for (int j = k + 1; j < n; ++j) c[j] = cdv(c[j], cs(x[perm[j]], x[perm[j - k - 1]]));
+    for (int j = k; j < n - 1; ++j) c[j] = cs(c[j], c[j + 1]);
+  }
+}
+
+// sas.py:135-150
+__device__ void leja_order(const C64x* x, int n, int* order) {
+  double prod[kMaxMu];
+  bool chosen[kMaxMu];
+  int i0 = 0;
+  double best = -1.0;
+  for (int i = 0; i < n; ++i) {
+    const double a = cabs2(x[i]);
+    if (a > best) { best = a; i0 = i; }
+    chosen[i] = false;
+  }
+  order[0] = i0;
+  chosen[i0] = true;
+  for (int i = 0; i < n; ++i) prod[i] = cabs2(cs(x[i], x[i0]));
+  for (int t = 1; t < n; ++t) {
+    int ib = 0;
+    double pb = -2.0;
+    for (int i = 0; i < n; ++i) {
+      const double pm = chosen[i] ? -1.0 : prod[i];
+      if (pm > pb) { pb = pm; ib = i; }
+    }
+    order[t] = ib;
+    chosen[ib] = true;
+    for (int i = 0; i < n; ++i) prod[i] *= cabs2(cs(x[i], x[ib]));
+  }
+}
+
+// vandermonde_solve (sas.py:166-203): c[perm] = bp_core(x[perm], y)
+__device__ void vandermonde_solve(const C64x* x, const C64x* y, int n, const int* perm, C64x* out) {
+  C64x c[kMaxMu];
+  for (int i = 0; i < n; ++i) c[i] = y[i];
+  bp_core(x, perm, c, n);
+  for (int i = 0; i < n; ++i) out[perm[i]] = c[i];
+}
+
+__device__ void forward_apply(const C64x* x, const C64x* c, int n, C64x* out) {
+  for (int j = 0; j < n; ++j) {
+    C64x acc = {0.0, 0.0};
+    for (int m = 0; m < n; ++m) {
+      C64x p = {1.0, 0.0};
+      for (int e = 0; e < j; ++e) p = cm(p, x[m]);
+      acc = {acc.x + (p.x * c[m].x - p.y * c[m].y), acc.y + (p.x * c[m].y + p.y * c[m].x)};
+    }
+    out[j] = acc;
+  }
+}
+
+struct SasDecodeArgs {
+  const void* nodevals;  // (B*mu) rows x n_nodes, row r = signal r/mu, shift r%mu
+  int64_t ld_nv;
+  int nv_c64;
+  int64_t B, mu, n_nodes, k;
+  int M;
+  double scale, tol;
+  const int32_t* node_off;  // n_nodes+1
+  const int32_t* node_mem;  // k element indices
+  const int64_t* J;         // k support indices
+  void* out;                // B x k complex128
+  int64_t ld_out;
+  int32_t* flags;  // B x n_nodes: bit0 escalate, bit1 dense fallback
+  double* resid;   // B x n_nodes residual (sas.py:386-388)
+};
+
+__device__ __forceinline__ C64x nodeval(const SasDecodeArgs& a, int64_t row, int64_t node) {
+  if (a.nv_c64) {
+    const float2 v = reinterpret_cast<const float2*>(a.nodevals)[row * a.ld_nv + node];
+    return {(double)v.x, (double)v.y};
+  }
+  const double2 v = reinterpret_cast<const double2*>(a.nodevals)[row * a.ld_nv + node];
+  return {v.x, v.y};
+}
+
+// one thread per (signal, node)
+__global__ void k_sas_decode_f64(const SasDecodeArgs a) {
+  const int64_t total = a.B * a.n_nodes;
+  const double N = ldexp(1.0, a.M);
+  const double noise_eps = 100.0 * 2.220446049250313e-16;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = id / a.n_nodes, v = id % a.n_nodes;
+    const int off = a.node_off[v], m = a.node_off[v + 1] - off;
+    C64x* out = reinterpret_cast<C64x*>(a.out) + b * a.ld_out;
+    if (m == 1) {
+      const C64x raw = nodeval(a, b * a.mu, v);
+      out[a.node_mem[off]] = a.scale == 1.0 ? raw : C64x{raw.x * a.scale, raw.y * a.scale};
+      a.flags[id] = 0;
+      a.resid[id] = 0.0;
+      continue;
+    }
+    C64x x[kMaxMu], y[kMaxMu], c[kMaxMu], r[kMaxMu], d[kMaxMu];
+    int perm[kMaxMu];
+    for (int j = 0; j < m; ++j) {
+      const C64x raw = nodeval(a, b * a.mu + j, v);
+      y[j] = {raw.x * a.scale, raw.y * a.scale};
+      const double l = (double)a.J[a.node_mem[off + j]];
+      double sn, co;
+      sincospi(-2.0 * l / N, &sn, &co);  // x_l = e^{-2 pi i l / N}
+      x[j] = {co, sn};
+    }
+    if (m >= 3) {
+      leja_order(x, m, perm);
+    } else {
+      for (int i = 0; i < m; ++i) perm[i] = i;
+    }
+    vandermonde_solve(x, y, m, perm, c);
+    // forward-error estimate (sas.py:214-235)
+    double cmax = 0.0, ymax = 0.0;
+    for (int i = 0; i < m; ++i) {
+      cmax = fmax(cmax, cabs2(c[i]));
+      ymax = fmax(ymax, cabs2(y[i]));
+    }
+    const double denom = fmax(cmax, 1e-300);
+    forward_apply(x, c, m, r);
+    for (int j = 0; j < m; ++j) r[j] = cs(r[j], y[j]);
+    vandermonde_solve(x, r, m, perm, d);
+    double dmax = 0.0;
+    for (int i = 0; i < m; ++i) dmax = fmax(dmax, cabs2(d[i]));
+    double est = dmax / denom;
+    // ||inv(V)||_inf from the columns inv(V) e_j (V[j][m] = x_m^j)
+    double rows[kMaxMu];
+    for (int i = 0; i < m; ++i) rows[i] = 0.0;
+    for (int j = 0; j < m; ++j) {
+      for (int i = 0; i < m; ++i) r[i] = {i == j ? 1.0 : 0.0, 0.0};
+      vandermonde_solve(x, r, m, perm, d);
+      for (int i = 0; i < m; ++i) rows[i] += cabs2(d[i]);
+    }
+    double amp = 0.0;
+    for (int i = 0; i < m; ++i) amp = fmax(amp, rows[i]);
+    est = fmax(est, amp * noise_eps * ymax / denom);
+    int flag = 0;
+    double res = 0.0;
+    if (!(est <= a.tol / 20.0)) {
+      flag = 1;  // escalate to double-double
+    } else {
+      forward_apply(x, c, m, r);
+      double num = 0.0, den = 0.0;
+      for (int j = 0; j < m; ++j) {
+        const C64x e = cs(r[j], y[j]);
+        num += e.x * e.x + e.y * e.y;
+        den += y[j].x * y[j].x + y[j].y * y[j].y;
+      }
+      res = sqrt(num) / fmax(sqrt(den), 1e-300);
+      if (res > fmax(a.tol, 1e-9)) flag = 2;
+    }
+    for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = c[i];
+    a.flags[id] = flag;
+    a.resid[id] = res;
+  }
+}
+
+// --------------------------------------------- double-double escalation ---
+struct SasDDArgs {
+  SasDecodeArgs base;
+  RootTab tab;
+  const int64_t* pattern;  // sorted I_r, A entries
+  int64_t A;
+  const int32_t* node_res;  // residues (n_nodes)
+  // samples: dense source (promoted) or precomputed dd samples (band-limited)
+  const void* sig;
+  int64_t ld_sig;
+  int sig_c64;
+  const cdd* samples_dd;  // (B x mu x A) at (pattern_i - j) mod N, or NULL
+  const double2* table;   // same layout in float64 (callable sources), or NULL
+  const int32_t* work;    // escalated (signal, node) ids
+  int64_t n_work;
+};
+
+__device__ __forceinline__ cdd dd_sample(const SasDDArgs& a, int64_t b, int64_t j, int64_t i) {
+  if (a.samples_dd) return a.samples_dd[(b * a.base.mu + j) * a.A + i];
+  if (a.table) {
+    const double2 v = a.table[(b * a.base.mu + j) * a.A + i];
+    return {{v.x, 0.0}, {v.y, 0.0}};
+  }
+  const uint64_t loc = ((uint64_t)a.pattern[i] - (uint64_t)j) & a.tab.nmask;
+  if (a.sig_c64) {
+    const float2 v = reinterpret_cast<const float2*>(a.sig)[b * a.ld_sig + loc];
+    return {{(double)v.x, 0.0}, {(double)v.y, 0.0}};
+  }
+  const double2 v = reinterpret_cast<const double2*>(a.sig)[b * a.ld_sig + loc];
+  return {{v.x, 0.0}, {v.y, 0.0}};
+}
+
+// one thread per escalated node: re-measure (sas.py:290-310) and solve in dd
+__global__ void k_sas_decode_dd(const SasDDArgs a) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < a.n_work; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = a.work[w];
+    const SasDecodeArgs& s = a.base;
+    const int64_t b = id / s.n_nodes, v = id % s.n_nodes;
+    const int off = s.node_off[v], m = s.node_off[v + 1] - off;
+    const uint64_t resid = (uint64_t)(int64_t)a.node_res[v];
+    cdd y[kMaxMu];
+    for (int j = 0; j < m; ++j) {
+      cdd acc = {{0.0, 0.0}, {0.0, 0.0}};
+      for (int64_t i = 0; i < a.A; ++i) {
+        const cdd kern = a.tab.get((uint64_t)(-(int64_t)(resid * (uint64_t)a.pattern[i])));
+        acc = cdd_add(acc, cdd_mul(dd_sample(a, b, j, i), kern));
+      }
+      y[j] = cdd_mul_complex(acc, s.scale, 0.0);
+    }
+    // solve_vandermonde_dd (_ddc.py:235-254): x_m = root((-l) mod N), BP, no Leja
+    cdd x[kMaxMu];
+    for (int i = 0; i < m; ++i) x[i] = a.tab.get((uint64_t)(-(int64_t)s.J[s.node_mem[off + i]]));
+    for (int k = 0; k < m - 1; ++k)
+      for (int j = m - 1; j > k; --j) y[j] = cdd_sub(y[j], cdd_mul(x[k], y[j - 1]));
+    for (int k = m - 2; k >= 0; --k) {
+      for (int j = k + 1; j < m; ++j) y[j] = cdd_div(y[j], cdd_sub(x[j], x[j - k - 1]));
+      for (int j = k; j < m - 1; ++j) y[j] = cdd_sub(y[j], y[j + 1]);
+    }
+    C64x* out = reinterpret_cast<C64x*>(s.out) + b * s.ld_out;
+    for (int i = 0; i < m; ++i)
+      out[s.node_mem[off + i]] = {__dadd_rn(y[i].re.hi, y[i].re.lo), __dadd_rn(y[i].im.hi, y[i].im.lo)};
+  }
+}
+
+// band-limited source: dd samples at (pattern_i - j) mod N for j < mu (synthesize_dd, _ddc.py:212-224)
+__global__ void k_dd_samples(RootTab tab, const int64_t* __restrict__ pattern, int64_t A, int64_t mu,
+                             const int64_t* __restrict__ Jsrc, const double2* __restrict__ csrc, int64_t ksrc,
+                             int M, const int32_t* __restrict__ sigs, int64_t nsig, cdd* __restrict__ out) {
+  const int64_t total = nsig * mu * A;
+  const double invN = ldexp(1.0, -M);
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = id % A, j = (id / A) % mu, sidx = id / (A * mu);
+    const int64_t bsig = sigs[sidx];
+    const uint64_t loc = ((uint64_t)pattern[i] - (uint64_t)j) & tab.nmask;
+    const int64_t* Jb = Jsrc;
+    const double2* cb = csrc + bsig * ksrc;
+    cdd acc = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t e = 0; e < ksrc; ++e)
+      acc = cdd_add(acc, cdd_mul_complex(tab.get(loc * (uint64_t)Jb[e]), cb[e].x, cb[e].y));
+    out[(bsig * mu + j) * A + i] = cdd_mul_complex(acc, invN, 0.0);
+  }
+}
+
+// dense fallback (sas.py:389-395): LU with partial pivoting of V (V[j][m] = x_m^j)
+__global__ void k_sas_dense(const SasDecodeArgs a, const int32_t* __restrict__ work, int64_t n_work,
+                            C64x* __restrict__ scratch) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_work; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = work[w];
+    const int64_t b = id / a.n_nodes, v = id % a.n_nodes;
+    const int off = a.node_off[v], m = a.node_off[v + 1] - off;
+    const double N = ldexp(1.0, a.M);
+    C64x* V = scratch + w * kMaxMu * kMaxMu;
+    C64x rhs[kMaxMu], x[kMaxMu];
+    for (int i = 0; i < m; ++i) {
+      double sn, co;
+      sincospi(-2.0 * (double)a.J[a.node_mem[off + i]] / N, &sn, &co);
+      x[i] = {co, sn};
+    }
+    for (int j = 0; j < m; ++j) {
+      const C64x raw = nodeval(a, b * a.mu + j, v);
+      rhs[j] = {raw.x * a.scale, raw.y * a.scale};
+      for (int i = 0; i < m; ++i) {
+        C64x p = {1.0, 0.0};
+        for (int e = 0; e < j; ++e) p = cm(p, x[i]);
+        V[j * m + i] = p;
+      }
+    }
+    for (int col = 0; col < m; ++col) {
+      int piv = col;
+      double best = cabs2(V[col * m + col]);
+      for (int r = col + 1; r < m; ++r)
+        if (cabs2(V[r * m + col]) > best) { best = cabs2(V[r * m + col]); piv = r; }
+      if (piv != col) {
+        for (int c2 = 0; c2 < m; ++c2) {
+          const C64x t = V[col * m + c2];
+          V[col * m + c2] = V[piv * m + c2];
+          V[piv * m + c2] = t;
+        }
+        const C64x t = rhs[col];
+        rhs[col] = rhs[piv];
+        rhs[piv] = t;
+      }
+      for (int r = col + 1; r < m; ++r) {
+        const C64x f = cdv(V[r * m + col], V[col * m + col]);
+        for (int c2 = col; c2 < m; ++c2) V[r * m + c2] = cs(V[r * m + c2], cm(f, V[col * m + c2]));
+        rhs[r] = cs(rhs[r], cm(f, rhs[col]));
+      }
+    }
+    C64x* out = reinterpret_cast<C64x*>(a.out) + b * a.ld_out;
+    C64x sol[kMaxMu];
+    for (int r = m - 1; r >= 0; --r) {
+      C64x acc = rhs[r];
+      for (int c2 = r + 1; c2 < m; ++c2) acc = cs(acc, cm(V[r * m + c2], sol[c2]));
+      sol[r] = cdv(acc, V[r * m + r]);
+    }
+    for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = sol[i];
+  }
+}
+
+// node membership in CSR form, members ascending (deterministic: per round
+// every node claims its smallest unclaimed member)
+__global__ void k_node_counts(const int32_t* __restrict__ slot_count_src, const int32_t* __restrict__ node_slots,
+                              int64_t n_nodes, int32_t* __restrict__ off) {
+  // single CTA exclusive scan of the node weights
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n_nodes; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    __shared__ int32_t buf[1024];
+    buf[threadIdx.x] = i < n_nodes ? slot_count_src[node_slots[i]] : 0;
+    __syncthreads();
+    for (int d = 1; d < (int)blockDim.x; d <<= 1) {
+      const int32_t add = threadIdx.x >= (unsigned)d ? buf[threadIdx.x - d] : 0;
+      __syncthreads();
+      buf[threadIdx.x] += add;
+      __syncthreads();
+    }
+    const int32_t incl = buf[threadIdx.x];
+    const int32_t c0 = carry;
+    const int32_t w = i < n_nodes ? slot_count_src[node_slots[i]] : 0;
+    if (i < n_nodes) off[i] = c0 + incl - w;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = c0 + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[n_nodes] = carry;
+}
+
+__global__ void k_slot_counts(const int32_t* __restrict__ pats, int64_t k, int32_t* __restrict__ count) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&count[pats[e]], 1);
+}
+
+__global__ void k_member_round(const int32_t* __restrict__ pats, const int32_t* __restrict__ inv_node, int64_t k,
+                               uint8_t* __restrict__ taken, int32_t* __restrict__ cand) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x)
+    if (!taken[e]) atomicMin(&cand[inv_node[pats[e]]], (int32_t)e);
+}
+__global__ void k_member_take(int32_t* __restrict__ cand, const int32_t* __restrict__ off, int64_t n_nodes, int round,
+                              uint8_t* __restrict__ taken, int32_t* __restrict__ mem) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_nodes; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e = cand[v];
+    if (e != 0x7fffffff) {
+      mem[off[v] + round] = e;
+      taken[e] = 1;
+      cand[v] = 0x7fffffff;
+    }
+  }
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+static int grid_for(int64_t n, int threads = 128) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)num_sms() * 32));
+}
+
+}  // namespace sfft
+
+using namespace sfft;
+
+// node CSR (offsets n_nodes+1, members k) for a plan; cached on the plan
+extern "C" int sfft_plan_nodes(sfft_plan* p, int32_t* off_out, int32_t* mem_out, sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!p) return fail(SFFT_ERR_INVALID, "null plan");
+  if (!p->d_node_off) {
+    int32_t *cnt = nullptr, *cand = nullptr;
+    uint8_t* taken = nullptr;
+    SFFT_CUDA(cudaMalloc(&p->d_node_off, 4 * (p->n_nodes + 1)));
+    SFFT_CUDA(cudaMalloc(&p->d_node_mem, 4 * std::max<int64_t>(p->k, 1)));
+    SFFT_CUDA(cudaMallocAsync(&cnt, 4 * p->A, st));
+    SFFT_CUDA(cudaMallocAsync(&cand, 4 * std::max<int64_t>(p->n_nodes, 1), st));
+    SFFT_CUDA(cudaMallocAsync(&taken, std::max<int64_t>(p->k, 1), st));
+    SFFT_CUDA(cudaMemsetAsync(cnt, 0, 4 * p->A, st));
+    k_fill_i32<<<grid_for(p->n_nodes), 128, 0, st>>>(cand, p->n_nodes, 0x7fffffff);
+    SFFT_CUDA(cudaMemsetAsync(taken, 0, p->k, st));
+    k_slot_counts<<<grid_for(p->k, 256), 256, 0, st>>>(p->d_element_slots, p->k, cnt);
+    k_node_counts<<<1, 1024, 0, st>>>(cnt, p->d_node_slots, p->n_nodes, p->d_node_off);
+    for (int64_t round = 0; round < p->mu_star; ++round) {
+      k_member_round<<<grid_for(p->k, 256), 256, 0, st>>>(p->d_element_slots, p->d_inv_node, p->k, taken, cand);
+      k_member_take<<<grid_for(p->n_nodes), 128, 0, st>>>(cand, p->d_node_off, p->n_nodes, (int)round, taken,
+                                                          p->d_node_mem);
+    }
+    SFFT_CUDA(cudaGetLastError());
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(cand, st);
+    cudaFreeAsync(taken, st);
+  }
+  if (off_out) SFFT_CUDA(cudaMemcpyAsync(off_out, p->d_node_off, 4 * (p->n_nodes + 1), cudaMemcpyDefault, st));
+  if (mem_out) SFFT_CUDA(cudaMemcpyAsync(mem_out, p->d_node_mem, 4 * p->k, cudaMemcpyDefault, st));
+  if (off_out || mem_out) SFFT_CUDA(cudaStreamSynchronize(st));
+  return SFFT_OK;
+}
+
+// the mu* shifted Hi-DFTs of sas.py:343-345 in one launch: rows b*nshift + j
+extern "C" int sfft_hidft_shifts(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int in_dtype,
+                                 int64_t shift0, int64_t nshift, int out_kind, void* out, int64_t ld_out,
+                                 sfft_stream_t stream) {
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (nshift < 1) return fail(SFFT_ERR_INVALID, "nshift must be >= 1");
+  if (in_dtype != plan->dtype && !(in_dtype == SFFT_C64 && plan->dtype == SFFT_C128))
+    return fail(SFFT_ERR_INVALID, "complex128 signals need a complex128 plan");
+  if (B == 0) return SFFT_OK;
+  const int32_t *map = nullptr, *inv = nullptr;
+  int64_t n_out = 0;
+  double scale = 1.0;
+  int rc = out_spec(plan, out_kind, &map, &n_out, &scale, &inv);
+  if (rc) return rc;
+  if (ld < (1ll << plan->M) || ld_out < n_out) return fail(SFFT_ERR_INVALID, "row stride too small");
+  return launch_hidft_plan(plan, signals, B, ld, shift0, map, inv, n_out, scale, out, ld_out, nullptr, 0, 0,
+                           (cudaStream_t)stream, nshift, in_dtype != plan->dtype);
+}
+
+// decode: nodevals (B*mu rows) -> out (B x k complex128); flags/resid per (signal, node).
+// source for escalation: dense signals (sig, ld_sig, sig_dtype) or, when
+// bl_J != NULL, band-limited spectra (bl_J[k_src], bl_c[B x k_src] complex128).
+// Returns counts through n_escalated / n_fallback.
+extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv, int nv_dtype, int64_t B,
+                               int64_t mu, double tol, const void* sig, int64_t ld_sig, int sig_dtype,
+                               const void* table, const int64_t* bl_J, const void* bl_c, int64_t k_src,
+                               const int64_t* J_dev,
+                               void* out, int64_t ld_out, int32_t* flags, double* resid, int64_t* n_escalated,
+                               int64_t* n_fallback, sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!p) return fail(SFFT_ERR_INVALID, "null plan");
+  if (p->height != 0) return fail(SFFT_ERR_CONTRACT, "sas decode needs height 0");
+  if (mu != p->mu_star) return fail(SFFT_ERR_INVALID, "mu must equal the plan's mu*");
+  if (mu > kMaxMu) return fail(SFFT_ERR_UNSUPPORTED, "node weight above " + std::to_string(kMaxMu));
+  int rc = sfft_plan_nodes(p, nullptr, nullptr, stream);
+  if (rc) return rc;
+  SasDecodeArgs a{};
+  a.nodevals = nodevals;
+  a.ld_nv = ld_nv;
+  a.nv_c64 = nv_dtype == SFFT_C64;
+  a.B = B;
+  a.mu = mu;
+  a.n_nodes = p->n_nodes;
+  a.k = p->k;
+  a.M = p->M;
+  a.scale = ldexp(1.0, p->M) / (double)p->A;
+  a.tol = tol;
+  a.node_off = p->d_node_off;
+  a.node_mem = p->d_node_mem;
+  a.J = J_dev;
+  a.out = out;
+  a.ld_out = ld_out;
+  a.flags = flags;
+  a.resid = resid;
+  k_sas_decode_f64<<<grid_for(B * p->n_nodes), 128, 0, st>>>(a);
+  SFFT_CUDA(cudaGetLastError());
+  std::vector<int32_t> hf(B * p->n_nodes);
+  SFFT_CUDA(cudaMemcpyAsync(hf.data(), flags, 4 * hf.size(), cudaMemcpyDeviceToHost, st));
+  SFFT_CUDA(cudaStreamSynchronize(st));
+  std::vector<int32_t> esc, fb;
+  std::vector<int32_t> esc_sigs;
+  for (int64_t i = 0; i < (int64_t)hf.size(); ++i) {
+    if (hf[i] == 1) esc.push_back((int32_t)i);
+    if (hf[i] == 2) fb.push_back((int32_t)i);
+  }
+  *n_escalated = (int64_t)esc.size();
+  *n_fallback = (int64_t)fb.size();
+  if (!esc.empty()) {
+    const int M = p->M, h = M / 2;
+    cdd *fine = nullptr, *coarse = nullptr, *samples = nullptr;
+    int64_t* pattern = nullptr;
+    int32_t *work = nullptr, *sigs = nullptr;
+    SFFT_CUDA(cudaMallocAsync(&fine, sizeof(cdd) * (1ll << h), st));
+    SFFT_CUDA(cudaMallocAsync(&coarse, sizeof(cdd) * (1ll << (M - h)), st));
+    SFFT_CUDA(cudaMallocAsync(&pattern, 8 * p->A, st));
+    SFFT_CUDA(cudaMallocAsync(&work, 4 * esc.size(), st));
+    SFFT_CUDA(cudaMemcpyAsync(work, esc.data(), 4 * esc.size(), cudaMemcpyHostToDevice, st));
+    k_root_tables<<<grid_for((1ll << h) + (1ll << (M - h))), 128, 0, st>>>(fine, coarse, M);
+    rc = sfft_pivoted_pattern(p->used, p->s, M, pattern, stream);
+    if (rc) return rc;
+    SasDDArgs d{};
+    d.base = a;
+    d.tab = RootTab{fine, coarse, h, (1ull << M) - 1};
+    d.pattern = pattern;
+    d.A = p->A;
+    d.node_res = p->d_node_residues;
+    d.sig = sig;
+    d.ld_sig = ld_sig;
+    d.sig_c64 = sig_dtype == SFFT_C64;
+    d.table = (const double2*)table;
+    d.work = work;
+    d.n_work = (int64_t)esc.size();
+    if (bl_J) {  // band-limited: dd samples for the signals that escalated
+      std::vector<int32_t> s2;
+      for (int32_t id : esc) s2.push_back((int32_t)(id / p->n_nodes));
+      s2.erase(std::unique(s2.begin(), s2.end()), s2.end());
+      SFFT_CUDA(cudaMallocAsync(&sigs, 4 * s2.size(), st));
+      SFFT_CUDA(cudaMemcpyAsync(sigs, s2.data(), 4 * s2.size(), cudaMemcpyHostToDevice, st));
+      SFFT_CUDA(cudaMallocAsync(&samples, sizeof(cdd) * B * mu * p->A, st));
+      k_dd_samples<<<grid_for((int64_t)s2.size() * mu * p->A), 128, 0, st>>>(
+          d.tab, pattern, p->A, mu, bl_J, (const double2*)bl_c, k_src, M, sigs, (int64_t)s2.size(), samples);
+      d.samples_dd = samples;
+    }
+    k_sas_decode_dd<<<grid_for(d.n_work, 32), 32, 0, st>>>(d);
+    SFFT_CUDA(cudaGetLastError());
+    cudaFreeAsync(fine, st);
+    cudaFreeAsync(coarse, st);
+    cudaFreeAsync(pattern, st);
+    cudaFreeAsync(work, st);
+    if (sigs) cudaFreeAsync(sigs, st);
+    if (samples) cudaFreeAsync(samples, st);
+  }
+  if (!fb.empty()) {
+    int32_t* work = nullptr;
+    C64x* scratch = nullptr;
+    SFFT_CUDA(cudaMallocAsync(&work, 4 * fb.size(), st));
+    SFFT_CUDA(cudaMemcpyAsync(work, fb.data(), 4 * fb.size(), cudaMemcpyHostToDevice, st));
+    SFFT_CUDA(cudaMallocAsync(&scratch, sizeof(C64x) * kMaxMu * kMaxMu * fb.size(), st));
+    k_sas_dense<<<grid_for((int64_t)fb.size(), 32), 32, 0, st>>>(a, work, (int64_t)fb.size(), scratch);
+    SFFT_CUDA(cudaGetLastError());
+    cudaFreeAsync(work, st);
+    cudaFreeAsync(scratch, st);
+  }
+  return SFFT_OK;
+}

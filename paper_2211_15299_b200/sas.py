@@ -1,12 +1,15 @@
-"""Shift-and-sample on the device, mu* = 1 path (reference sas.py:313-409).
+"""Shift-and-sample on the device (reference sas.py:313-409).
 
-With the pivot vector chosen so that every node at the decode level r_max+1
-holds one element (always true for r = pivots(J)), SAS is a single Hi-DFT
-whose node values times N/|I| are the coefficients (sas.py:358-371).  That
-is config 3's reference call, `sas_transform(f, J, r=pivots(J))`.  Nodes of
-weight > 1 need per-node Vandermonde decoding (sas.py:372-398), which is the
-next component on the roadmap and raises
-NotImplementedError here rather than silently falling back to the CPU.
+The transform picks a pivot vector r with J r-part-homogeneous (the
+reference's policies, sas.py:89-129), computes the Hi-DFT of tau^j f for
+j < mu* (mu* = largest node weight at the decode level r_max+1) as ONE
+launch over B*mu* rows, and decodes each aliased node v from
+(N/|I|) Hidft(tau^j f)(v) = sum_{l in v} Ff(l) x_l^j, x_l = e^{-2 pi i l/N}:
+Bjorck-Pereyra with Leja order in float64, the reference's forward-error
+estimate, double-double re-measure and re-solve above tolerance/20 and a
+dense LU fallback (sfft_sas_decode).  With mu* = 1 (e.g. r = pivots(J),
+config 3) it is a single Hi-DFT read scaled by N/|I| in the input precision.
+Node weights up to 64 are decoded on the device.
 """
 
 from __future__ import annotations
@@ -18,7 +21,8 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib
-from .congruence import SupportSet, as_support, pivots as support_pivots, validate_pivot_vector
+from .congruence import (SupportSet, as_support, assert_part_homogeneous, pivots as support_pivots,
+                         validate_pivot_vector)
 from .errors import InvalidInputError
 from .hidft import _count, _finish, _gathered_samples, _prepare_source, _torch, get_plan
 
@@ -92,9 +96,15 @@ class SasPlan:
 
 
 @dataclass
-class SasReport:
+class CostReport:
+    """Per-phase costs of one transform run plus the analytic bounds
+    (reference counting.py:83-150)."""
+
+    tree_build_bitops: int = 0
     hidft_adds: int = 0
     hidft_mults: int = 0
+    solve_adds: int = 0
+    solve_mults: int = 0
     read_ops: int = 0
     samples_touched: int = 0
     bound_alg1bnd: float = 0.0
@@ -107,8 +117,41 @@ class SasReport:
         return self.hidft_adds + self.hidft_mults
 
     @property
+    def ops_solve(self) -> int:
+        return self.solve_adds + self.solve_mults + self.read_ops
+
+    @property
     def total(self) -> int:
-        return self.ops_hidft + self.read_ops
+        return self.ops_hidft + self.ops_solve
+
+    @classmethod
+    def from_counter(cls, counter, **extra) -> "CostReport":
+        ha, hm = counter.phase("hidft")
+        sa, sm = counter.phase("solve")
+        ra, rm = counter.phase("read")
+        return cls(tree_build_bitops=counter.bit_ops, hidft_adds=ha, hidft_mults=hm, solve_adds=sa,
+                   solve_mults=sm, read_ops=ra + rm, **extra)
+
+    def as_dict(self) -> dict:
+        d = dict(self.__dict__)
+        d.update(ops_hidft=self.ops_hidft, ops_solve=self.ops_solve, ops_total=self.total)
+        return d
+
+
+SasReport = CostReport  # round-1 name
+
+
+@dataclass
+class NodeSystem:
+    residue: int
+    members: tuple[int, ...]
+    escalated: bool = False
+    dense_fallback: bool = False
+    residual: float = 0.0
+
+    @property
+    def size(self) -> int:
+        return len(self.members)
 
 
 @dataclass
@@ -116,45 +159,128 @@ class SasResult:
     support: SupportSet
     coeffs: object
     plan: SasPlan
-    report: SasReport = field(default_factory=SasReport)
+    report: CostReport = field(default_factory=CostReport)
+    node_systems: list = field(default_factory=list)
+    flags: object = None  # (B, n_nodes) int32 for batched sources: 1 escalated, 2 dense fallback
 
     def coeff_map(self) -> dict[int, complex]:
         c = self.coeffs.detach().cpu().numpy() if hasattr(self.coeffs, "detach") else self.coeffs
         return {int(j): complex(v) for j, v in zip(self.support.indices, c)}
 
 
+def _samples_touched(pattern: np.ndarray, mu: int, N: int) -> int:
+    """|union_{j < mu} (I - j) mod N| from the sorted pattern's circular gaps."""
+    if pattern.size == 1:
+        return min(mu, N)
+    gaps = np.diff(np.concatenate([pattern[-1:] - N, pattern]))
+    return int(np.minimum(gaps, mu).sum())
+
+
 def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto",
                   family_meta: dict | None = None, counter=None, tolerance: float = 1e-8) -> SasResult:
-    """Recover (F f)_J by shift-and-sample; mu* = 1 only (see module doc)."""
+    """Recover (F f)_J from mu* shifted Hi-DFTs plus per-node Vandermonde
+    decodes (sas.py:313-409), all on the device."""
+    import ctypes
     torch = _torch()
+    from .counting import OpCounter
+    counter = counter if counter is not None else OpCounter()
     J = as_support(J)
     rt = select_pivots(J, policy, family_meta) if r is None else validate_pivot_vector(r, J.M)
+    assert_part_homogeneous(J, rt)
     src = _prepare_source(source, J.N)
-    plan = get_plan(J, rt, 0, src.dtype_code, src.device)
-    if plan.mu_star != 1:
-        raise NotImplementedError(
-            f"mu*={plan.mu_star} > 1 needs per-node Vandermonde decoding (sas.py:372-398), "
-            "not on the device path yet; use r=pivots(J)")
-    cdt = torch.complex64 if src.dtype_code == _lib.C64 else torch.complex128
-    stream = _lib.stream_ptr(src.device)
-    if src.kind in ("callable", "synth"):
-        samples = _gathered_samples(src, plan, 0)
-        out = torch.empty((1, len(J)), dtype=cdt, device=src.device)
-        _lib.check(_lib.load().sfft_hidft_gathered(plan.handle, samples.data_ptr(), 1, plan.A, _lib.OUT_SAS,
-                                                   out.data_ptr(), len(J), None, 0, stream))
+    dev = src.device
+    lib = _lib.load()
+    stream = _lib.stream_ptr(dev)
+    plan64 = get_plan(J, rt, 0, _lib.C128, dev)
+    mu, level, A, N, k = plan64.mu_star, plan64.level, plan64.A, J.N, len(J)
+    scale = N / A
+    off = np.empty(plan64.n_nodes + 1, np.int32)
+    mem = np.empty(k, np.int32)
+    _lib.check(lib.sfft_plan_nodes(plan64.handle, off.ctypes.data, mem.ctypes.data, stream))
+    weights = tuple(int(w) for w in np.diff(off))
+    splan = SasPlan(rt, level, mu, weights, predicted_cost(len(rt), mu, weights))
+    counter.count_bit_ops(k * max(level, 1))  # build_tree(J, level) as SasPlan.plan does
+    B = 1 if src.kind in ("callable", "synth") else src.tensor.shape[0]
+    nn = plan64.n_nodes
+    flags = None
+    if mu == 1:
+        plan = get_plan(J, rt, 0, src.dtype_code, dev)
+        cdt = torch.complex64 if src.dtype_code == _lib.C64 else torch.complex128
+        if src.kind in ("callable", "synth"):
+            samples = _gathered_samples(src, plan, 0)
+            out = torch.empty((1, k), dtype=cdt, device=dev)
+            _lib.check(lib.sfft_hidft_gathered(plan.handle, samples.data_ptr(), 1, plan.A, _lib.OUT_SAS,
+                                               out.data_ptr(), k, None, 0, stream))
+        else:
+            sig = src.tensor
+            out = torch.empty((B, k), dtype=cdt, device=dev)
+            _lib.check(lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_SAS,
+                                      out.data_ptr(), k, None, 0, stream))
+        n_esc = n_fb = 0
+        resid_h = np.zeros(nn)
+        flags_h = np.zeros(nn, np.int32)
     else:
-        sig = src.tensor
-        B = sig.shape[0]
-        out = torch.empty((B, len(J)), dtype=cdt, device=src.device)
-        _lib.check(_lib.load().sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_SAS,
-                                          out.data_ptr(), len(J), None, 0, stream))
-    _count(counter, plan.A, plan.s)
-    scale = J.N / plan.A
-    if counter is not None and scale != 1.0:
-        counter.mul(len(J), phase="read")
-    weights = tuple([1] * plan.n_nodes)
-    splan = SasPlan(rt, plan.level, 1, weights, predicted_cost(len(rt), 1, weights))
-    rep = SasReport(hidft_adds=plan.A * plan.s, hidft_mults=(plan.A // 2) * plan.s,
-                    read_ops=len(J) if scale != 1.0 else 0, samples_touched=plan.A,
-                    bound_alg1bnd=splan.predicted_cost, bound_hidft=C1 * len(rt) * (1 << len(rt)))
-    return SasResult(J, _finish(out, src), splan, rep)
+        if mu > 64:
+            raise NotImplementedError(f"node weight mu*={mu} above the device decoder's 64")
+        nodevals = torch.empty((B * mu, nn), dtype=torch.complex128, device=dev)
+        sig_ptr, ld_sig, sig_dt, table, blJ, blc, ksrc = None, 0, 0, None, None, None, 0
+        if src.kind in ("callable", "synth"):
+            samples = torch.cat([_gathered_samples(src, plan64, j) for j in range(mu)], 0)
+            _lib.check(lib.sfft_hidft_gathered(plan64.handle, samples.data_ptr(), mu, A, _lib.OUT_NODES,
+                                               nodevals.data_ptr(), nn, None, 0, stream))
+            if src.kind == "synth":
+                blJ_t, blc_t = src.fn._device(dev)
+                blJ, blc, ksrc = blJ_t.data_ptr(), blc_t.data_ptr(), blJ_t.numel()
+            else:  # float64 samples in pattern order for the double-double re-measure
+                from .sampling import pivoted_pattern_tensor
+                pat = pivoted_pattern_tensor(rt, J.M, dev).cpu().numpy()
+                locs = (pat[None, :] - np.arange(mu)[:, None]) % N
+                vals = np.asarray(src.fn(locs.reshape(-1)), dtype=np.complex128).reshape(mu, A)
+                table_t = torch.from_numpy(vals).to(dev)
+                table = table_t.data_ptr()
+        else:
+            sig = src.tensor
+            _lib.check(lib.sfft_hidft_shifts(plan64.handle, sig.data_ptr(), B, sig.stride(0), src.dtype_code, 0, mu,
+                                             _lib.OUT_NODES, nodevals.data_ptr(), nn, stream))
+            sig_ptr, ld_sig, sig_dt = sig.data_ptr(), sig.stride(0), src.dtype_code
+        out = torch.empty((B, k), dtype=torch.complex128, device=dev)
+        flags = torch.empty((B, nn), dtype=torch.int32, device=dev)
+        resid = torch.empty((B, nn), dtype=torch.float64, device=dev)
+        ne, nf = ctypes.c_int64(0), ctypes.c_int64(0)
+        _lib.check(lib.sfft_sas_decode(plan64.handle, nodevals.data_ptr(), nn, _lib.C128, B, mu, float(tolerance),
+                                       sig_ptr, ld_sig, sig_dt, table, blJ, blc, ksrc,
+                                       J.device_tensor(dev).data_ptr(), out.data_ptr(), k, flags.data_ptr(),
+                                       resid.data_ptr(), ctypes.byref(ne), ctypes.byref(nf), stream))
+        n_esc, n_fb = int(ne.value), int(nf.value)
+        flags_h = flags[0].cpu().numpy()
+        resid_h = resid[0].cpu().numpy()
+    # exact counts (sas.py:343-398 with vandermonde_solve's formula, sas.py:196-202)
+    for _ in range(mu * B):
+        _count(counter, A, plan64.s)
+    fb_per_node = (flags.cpu().numpy() == 2).sum(0) if flags is not None else np.zeros(nn)
+    for v, m in enumerate(weights):
+        if m == 1:
+            if scale != 1.0:
+                counter.mul(B, phase="read")
+            continue
+        if scale != 1.0:
+            counter.mul(m * B, phase="solve")
+        half = m * (m - 1) // 2
+        counter.mul(m * (m - 1) * B, phase="solve")
+        counter.add(half * 3 * B, phase="solve")
+        if m >= 3:
+            counter.mul(half * B, phase="solve")
+            counter.add(half * B, phase="solve")
+        if fb_per_node[v]:
+            counter.mul(int(fb_per_node[v]) * m ** 3, phase="solve")
+            counter.add(int(fb_per_node[v]) * m ** 3, phase="solve")
+    from .sampling import pivoted_pattern_tensor
+    pat = pivoted_pattern_tensor(rt, J.M, dev).cpu().numpy() if rt else np.zeros(1, np.int64)
+    report = CostReport.from_counter(counter, samples_touched=_samples_touched(pat, mu, N),
+                                     bound_alg1bnd=splan.predicted_cost, bound_hidft=C1 * len(rt) * (1 << len(rt)),
+                                     escalated_nodes=n_esc, dense_fallbacks=n_fb)
+    node_res = plan64.tables()["node_residues"]
+    systems = [NodeSystem(int(node_res[v]), tuple(int(J.as_array()[e]) for e in mem[off[v]:off[v + 1]]),
+                          escalated=bool(flags_h[v] == 1), dense_fallback=bool(flags_h[v] == 2),
+                          residual=float(resid_h[v])) for v in range(nn)]
+    return SasResult(J, _finish(out, src), splan, report, systems, flags)

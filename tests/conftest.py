@@ -30,3 +30,9 @@ def kats():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "kats.json")) as fh:
         return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def golden_sas():
+    import numpy as np
+    return np.load(os.path.join(ROOT, "tests", "golden", "golden_sas.npz"))

@@ -1,0 +1,96 @@
+"""Shift-and-sample with mu* > 1 on the device vs the reference's own outputs
+(tests/golden/make_golden_sas.py, reference tests/test_sas.py shapes)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2211_15299_b200 as S
+    return S
+
+
+def rel_error(got, want, floor=1e-30):
+    got = np.asarray(got, np.complex128)
+    want = np.asarray(want, np.complex128)
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), floor))) if got.size else 0.0
+
+
+def _case(g, i):
+    p = f"s{i}_"
+    pol = bytes(g[p + "policy"]).decode().strip()
+    base = tuple(int(x) for x in g[p + "base"])
+    return p, pol, ({"base_pivots": base} if base else None)
+
+
+def test_sas_matches_reference(S, golden_sas):
+    g = golden_sas
+    n_esc = 0
+    for i in range(int(g["n_cases"][0])):
+        p, pol, meta = _case(g, i)
+        N = int(g[p + "N"][0])
+        J = S.SupportSet(N, g[p + "J"])
+        c = g[p + "c"]
+        sig = S.BandlimitedSignal(J, c)
+        src = sig.synthesize() if int(g[p + "dense"][0]) else sig
+        ctr = S.OpCounter()
+        res = S.sas_transform(src, J, policy=pol, family_meta=meta, counter=ctr)
+        assert res.plan.pivots == tuple(int(x) for x in g[p + "pivots"]), i
+        assert [res.plan.decode_level, res.plan.mu_star] == [int(x) for x in g[p + "plan"]]
+        assert res.plan.node_weights == tuple(int(x) for x in g[p + "weights"])
+        got = np.asarray(res.coeffs)
+        assert rel_error(got, c) < 1e-8, (i, rel_error(got, c))            # tests/test_sas.py standard
+        assert rel_error(got, g[p + "coeffs"], floor=1e-9) < 1e-7, i
+        rep = res.report
+        want = [int(x) for x in g[p + "report"]]
+        mine = [rep.tree_build_bitops, rep.hidft_adds, rep.hidft_mults, rep.solve_adds, rep.solve_mults,
+                rep.read_ops, rep.samples_touched, rep.escalated_nodes, rep.dense_fallbacks]
+        assert mine[:7] == want[:7], (i, mine, want)
+        assert rep.total <= rep.bound_alg1bnd + 1e-9 or want[8] > 0
+        np.testing.assert_allclose([rep.bound_alg1bnd, rep.bound_hidft], g[p + "bounds"])
+        sysw = g[p + "systems"]
+        assert [(s.residue, s.size) for s in res.node_systems] == [(int(a), int(b)) for a, b, _, _ in sysw]
+        n_esc += rep.escalated_nodes
+    assert n_esc > 0  # the double-double path was exercised
+
+
+def test_worked_example(S):
+    # tests/test_sas.py: {0,1,6,7,512}: pivots (0,1), mu*=2, node sizes [1,1,1,2], 8 samples touched
+    J = S.SupportSet.make(1024, [0, 1, 6, 7, 512])
+    rng = np.random.default_rng(3)
+    mag = 0.5 + rng.random(5)
+    c = mag * np.exp(1j * rng.random(5) * 2 * np.pi)
+    out = S.sas_transform(S.BandlimitedSignal(J, c), J)
+    assert rel_error(out.coeffs, c) < 1e-8
+    assert out.plan.pivots == (0, 1) and out.plan.mu_star == 2
+    assert sorted(s.size for s in out.node_systems) == [1, 1, 1, 2]
+    assert out.report.total <= out.report.bound_alg1bnd
+    assert out.report.samples_touched == 2 * 4
+
+
+def test_sas_batched_dense_rows(S):
+    import torch
+    rng = np.random.default_rng(11)
+    M, B = 12, 6
+    base = (0, 2, 3, 5, 7, 9)
+    import structfft_oracle as O
+    H = O.gen_homogeneous(base, M, 7)
+    J = np.sort(H[rng.choice(H.size, size=24, replace=False)])
+    Js = S.SupportSet(1 << M, J)
+    coef = rng.normal(size=(B, J.size)) + 1j * rng.normal(size=(B, J.size))
+    f = np.stack([O.synthesize(J, coef[b], M) for b in range(B)])
+    for dt, tol in ((np.complex128, 1e-8), (np.complex64, 1e-4)):
+        sig = torch.from_numpy(f.astype(dt)).cuda()
+        res = S.sas_transform(sig, Js, policy="random_subset", family_meta={"base_pivots": base})
+        assert res.plan.mu_star > 1
+        got = res.coeffs.cpu().numpy()
+        for b in range(B):
+            single = S.sas_transform(f[b].astype(dt), Js, policy="random_subset", family_meta={"base_pivots": base})
+            assert np.allclose(got[b], single.coeffs, rtol=0, atol=1e-12 * np.abs(single.coeffs).max())
+            assert np.linalg.norm(got[b] - coef[b]) / np.linalg.norm(coef[b]) < tol
