@@ -80,6 +80,25 @@ def main() -> None:
         out[p + "systems"] = np.asarray([[s.residue, s.size, int(s.escalated), int(s.dense_fallback)]
                                          for s in res.node_systems], np.int64)
     out["n_cases"] = np.asarray([kept])
+    # config 3: the reference's "auto" and "random_subset" policies on
+    # signal 0 (dense complex64, as the bench feeds it)
+    from structfft.families import rng_from_seed
+    piv = tuple(sorted(int(x) for x in rng_from_seed(3, 7).choice(22, size=14, replace=False)))
+    H = R.gen_homogeneous(piv, 22, 3)
+    pick = np.sort(rng_from_seed(3, 8).choice(1 << 14, size=1 << 12, replace=False))
+    J3 = R.SupportSet.make(1 << 22, H.as_array()[pick].tolist())
+    g = rng_from_seed(3, 200, 0)
+    c3 = g.normal(size=len(J3)) + 1j * g.normal(size=len(J3))
+    spec = np.zeros(1 << 22, np.complex128)
+    spec[J3.as_array()] = c3
+    f3 = np.fft.ifft(spec).astype(np.complex64)
+    for pol in ("auto", "random_subset"):
+        res = R.sas_transform(f3, J3, policy=pol, family_meta={"base_pivots": piv})
+        rep = res.report
+        out[f"cfg3_{pol}_coeffs"] = res.coeffs
+        out[f"cfg3_{pol}_plan"] = np.asarray([len(res.plan.pivots), res.plan.mu_star, rep.escalated_nodes,
+                                              rep.dense_fallbacks, rep.samples_touched], np.int64)
+    out["cfg3_base_pivots"] = np.asarray(piv, np.int64)
     np.savez_compressed(os.path.join(HERE, "golden_sas.npz"), **out)
     print("sas cases", kept, "escalations", sum(int(out[f"s{i}_report"][7]) for i in range(kept)))
 

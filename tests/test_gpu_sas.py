@@ -94,3 +94,24 @@ def test_sas_batched_dense_rows(S):
             single = S.sas_transform(f[b].astype(dt), Js, policy="random_subset", family_meta={"base_pivots": base})
             assert np.allclose(got[b], single.coeffs, rtol=0, atol=1e-12 * np.abs(single.coeffs).max())
             assert np.linalg.norm(got[b] - coef[b]) / np.linalg.norm(coef[b]) < tol
+
+
+@pytest.mark.parametrize("pol", ["auto", "random_subset"])
+def test_config3_reference_policies(S, golden_sas, pol):
+    """Config 3 under the reference's own SAS policies (mu* = 10 / 28, the
+    latter with ~90 double-double escalations), identical dense c64 input."""
+    import torch
+    import structfft_oracle as O
+    g = golden_sas
+    J, M = O.config_support(3)
+    coef = O.config_coefficients(3, 0, J.size)
+    f = O.synthesize(J, coef, M).astype(np.complex64)
+    Js = S.SupportSet(1 << M, J)
+    base = tuple(int(x) for x in g["cfg3_base_pivots"])
+    res = S.sas_transform(torch.from_numpy(f).cuda(), Js, policy=pol, family_meta={"base_pivots": base})
+    s, mu, esc, fb, touched = (int(x) for x in g[f"cfg3_{pol}_plan"])
+    assert (len(res.plan.pivots), res.plan.mu_star, res.report.samples_touched) == (s, mu, touched)
+    assert abs(res.report.escalated_nodes - esc) <= max(2, esc // 20), (res.report.escalated_nodes, esc)
+    got = res.coeffs.cpu().numpy().reshape(-1)
+    want = g[f"cfg3_{pol}_coeffs"]
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-8
