@@ -141,10 +141,14 @@ def run_b200(args) -> None:
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # host-side collectives only (CPU tests of the multi-rank path)
+            dist.init_process_group("gloo")
 
     cfg = args.config
     spec = W.CONFIGS[cfg]
@@ -240,7 +244,8 @@ def run_b200(args) -> None:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     clocks = sampler.stop()
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
@@ -280,7 +285,7 @@ def run_b200(args) -> None:
     if not args.no_e2e:
         e2e = run_e2e(args, S, torch, sets[0], J, wl, esz, dev)
         if world > 1:
-            t = torch.tensor([e2e["seconds_per_step"]], dtype=torch.float64, device=dev)
+            t = torch.tensor([e2e["seconds_per_step"]], dtype=torch.float64, device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e["value"] = coeffs_per_step / float(t.item())
         del e2e["seconds_per_step"]
@@ -490,6 +495,8 @@ def main() -> None:
     ap.add_argument("--ref-seconds", type=float, default=150.0, help="whole --impl reference run budget")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-side collectives (multi-rank path test on fewer GPUs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
