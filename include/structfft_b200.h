@@ -142,6 +142,12 @@ SFFT_API int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const void
 SFFT_API int sfft_synthesize(const int64_t* J, const void* coeffs, int64_t k, int M,
                              const int64_t* locations, int64_t n, void* out, sfft_stream_t stream);
 
+/* select_pivots("auto") profile (sas.py:80-113): for each prefix t = 0..s of the
+ * pivot list piv (ascending pivots of J), the largest node weight mu[t] and the
+ * sum of squared node weights sumsq[t] at level piv[t-1]+1 (host outputs, s+1 each). */
+SFFT_API int sfft_prefix_weights(const int64_t* J, int64_t k, int M, const int32_t* piv, int s,
+                                 uint64_t* mu, uint64_t* sumsq, sfft_stream_t stream);
+
 /* Node membership of a plan's decode level (congruence tree, congruence.py:134-214):
  * offsets[n_nodes+1] and member element indices (ascending J within each node),
  * host or device buffers, either may be NULL (builds and caches the table). */

@@ -665,3 +665,72 @@ extern "C" int sfft_plan_tables(const sfft_plan* p, int64_t* element_slots, int6
   SFFT_CUDA(cudaStreamSynchronize(st));
   return SFFT_OK;
 }
+
+// ------------------------------------------------ SAS prefix weight profile ---
+// For the prefixes p[:t] (t = 0..s) of the pivot list of J, the congruence-tree
+// nodes at level p[t-1]+1 are the classes of the first t pattern bits (J has
+// no other pivot below p[t-1]), so one pass over J fills all prefix
+// histograms; mu*(t) = max weight, sum w^2 (sas.py:80-86, 105-113).
+__global__ void k_prefix_hist(const int64_t* __restrict__ J, int64_t k, const int32_t* __restrict__ piv, int s,
+                              uint32_t* __restrict__ hist) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = (uint64_t)J[e];
+    uint32_t pat = 0;
+    atomicAdd(&hist[0], 1u);  // t = 0: the root
+    for (int t = 1; t <= s; ++t) {
+      pat |= (uint32_t)((j >> piv[t - 1]) & 1u) << (t - 1);
+      atomicAdd(&hist[((1u << t) - 1) + pat], 1u);
+    }
+  }
+}
+
+__global__ void k_prefix_reduce(const uint32_t* __restrict__ hist, int s, unsigned long long* __restrict__ out) {
+  // out[2t] = max weight, out[2t+1] = sum of squared weights, for t = 0..s
+  for (int t = blockIdx.x; t <= s; t += gridDim.x) {
+    const uint32_t* h = hist + ((1u << t) - 1);
+    unsigned long long mx = 0, sq = 0;
+    for (int64_t i = threadIdx.x; i < (1ll << t); i += blockDim.x) {
+      const unsigned long long w = h[i];
+      mx = mx > w ? mx : w;
+      sq += w * w;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, d);
+      mx = mx > o ? mx : o;
+      sq += __shfl_xor_sync(0xffffffffu, sq, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(&out[2 * t], mx);
+      atomicAdd(&out[2 * t + 1], sq);
+    }
+  }
+}
+
+extern "C" int sfft_prefix_weights(const int64_t* J, int64_t k, int M, const int32_t* piv, int s,
+                                   uint64_t* mu_out, uint64_t* sumsq_out, sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
+  if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
+  if (s < 0 || s > 26) return fail(SFFT_ERR_UNSUPPORTED, "prefix profile limited to 26 pivots");
+  int rc;
+  DevBuf tmpJ, dpiv, hist, out;
+  const int64_t* dJ = nullptr;
+  if ((rc = to_device_J(J, k, st, tmpJ, &dJ))) return rc;
+  if ((rc = alloc(dpiv, 4 * std::max(s, 1), st))) return rc;
+  if ((rc = alloc(hist, 4 * ((2ll << s) - 1), st))) return rc;
+  if ((rc = alloc(out, 16 * (s + 1), st))) return rc;
+  if (s) SFFT_CUDA(cudaMemcpyAsync(dpiv.p, piv, 4 * s, cudaMemcpyHostToDevice, st));
+  SFFT_CUDA(cudaMemsetAsync(hist.p, 0, 4 * ((2ll << s) - 1), st));
+  SFFT_CUDA(cudaMemsetAsync(out.p, 0, 16 * (s + 1), st));
+  k_prefix_hist<<<grid_1d(k), 256, 0, st>>>(dJ, k, (const int32_t*)dpiv.p, s, (uint32_t*)hist.p);
+  k_prefix_reduce<<<s + 1, 256, 0, st>>>((const uint32_t*)hist.p, s, (unsigned long long*)out.p);
+  SFFT_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> h(2 * (s + 1));
+  SFFT_CUDA(cudaMemcpyAsync(h.data(), out.p, 16 * (s + 1), cudaMemcpyDeviceToHost, st));
+  SFFT_CUDA(cudaStreamSynchronize(st));
+  for (int t = 0; t <= s; ++t) {
+    mu_out[t] = h[2 * t];
+    sumsq_out[t] = h[2 * t + 1];
+  }
+  return SFFT_OK;
+}

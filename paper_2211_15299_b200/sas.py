@@ -36,10 +36,16 @@ def predicted_cost(size_r: int, mu_star: int, node_weights: Sequence[int]) -> fl
     return C1 * size_r * (1 << size_r) * mu_star + C2 * sum(int(w) * int(w) for w in node_weights)
 
 
-def _weights_at(J: SupportSet, level: int) -> np.ndarray:
-    """Node weights of the congruence tree at `level` (counts per residue)."""
-    _, counts = np.unique(J.as_array() & ((1 << level) - 1), return_counts=True)
-    return counts
+def _prefix_profile(J: SupportSet, piv: tuple[int, ...]) -> tuple[np.ndarray, np.ndarray]:
+    """(mu*, sum w^2) at the decode level of every prefix of piv (sfft_prefix_weights)."""
+    dev = _lib.require_device()
+    s = len(piv)
+    mu = np.zeros(s + 1, np.uint64)
+    sq = np.zeros(s + 1, np.uint64)
+    pv = np.asarray(piv if piv else [0], np.int32)
+    _lib.check(_lib.load().sfft_prefix_weights(J.device_tensor(dev).data_ptr(), len(J), J.M, pv.ctypes.data, s,
+                                               mu.ctypes.data, sq.ctypes.data, _lib.stream_ptr(dev)))
+    return mu.astype(np.int64), sq.astype(np.int64)
 
 
 def _stock_pivot_count(k: int) -> int:
@@ -56,12 +62,12 @@ def select_pivots(J, policy: str = "auto", family_meta: dict | None = None) -> t
         raise InvalidInputError(f"unknown policy {policy!r}; expected one of {POLICIES}")
     meta = family_meta or {}
     if policy == "auto":
+        # node-weight profile of every prefix of pivots(J), one device pass
         p = support_pivots(J)
+        mu, sq = _prefix_profile(J, p)
         best, best_cost = (), math.inf
         for t in range(len(p) + 1):
-            level = p[t - 1] + 1 if t else 0
-            w = _weights_at(J, level)
-            cost = predicted_cost(t, int(w.max()), w)
+            cost = C1 * t * (1 << t) * mu[t] + C2 * sq[t]
             if cost < best_cost:  # ties keep the shorter prefix
                 best, best_cost = p[:t], cost
         r = best

@@ -115,3 +115,26 @@ def test_config3_reference_policies(S, golden_sas, pol):
     got = res.coeffs.cpu().numpy().reshape(-1)
     want = g[f"cfg3_{pol}_coeffs"]
     assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-8
+
+
+def test_select_pivots_policies(S):
+    # reference tests/test_sas.py TestSelectPivots
+    import math
+    import structfft_oracle as O
+    J = S.SupportSet(32, O.gen_homogeneous((1, 3), 5, 3))
+    assert S.select_pivots(J, "auto") == S.pivots(J)
+    assert S.select_pivots(S.SupportSet.make(1024, [0, 1, 6, 7, 512]), "auto") == (0, 1)
+    jstar = S.SupportSet.make(1 << 10, [1 << i for i in range(10)])
+    r = S.select_pivots(jstar, "auto")
+    assert r == tuple(range(len(r)))
+    with pytest.raises(S.InvalidInputError):
+        S.select_pivots(jstar, "uoh")
+    with pytest.raises(S.InvalidInputError):
+        S.select_pivots(jstar, "balanced")
+    with pytest.raises(S.InvalidInputError):
+        S.select_pivots(jstar, "nope")
+    base = (0, 2, 5, 7, 9)
+    K = O.gen_homogeneous(base, 12, 1)
+    sub = S.SupportSet(1 << 12, K[:9])
+    t = int(math.floor(math.log2(9) - math.log2(math.log2(9))))
+    assert S.select_pivots(sub, "random_subset", {"base_pivots": base}) == base[:t]
