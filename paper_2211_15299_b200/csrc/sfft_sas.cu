@@ -16,6 +16,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "sfft_common.cuh"
@@ -352,9 +354,17 @@ __device__ __forceinline__ cdd dd_sample(const SasDDArgs& a, int64_t b, int64_t 
   return {{v.x, 0.0}, {v.y, 0.0}};
 }
 
-// one thread per escalated node: re-measure (sas.py:290-310) and solve in dd
+__device__ __forceinline__ dd shfl_dd(dd v, int d) {
+  return {__shfl_xor_sync(0xffffffffu, v.hi, d), __shfl_xor_sync(0xffffffffu, v.lo, d)};
+}
+
+// one WARP per escalated node: re-measure (sas.py:290-310) with the A-term dd
+// dot products split across the lanes (butterfly-reduced in dd), then lane 0
+// solves in dd (_ddc.py:235-254)
 __global__ void k_sas_decode_dd(const SasDDArgs a) {
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < a.n_work; w += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < a.n_work; w += warps) {
     const int64_t id = a.work[w];
     const SasDecodeArgs& s = a.base;
     const int64_t b = id / s.n_nodes, v = id % s.n_nodes;
@@ -363,13 +373,18 @@ __global__ void k_sas_decode_dd(const SasDDArgs a) {
     cdd y[kMaxMu];
     for (int j = 0; j < m; ++j) {
       cdd acc = {{0.0, 0.0}, {0.0, 0.0}};
-      for (int64_t i = 0; i < a.A; ++i) {
+      for (int64_t i = lane; i < a.A; i += 32) {
         const cdd kern = a.tab.get((uint64_t)(-(int64_t)(resid * (uint64_t)a.pattern[i])));
         acc = cdd_add(acc, cdd_mul(dd_sample(a, b, j, i), kern));
       }
+      for (int d = 16; d > 0; d >>= 1) {
+        const cdd o = {shfl_dd(acc.re, d), shfl_dd(acc.im, d)};
+        acc = cdd_add(acc, o);
+      }
       y[j] = cdd_mul_complex(acc, s.scale, 0.0);
     }
-    // solve_vandermonde_dd (_ddc.py:235-254): x_m = root((-l) mod N), BP, no Leja
+    if (lane != 0) continue;
+    // solve_vandermonde_dd: x_m = root((-l) mod N), BP, no Leja
     cdd x[kMaxMu];
     for (int i = 0; i < m; ++i) x[i] = a.tab.get((uint64_t)(-(int64_t)s.J[s.node_mem[off + i]]));
     for (int k = 0; k < m - 1; ++k)
@@ -515,6 +530,33 @@ __global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
+static int grid_for(int64_t n, int threads);
+
+// double-double root tables per (device, M), built once (the reference caches
+// its RootTable per modulus too, _ddc.py:208-209)
+static std::mutex g_root_mu;
+static std::map<std::pair<int, int>, std::pair<cdd*, cdd*>> g_roots;
+
+static int root_tables(int M, cdd** fine, cdd** coarse, cudaStream_t st) {
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_root_mu);
+  auto it = g_roots.find({dev, M});
+  if (it == g_roots.end()) {
+    const int h = M / 2;
+    cdd *f = nullptr, *c = nullptr;
+    SFFT_CUDA(cudaMalloc(&f, sizeof(cdd) * (1ll << h)));
+    SFFT_CUDA(cudaMalloc(&c, sizeof(cdd) * (1ll << (M - h))));
+    k_root_tables<<<grid_for((1ll << h) + (1ll << (M - h)), 128), 128, 0, st>>>(f, c, M);
+    SFFT_CUDA(cudaGetLastError());
+    SFFT_CUDA(cudaStreamSynchronize(st));  // usable from any stream afterwards
+    it = g_roots.emplace(std::make_pair(dev, M), std::make_pair(f, c)).first;
+  }
+  *fine = it->second.first;
+  *coarse = it->second.second;
+  return SFFT_OK;
+}
+
 static int grid_for(int64_t n, int threads = 128) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)num_sms() * 32));
 }
@@ -524,9 +566,12 @@ static int grid_for(int64_t n, int threads = 128) {
 using namespace sfft;
 
 // node CSR (offsets n_nodes+1, members k) for a plan; cached on the plan
+static std::mutex g_nodes_mu;
+
 extern "C" int sfft_plan_nodes(sfft_plan* p, int32_t* off_out, int32_t* mem_out, sfft_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!p) return fail(SFFT_ERR_INVALID, "null plan");
+  std::lock_guard<std::mutex> lk(g_nodes_mu);  // the table is built once, lazily
   if (!p->d_node_off) {
     int32_t *cnt = nullptr, *cand = nullptr;
     uint8_t* taken = nullptr;
@@ -626,14 +671,12 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
   if (!esc.empty()) {
     const int M = p->M, h = M / 2;
     cdd *fine = nullptr, *coarse = nullptr, *samples = nullptr;
+    if ((rc = root_tables(M, &fine, &coarse, st))) return rc;
     int64_t* pattern = nullptr;
     int32_t *work = nullptr, *sigs = nullptr;
-    SFFT_CUDA(cudaMallocAsync(&fine, sizeof(cdd) * (1ll << h), st));
-    SFFT_CUDA(cudaMallocAsync(&coarse, sizeof(cdd) * (1ll << (M - h)), st));
     SFFT_CUDA(cudaMallocAsync(&pattern, 8 * p->A, st));
     SFFT_CUDA(cudaMallocAsync(&work, 4 * esc.size(), st));
     SFFT_CUDA(cudaMemcpyAsync(work, esc.data(), 4 * esc.size(), cudaMemcpyHostToDevice, st));
-    k_root_tables<<<grid_for((1ll << h) + (1ll << (M - h))), 128, 0, st>>>(fine, coarse, M);
     rc = sfft_pivoted_pattern(p->used, p->s, M, pattern, stream);
     if (rc) return rc;
     SasDDArgs d{};
@@ -659,10 +702,8 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
           d.tab, pattern, p->A, mu, bl_J, (const double2*)bl_c, k_src, M, sigs, (int64_t)s2.size(), samples);
       d.samples_dd = samples;
     }
-    k_sas_decode_dd<<<grid_for(d.n_work, 32), 32, 0, st>>>(d);
+    k_sas_decode_dd<<<grid_for(d.n_work * 32, 128), 128, 0, st>>>(d);
     SFFT_CUDA(cudaGetLastError());
-    cudaFreeAsync(fine, st);
-    cudaFreeAsync(coarse, st);
     cudaFreeAsync(pattern, st);
     cudaFreeAsync(work, st);
     if (sigs) cudaFreeAsync(sigs, st);

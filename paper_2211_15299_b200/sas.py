@@ -37,7 +37,11 @@ def predicted_cost(size_r: int, mu_star: int, node_weights: Sequence[int]) -> fl
 
 
 def _prefix_profile(J: SupportSet, piv: tuple[int, ...]) -> tuple[np.ndarray, np.ndarray]:
-    """(mu*, sum w^2) at the decode level of every prefix of piv (sfft_prefix_weights)."""
+    """(mu*, sum w^2) at the decode level of every prefix of piv (sfft_prefix_weights),
+    cached on the immutable support."""
+    key = ("prefix_profile", tuple(piv))
+    if key in J._plans:
+        return J._plans[key]
     dev = _lib.require_device()
     s = len(piv)
     mu = np.zeros(s + 1, np.uint64)
@@ -45,7 +49,8 @@ def _prefix_profile(J: SupportSet, piv: tuple[int, ...]) -> tuple[np.ndarray, np
     pv = np.asarray(piv if piv else [0], np.int32)
     _lib.check(_lib.load().sfft_prefix_weights(J.device_tensor(dev).data_ptr(), len(J), J.M, pv.ctypes.data, s,
                                                mu.ctypes.data, sq.ctypes.data, _lib.stream_ptr(dev)))
-    return mu.astype(np.int64), sq.astype(np.int64)
+    J._plans[key] = (mu.astype(np.int64), sq.astype(np.int64))
+    return J._plans[key]
 
 
 def _stock_pivot_count(k: int) -> int:
@@ -160,14 +165,25 @@ class NodeSystem:
         return len(self.members)
 
 
-@dataclass
 class SasResult:
-    support: SupportSet
-    coeffs: object
-    plan: SasPlan
-    report: CostReport = field(default_factory=CostReport)
-    node_systems: list = field(default_factory=list)
-    flags: object = None  # (B, n_nodes) int32 for batched sources: 1 escalated, 2 dense fallback
+    """coeffs, plan, report as the reference (sas.py:251-260); node_systems is
+    built on first access (per-node records of the first signal); flags holds
+    all signals' (B, n_nodes) escalation / fallback markers (1 / 2)."""
+
+    def __init__(self, support, coeffs, plan, report, systems_fn=None, flags=None):
+        self.support = support
+        self.coeffs = coeffs
+        self.plan = plan
+        self.report = report
+        self._systems_fn = systems_fn
+        self._systems = None
+        self.flags = flags
+
+    @property
+    def node_systems(self) -> list:
+        if self._systems is None:
+            self._systems = self._systems_fn() if self._systems_fn else []
+        return self._systems
 
     def coeff_map(self) -> dict[int, complex]:
         c = self.coeffs.detach().cpu().numpy() if hasattr(self.coeffs, "detach") else self.coeffs
@@ -200,9 +216,12 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
     plan64 = get_plan(J, rt, 0, _lib.C128, dev)
     mu, level, A, N, k = plan64.mu_star, plan64.level, plan64.A, J.N, len(J)
     scale = N / A
-    off = np.empty(plan64.n_nodes + 1, np.int32)
-    mem = np.empty(k, np.int32)
-    _lib.check(lib.sfft_plan_nodes(plan64.handle, off.ctypes.data, mem.ctypes.data, stream))
+    if getattr(plan64, "_nodes", None) is None:
+        off = np.empty(plan64.n_nodes + 1, np.int32)
+        mem = np.empty(k, np.int32)
+        _lib.check(lib.sfft_plan_nodes(plan64.handle, off.ctypes.data, mem.ctypes.data, stream))
+        plan64._nodes = (off, mem)
+    off, mem = plan64._nodes
     weights = tuple(int(w) for w in np.diff(off))
     splan = SasPlan(rt, level, mu, weights, predicted_cost(len(rt), mu, weights))
     counter.count_bit_ops(k * max(level, 1))  # build_tree(J, level) as SasPlan.plan does
@@ -261,32 +280,31 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
         flags_h = flags[0].cpu().numpy()
         resid_h = resid[0].cpu().numpy()
     # exact counts (sas.py:343-398 with vandermonde_solve's formula, sas.py:196-202)
-    for _ in range(mu * B):
-        _count(counter, A, plan64.s)
-    fb_per_node = (flags.cpu().numpy() == 2).sum(0) if flags is not None else np.zeros(nn)
-    for v, m in enumerate(weights):
-        if m == 1:
-            if scale != 1.0:
-                counter.mul(B, phase="read")
-            continue
-        if scale != 1.0:
-            counter.mul(m * B, phase="solve")
-        half = m * (m - 1) // 2
-        counter.mul(m * (m - 1) * B, phase="solve")
-        counter.add(half * 3 * B, phase="solve")
-        if m >= 3:
-            counter.mul(half * B, phase="solve")
-            counter.add(half * B, phase="solve")
-        if fb_per_node[v]:
-            counter.mul(int(fb_per_node[v]) * m ** 3, phase="solve")
-            counter.add(int(fb_per_node[v]) * m ** 3, phase="solve")
+    if plan64.s:  # mu* shifted Hi-DFTs per signal: A/2 mults + A adds per stage (hidft.py:165-167)
+        counter.mul((A // 2) * plan64.s * mu * B, phase="hidft")
+        counter.add(A * plan64.s * mu * B, phase="hidft")
+    fb_per_node = (flags.cpu().numpy() == 2).sum(0) if flags is not None else np.zeros(nn, np.int64)
+    w = np.asarray(weights, np.int64)
+    single, multi = w == 1, w >= 2
+    half = w * (w - 1) // 2
+    if scale != 1.0:
+        counter.mul(int(single.sum()) * B, phase="read")
+        counter.mul(int(w[multi].sum()) * B, phase="solve")
+    counter.mul(int((w * (w - 1))[multi].sum() + half[w >= 3].sum()) * B, phase="solve")
+    counter.add(int((3 * half)[multi].sum() + half[w >= 3].sum()) * B, phase="solve")
+    nfb = int((fb_per_node * w ** 3).sum())
+    if nfb:
+        counter.mul(nfb, phase="solve")
+        counter.add(nfb, phase="solve")
     from .sampling import pivoted_pattern_tensor
     pat = pivoted_pattern_tensor(rt, J.M, dev).cpu().numpy() if rt else np.zeros(1, np.int64)
     report = CostReport.from_counter(counter, samples_touched=_samples_touched(pat, mu, N),
                                      bound_alg1bnd=splan.predicted_cost, bound_hidft=C1 * len(rt) * (1 << len(rt)),
                                      escalated_nodes=n_esc, dense_fallbacks=n_fb)
-    node_res = plan64.tables()["node_residues"]
-    systems = [NodeSystem(int(node_res[v]), tuple(int(J.as_array()[e]) for e in mem[off[v]:off[v + 1]]),
-                          escalated=bool(flags_h[v] == 1), dense_fallback=bool(flags_h[v] == 2),
-                          residual=float(resid_h[v])) for v in range(nn)]
+    def systems():
+        node_res = plan64.tables()["node_residues"].tolist()
+        members = np.split(J._arr[mem], off[1:-1])
+        return [NodeSystem(node_res[v], tuple(members[v].tolist()), escalated=bool(flags_h[v] == 1),
+                           dense_fallback=bool(flags_h[v] == 2), residual=float(resid_h[v])) for v in range(nn)]
+
     return SasResult(J, _finish(out, src), splan, report, systems, flags)
