@@ -290,16 +290,32 @@ __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
     double dmax = 0.0;
     for (int i = 0; i < m; ++i) dmax = fmax(dmax, cabs2(d[i]));
     double est = dmax / denom;
-    // ||inv(V)||_inf from the columns inv(V) e_j (V[j][m] = x_m^j)
-    double rows[kMaxMu];
-    for (int i = 0; i < m; ++i) rows[i] = 0.0;
-    for (int j = 0; j < m; ++j) {
-      for (int i = 0; i < m; ++i) r[i] = {i == j ? 1.0 : 0.0, 0.0};
-      vandermonde_solve(x, r, m, perm, d);
-      for (int i = 0; i < m; ++i) rows[i] += cabs2(d[i]);
-    }
+    // ||inv(V)||_inf in O(m^2): row q of inv(V) (V[j][m] = x_m^j) holds the
+    // coefficients of the Lagrange basis L_q(z) = P(z) / ((z - x_q) P'(x_q)),
+    // P(z) = prod_i (z - x_i); synthetic division per node (the reference
+    // inverts V densely, sas.py:229-233; this is the same norm)
     double amp = 0.0;
-    for (int i = 0; i < m; ++i) amp = fmax(amp, rows[i]);
+    {
+      C64x P[kMaxMu + 1];
+      P[0] = {1.0, 0.0};
+      for (int i = 1; i <= m; ++i) P[i] = {0.0, 0.0};
+      for (int i = 0; i < m; ++i)  // multiply by (z - x_i)
+        for (int e = i + 1; e >= 0; --e) P[e] = cs(e ? P[e - 1] : C64x{0.0, 0.0}, cm(x[i], P[e]));
+      for (int q = 0; q < m; ++q) {
+        C64x qc = P[m];  // Q(z) = P(z) / (z - x_q): leading coefficient
+        C64x den = {1.0, 0.0};
+        for (int i = 0; i < m; ++i)
+          if (i != q) den = cm(den, cs(x[q], x[i]));
+        const double dabs = cabs2(den);
+        double row = cabs2(qc);
+        for (int e = m - 1; e >= 1; --e) {
+          const C64x t = cm(x[q], qc);
+          qc = {P[e].x + t.x, P[e].y + t.y};
+          row += cabs2(qc);
+        }
+        amp = fmax(amp, row / fmax(dabs, 1e-300));
+      }
+    }
     est = fmax(est, amp * noise_eps * ymax / denom);
     int flag = 0;
     double res = 0.0;
