@@ -1,0 +1,24 @@
+"""The plain-C consumer of the C-ABI runs on the GPU (examples/capi_demo.c)."""
+
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_capi_demo_runs(tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = tmp_path / "capi_demo"
+    lib = os.path.join(ROOT, "paper_2211_15299_b200")
+    cmd = ["gcc", "-O2", os.path.join(ROOT, "examples", "capi_demo.c"), "-I", os.path.join(ROOT, "include"),
+           "-I/usr/local/cuda/include", "-L", lib, "-lsfft_b200", "-L/usr/local/cuda/lib64", "-lcudart", "-lm",
+           f"-Wl,-rpath,{lib}", "-o", str(exe)]
+    assert subprocess.run(cmd, capture_output=True).returncode == 0
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "status 3" in out.stdout

@@ -388,3 +388,24 @@ def test_config5_full_batch(S, torch, golden_configs, cfg):
     assert rel_l2(got[0][: head.size], head) < max(tol, 1e-6)
     del sig
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_plan_tables_at_config_size(S, cfg):
+    """Index tables of the device plan bit-exact with the oracle's _build_plan
+    restatement at the BASELINE configs' sizes (s up to 16)."""
+    J, M = O.config_support(cfg)
+    r = O.pivots(J, M)
+    Js = S.SupportSet(1 << M, J)
+    assert S.pivots(Js) == r
+    assert S.classify(Js).is_homogeneous == O.is_homogeneous(J, M)
+    plan = S.get_plan(Js, r, 0, 1, S._lib.require_device())
+    t = plan.tables()
+    o = O.build_plan(J, M, r)
+    assert plan.level == o.level and plan.mu_star == int(o.slot_count.max())
+    for name, want in (("element_slots", o.element_slots), ("slot_residues", o.slot_residues),
+                       ("slot_real", o.slot_real), ("node_residues", o.node_residues), ("offsets", o.offsets)):
+        assert np.array_equal(t[name], want), name
+    tw = np.concatenate(o.twiddles)
+    assert np.max(np.abs(t["twiddles"] - tw)) < 1e-15
+    assert np.array_equal(S.pivoted_pattern(r, M).as_array(), O.pivoted_pattern(r, M))

@@ -164,3 +164,17 @@ def test_oracle_reference_call_on_workload():
     f = O.synthesize(wl.support, wl.coeffs[0], wl.M)
     got = O.reference_call(f, wl.support, wl.M)
     assert np.linalg.norm(got - wl.coeffs[0]) / np.linalg.norm(wl.coeffs[0]) < 1e-12
+
+
+def test_capi_demo_compiles_with_plain_c(tmp_path):
+    """The C-ABI is usable from plain C (gcc, no torch): compile and link the demo."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    exe = tmp_path / "capi_demo"
+    cmd = ["gcc", "-O2", os.path.join(ROOT, "examples", "capi_demo.c"), "-I", os.path.join(ROOT, "include"),
+           "-I/usr/local/cuda/include", "-L", os.path.join(ROOT, "paper_2211_15299_b200"), "-lsfft_b200",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-lm", "-o", str(exe)]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr

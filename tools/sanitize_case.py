@@ -1,0 +1,36 @@
+"""Small run of every kernel family, for compute-sanitizer (one tool per call)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import paper_2211_15299_b200 as S  # noqa: E402
+import structfft_oracle as O  # noqa: E402
+
+rng = np.random.default_rng(1)
+# plan kernel (shared support), c64 and c128, with shift and height
+J = O.gen_homogeneous((0, 2, 3, 5, 7, 9), 14, 3)
+Js = S.SupportSet(1 << 14, J)
+f = torch.randn(4, 1 << 14, dtype=torch.complex64, device="cuda")
+S.hidft(f, Js, S.pivots(Js), shift=77)
+S.hidft(f.to(torch.complex128), Js, S.pivots(Js), height=2)
+S.hidft_to_dft_batched(f, Js)
+# fused per-signal
+sup = np.stack([O.gen_homogeneous(sorted(rng.choice(14, size=6, replace=False).tolist()), 14, int(rng.integers(1 << 30))) for _ in range(4)])
+S.hidft_to_dft_batched(f, torch.from_numpy(sup).cuda())
+# cluster kernel (s = 15, c64)
+J2 = O.gen_homogeneous(sorted(rng.choice(20, size=15, replace=False).tolist()), 20, 5)
+f2 = torch.randn(2, 1 << 20, dtype=torch.complex64, device="cuda")
+S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J2))
+# SAS mu* > 1 with escalation, band-limited source
+H = O.gen_homogeneous((0, 2, 3, 5, 7, 9, 10), 14, 4)
+Jsub = np.sort(H[rng.choice(H.size, size=40, replace=False)])
+Jb = S.SupportSet(1 << 14, Jsub)
+c = rng.normal(size=40) + 1j * rng.normal(size=40)
+S.sas_transform(S.BandlimitedSignal(Jb, c), Jb, policy="random_subset", family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
+torch.cuda.synchronize()
+print("sanitize case ok")
