@@ -270,6 +270,11 @@ def run_b200(args) -> None:
         "bytes_per_launch": int(G_line), "achieved": round(G_line / (ms_per_step / 1e3) / 1e9, 1),
         "frac": round(G_line / (ms_per_step / 1e3) / 1e9 / hbm, 4),
         "note": "every isolated HBM read moves a 128 B line on this B200 (profiles/r01_gather_granularity.md)"}
+    # practical floor: the measured best rate of isolated line reads (3.94e10 lines/s,
+    # tools/gather_probe*.cu, profiles/r01_gather_granularity.md) for this launch's lines
+    floor_us = (lines / 128) / 3.94e10 * 1e6
+    roof["isolated_line_floor"] = {"us_per_launch": round(floor_us, 2),
+                                   "frac": round(floor_us / (ms_per_step * 1e3), 4)}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
