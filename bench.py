@@ -272,9 +272,11 @@ def run_b200(args) -> None:
         "note": "every isolated HBM read moves a 128 B line on this B200 (profiles/r01_gather_granularity.md)"}
     # practical floor: the measured best rate of isolated line reads (3.94e10 lines/s,
     # tools/gather_probe*.cu, profiles/r01_gather_granularity.md) for this launch's lines
-    floor_us = (lines / 128) / 3.94e10 * 1e6
-    roof["isolated_line_floor"] = {"us_per_launch": round(floor_us, 2),
-                                   "frac": round(floor_us / (ms_per_step * 1e3), 4)}
+    n_samples = B * (pattern_bytes[1] / esz if pattern_bytes and pattern_bytes[1] else wl.k)
+    if lines / 128 >= 0.99 * n_samples:  # every sample in its own line (configs 2-4)
+        floor_us = (lines / 128) / 3.94e10 * 1e6
+        roof["isolated_line_floor"] = {"us_per_launch": round(floor_us, 2),
+                                       "frac": round(floor_us / (ms_per_step * 1e3), 4)}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
