@@ -364,9 +364,11 @@ def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
     dt = (time.perf_counter() - t0) / steps
     del host
     return {"value": B * wl.k / dt, "unit": UNIT, "h2d_bytes_per_step": int(B * A * esz + support_bytes),
-            "d2h_bytes_per_step": int(res.numel() * esz), "seconds_per_step": dt,
-            "path": "public API on a page-locked host tensor: zero-copy gather of the 2^s needed samples "
-                    "per signal over PCIe, result copied to host"}
+            "d2h_bytes_per_step": int(np.asarray(res).size * esz), "seconds_per_step": dt,
+            "path": "public API on a page-locked host tensor -> sfft_hidft_host: native host threads gather "
+                    "the 2^s needed samples per signal into pinned staging while earlier row chunks are "
+                    "copied to the device, transformed and copied back (one stream); per-signal supports "
+                    "(config 4) read the rows zero-copy"}
 
 
 # ------------------------------------------------------- CPU reference ---

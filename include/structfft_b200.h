@@ -60,6 +60,12 @@ enum sfft_out_kind {
   SFFT_OUT_SLOTS = 3  /* HiDftResult.slot_values, slot order (hidft.py:180)                   */
 };
 
+/* layout of pre-gathered sample rows (A = 2^s per row) */
+enum sfft_sample_order {
+  SFFT_ORDER_SLOT = 0,    /* row[a] = f(off(a) - shift), slot order (hidft.py:155-158)          */
+  SFFT_ORDER_PATTERN = 1  /* row[q] = f(I_r[q] - shift), ascending pattern (pivoted_pattern)    */
+};
+
 SFFT_API const char* sfft_version(void);
 SFFT_API const char* sfft_last_error(void);
 /* 1 if the library was compiled for and can run on the current device */
@@ -129,6 +135,12 @@ SFFT_API int sfft_hidft_gathered(const sfft_plan* plan, const void* samples, int
                                  int out_kind, void* out, int64_t ld_out, void* slot_out,
                                  int64_t ld_slot, sfft_stream_t stream);
 
+/* sfft_hidft_gathered for rows in either sample order (SFFT_ORDER_PATTERN:
+ * the layout sfft_host_stage writes and sfft_sas_decode's table reads). */
+SFFT_API int sfft_hidft_staged(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld, int order,
+                               int out_kind, void* out, int64_t ld_out, void* slot_out, int64_t ld_slot,
+                               sfft_stream_t stream);
+
 /* Reorder/scale slot values (B rows, stride ld >= A) into an output kind:
  * hidft_to_dft(res) (hidft.py:188-207) or the mu*=1 SAS read (sas.py:363-371)
  * or node order. */
@@ -174,6 +186,40 @@ SFFT_API int sfft_sas_decode(sfft_plan* plan, const void* nodevals, int64_t ld_n
                              const void* table, const int64_t* bl_J, const void* bl_c, int64_t k_src,
                              const int64_t* J_dev, void* out, int64_t ld_out, int32_t* flags, double* resid,
                              int64_t* n_escalated, int64_t* n_fallback, sfft_stream_t stream);
+
+/* Host staging gather (signals in host memory): out[b*A + a] = signals[b*ld +
+ * locations[a]] for B rows of esz-byte elements (8 = complex64, 16 =
+ * complex128), on a persistent pool of nthreads host threads plus the
+ * caller (<= 0: all cores but the caller's).  Pure data movement feeding
+ * one DMA of B*A elements; the transform then runs on the device with
+ * sfft_hidft_gathered (sfft_hidft_host does both, pipelined). */
+SFFT_API int sfft_host_gather(const void* signals, int64_t B, int64_t ld, int esz, const int64_t* locations,
+                              int64_t A, void* out, int nthreads);
+
+/* hidft(f_b, J, r, height, shift) for B rows resident in HOST memory
+ * (pageable or page-locked), outputs to host memory: the drop-in for the
+ * reference's numpy path (hidft.py:135-185, hidft_to_dft hidft.py:188-207)
+ * with host arrays in and out.  Host threads gather the 2^s samples per row
+ * the plan reads into page-locked staging; row chunks (chunk_rows, <= 0:
+ * B/8, at least 16) are copied to the device, transformed and copied back
+ * on `stream` while later chunks are still being gathered.  nthreads <= 0:
+ * all cores but the caller's.  Synchronous: returns with out / slot_out
+ * written.  Same output kinds and strides as sfft_hidft. */
+SFFT_API int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int64_t shift,
+                             int out_kind, void* out, int64_t ld_out, void* slot_out, int64_t ld_slot,
+                             int64_t chunk_rows, int nthreads, sfft_stream_t stream);
+
+/* Stage the samples a plan reads from HOST-resident rows into DEVICE memory:
+ * output row b*nshift + j (j < nshift) holds f_b((I - shift0 - j) mod N) in
+ * `order` (sfft_sample_order), A = 2^s elements per row at row stride ld_out.
+ * in_dtype is the signals' type; out_dtype may be SFFT_C128 for complex64
+ * signals (promoted on the host, as the reference's float64 path does,
+ * sas.py:343-345).  Host threads gather while finished chunks are copied on
+ * `stream`; returns once every copy is enqueued (later work on `stream` sees
+ * the rows).  Feeds sfft_hidft_staged and sfft_sas_decode's sample table. */
+SFFT_API int sfft_host_stage(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int in_dtype,
+                             int64_t shift0, int64_t nshift, int order, int out_dtype, void* dev_out,
+                             int64_t ld_out, int nthreads, sfft_stream_t stream);
 
 /* Fused hidft(f_b, J_b, pivots(J_b)) + hidft_to_dft for homogeneous supports:
  * pivots, pattern, tables and twiddles are derived on chip per CTA, so one

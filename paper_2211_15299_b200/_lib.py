@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("SFFT_LIB") or os.path.join(_HERE, "libsfft_b200.so")
 OK, ERR_INVALID, ERR_CONTRACT, ERR_BUDGET, ERR_CUDA, ERR_UNSUPPORTED = 0, 2, 3, 4, 5, 6
 C64, C128 = 0, 1
 OUT_NODES, OUT_DFT, OUT_SAS, OUT_SLOTS = 0, 1, 2, 3
+ORDER_SLOT, ORDER_PATTERN = 0, 1
 
 _c = ctypes
 _P = _c.c_void_p
@@ -55,6 +56,11 @@ SIGNATURES = [
     ("sfft_hidft_shifts", _c.c_int, [_P, _P, _I64, _I64, _c.c_int, _I64, _I64, _c.c_int, _P, _I64, _P]),
     ("sfft_sas_decode", _c.c_int, [_P, _P, _I64, _c.c_int, _I64, _I64, _c.c_double, _P, _I64, _c.c_int, _P, _P,
                                    _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    ("sfft_host_gather", _c.c_int, [_P, _I64, _I64, _c.c_int, _P, _I64, _P, _c.c_int]),
+    ("sfft_hidft_host", _c.c_int, [_P, _P, _I64, _I64, _I64, _c.c_int, _P, _I64, _P, _I64, _I64, _c.c_int, _P]),
+    ("sfft_host_stage", _c.c_int, [_P, _P, _I64, _I64, _c.c_int, _I64, _I64, _c.c_int, _c.c_int, _P, _I64,
+                                   _c.c_int, _P]),
+    ("sfft_hidft_staged", _c.c_int, [_P, _P, _I64, _I64, _c.c_int, _c.c_int, _P, _I64, _P, _I64, _P]),
     ("sfft_hidft_to_dft_fused", _c.c_int, [_P, _I64, _I64, _c.c_int, _P, _I64, _I64, _c.c_int, _P,
                                            _I64, _P, _P]),
 ]

@@ -187,7 +187,10 @@ k_hidft_plan(const PlanArgs args) {
   const bool live = b < args.B * args.nshift;
   uint32_t d[S > 0 ? S : 1];
 #pragma unroll
-  for (int i = 0; i < S; ++i) d[i] = args.identity ? (1u << i) : (1u << (args.M - 1 - args.used[i]));
+  for (int i = 0; i < S; ++i)
+    d[i] = args.identity == 1   ? (1u << i)            // pre-gathered, slot order
+           : args.identity == 2 ? (1u << (S - 1 - i))  // pre-gathered, sorted (pattern) order
+                                : (1u << (args.M - 1 - args.used[i]));
   const uint32_t nmask = args.identity ? (uint32_t)(G::A - 1)
                                         : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
   Cx<T> v[G::E];
@@ -355,7 +358,10 @@ k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
   const int q = (int)cluster.block_rank();
   const int t = threadIdx.x;
   const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(args.tw);
-  const uint32_t nmask = (args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u);
+  // pre-gathered rows: slot order (identity 1) or sorted order (identity 2,
+  // coalesced: sorted position u reads row[u])
+  const uint32_t nmask = args.identity ? (uint32_t)((1u << S) - 1u)
+                                       : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
   const uint32_t mb0 = smem_addr(&s_mbar[0]), mb1 = smem_addr(&s_mbar[1]);
   const uint32_t r1_addr = smem_addr(R1), r2_addr = smem_addr(R2);
   if (t == 0) {
@@ -365,7 +371,10 @@ k_hidft_cluster(const PlanArgs args, const int32_t* __restrict__ inv1) {
     mbar_expect_tx(mb1, BYTES);
   }
   cluster.sync();  // barrier inits visible cluster-wide
-#define SFFT_D(i) (1u << (args.M - 1 - args.used[(i)]))
+#define SFFT_D(i)                                                 \
+  (args.identity == 1   ? (1u << (i))                             \
+   : args.identity == 2 ? (1u << (S - 1 - (i)))                   \
+                        : (1u << (args.M - 1 - args.used[(i)])))
   uint32_t offt = args.negshift;
 #pragma unroll
   for (int j = 0; j < LNT; ++j)
@@ -855,9 +864,14 @@ int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld
   a.ld1 = ld1;
   a.out2 = out2;
   a.ld2 = ld2;
-  if (identity && p->s > (p->dtype == SFFT_C64 ? kMaxPlanS_c64 : kMaxPlanS_c128))
-    return fail(SFFT_ERR_UNSUPPORTED, "pre-gathered samples need 2^s within one CTA");
   return dispatch_plan(p->dtype, p->s, a, inv1, st);
+}
+
+// 2^s beyond one CTA: the cluster kernel gathers in sorted order, so
+// pre-gathered rows are best staged in that order (coalesced reads); the
+// single-CTA kernel reads either order from L2-resident staging
+bool gathered_sorted(const sfft_plan* p) {
+  return p->s > (p->dtype == SFFT_C64 ? kMaxPlanS_c64 : kMaxPlanS_c128);
 }
 
 template <typename T>
@@ -948,6 +962,23 @@ extern "C" int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B,
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   return hidft_common(plan, signals, B, ld, 1ll << plan->M, shift, out_kind, out, ld_out, slot_out,
                       ld_slot, 0, (cudaStream_t)stream);
+}
+
+namespace sfft {
+int hidft_gathered(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld, int sorted, int out_kind,
+                   void* out, int64_t ld_out, void* slot_out, int64_t ld_slot, cudaStream_t st) {
+  return hidft_common(plan, samples, B, ld, plan->A, 0, out_kind, out, ld_out, slot_out, ld_slot,
+                      sorted ? 2 : 1, st);
+}
+}  // namespace sfft
+
+extern "C" int sfft_hidft_staged(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld, int order,
+                                 int out_kind, void* out, int64_t ld_out, void* slot_out, int64_t ld_slot,
+                                 sfft_stream_t stream) {
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (order != SFFT_ORDER_SLOT && order != SFFT_ORDER_PATTERN) return fail(SFFT_ERR_INVALID, "unknown sample order");
+  return hidft_gathered(plan, samples, B, ld, order == SFFT_ORDER_PATTERN, out_kind, out, ld_out, slot_out, ld_slot,
+                        (cudaStream_t)stream);
 }
 
 extern "C" int sfft_hidft_gathered(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld,

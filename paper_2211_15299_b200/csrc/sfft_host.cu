@@ -1,0 +1,422 @@
+// Host-resident signals.  Only the 2^s samples per row that the transform
+// reads ever cross PCIe: a persistent pool of host threads gathers them
+// (plan offsets, slot order) into page-locked staging, and the calling thread
+// streams finished row chunks to the device (DMA), runs the gathered
+// transform (sfft_hidft_gathered) and copies each chunk's result back, so
+// gather, both DMA directions and the kernel overlap chunk by chunk.  Rows
+// are handed out through an atomic counter (no static partition: a
+// descheduled worker does not stall a chunk) and the calling thread gathers
+// too while it has nothing to enqueue.  Pure data movement on the host.
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "sfft_common.cuh"
+#include "sfft_plan.h"
+
+namespace sfft {
+
+class HostPool {
+ public:
+  explicit HostPool(int n) {
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int size() const { return (int)workers_.size(); }
+  // start fn(worker) on every worker; returns at once
+  void start(const std::function<void(int)>* fn) {
+    std::lock_guard<std::mutex> lk(mu_);
+    job_ = fn;
+    pending_ = (int)workers_.size();
+    ++gen_;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        job = job_;
+      }
+      (*job)(i);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+static std::mutex g_host_mu;  // one host job at a time through the shared pool and staging
+static HostPool* g_pool = nullptr;
+
+// default: every core but the calling thread's (which gathers too)
+static int default_threads() { return std::max(1, (int)std::thread::hardware_concurrency() - 1); }
+
+static HostPool& pool(int want) {  // caller holds g_host_mu
+  const int n = want > 0 ? want : default_threads();
+  if (!g_pool || g_pool->size() != n) {
+    delete g_pool;
+    g_pool = new HostPool(n);
+  }
+  return *g_pool;
+}
+
+struct C64b { uint64_t v; };
+struct C128b { uint64_t lo, hi; };
+
+template <typename In, typename Out> struct Elem {
+  static Out conv(In v) { return v; }
+};
+template <> struct Elem<float2, double2> {
+  static double2 conv(float2 v) { return {(double)v.x, (double)v.y}; }
+};
+
+// Row dispenser shared by the pool and the calling thread.  Unit = one
+// source row, which produces nshift output rows: row j holds
+// src[(loc[a] - j) & nmask] for a < A (the shifts of one sample share its
+// cache line, so a row is read once for all of them).
+struct RowJob {
+  const char* sig = nullptr;
+  int64_t ld_bytes = 0, B = 0, A = 0, nshift = 1, grain = 1, chunk = 1;
+  uint64_t nmask = ~0ull;
+  int in_esz = 8, out_esz = 8;
+  const int64_t* loc = nullptr;
+  char* out = nullptr;
+  std::atomic<int64_t> next{0};
+  std::unique_ptr<std::atomic<int64_t>[]> done;  // source rows finished per chunk
+
+  template <typename In, typename Out>
+  void rows(int64_t r0, int64_t r1) const {
+    for (int64_t r = r0; r < r1; ++r) {
+      const In* row = reinterpret_cast<const In*>(sig + r * ld_bytes);
+      Out* o = reinterpret_cast<Out*>(out) + r * nshift * A;
+      if (nshift == 1 && nmask == ~0ull) {
+        for (int64_t a = 0; a < A; ++a) o[a] = Elem<In, Out>::conv(row[loc[a]]);
+      } else {
+        for (int64_t a = 0; a < A; ++a) {
+          const uint64_t p = (uint64_t)loc[a];
+          for (int64_t j = 0; j < nshift; ++j) o[j * A + a] = Elem<In, Out>::conv(row[(p - (uint64_t)j) & nmask]);
+        }
+      }
+    }
+  }
+  // gather one grain of source rows; false when none is left
+  bool step() {
+    const int64_t r0 = next.fetch_add(grain, std::memory_order_relaxed);
+    if (r0 >= B) return false;
+    const int64_t r1 = std::min(B, r0 + grain);
+    if (in_esz == 8 && out_esz == 8) rows<C64b, C64b>(r0, r1);
+    else if (in_esz == 8) rows<float2, double2>(r0, r1);
+    else rows<C128b, C128b>(r0, r1);
+    // grains never straddle chunks (chunk is a multiple of grain)
+    if (done) done[r0 / chunk].fetch_add(r1 - r0, std::memory_order_release);
+    return true;
+  }
+  void set_chunking(int64_t chunk_rows) {
+    grain = std::max<int64_t>(1, 4096 / std::max<int64_t>(A * nshift, 1));
+    int64_t c = chunk_rows > 0 ? chunk_rows : std::max<int64_t>(16, (B + 7) / 8);
+    chunk = (c + grain - 1) / grain * grain;
+    const int64_t n = (B + chunk - 1) / chunk;
+    done.reset(new std::atomic<int64_t>[n]);
+    for (int64_t k = 0; k < n; ++k) done[k].store(0, std::memory_order_relaxed);
+  }
+  int64_t nchunks() const { return (B + chunk - 1) / chunk; }
+  int64_t chunk_rows(int64_t c) const { return std::min(chunk, B - c * chunk); }
+  // calling thread: wait for chunk c, gathering rows itself meanwhile
+  void await(int64_t c) {
+    const int64_t want = chunk_rows(c);
+    while (done[c].load(std::memory_order_acquire) < want)
+      if (!step()) std::this_thread::yield();
+  }
+};
+
+// Page-locked and device staging, grown on demand, reused across calls
+// (page-locking per call costs more than the transfer).  h_free is recorded
+// after the last copy that reads h_in; the next job waits on it before
+// overwriting the staging.
+struct Staging {
+  void* h_in = nullptr;  size_t h_in_n = 0;
+  void* h_out = nullptr; size_t h_out_n = 0;
+  void* d_in = nullptr;  size_t d_in_n = 0;
+  void* d_out = nullptr; size_t d_out_n = 0;
+  void* d_slot = nullptr; size_t d_slot_n = 0;
+  cudaEvent_t h_free = nullptr;
+  int device = -1;
+};
+static Staging g_stage;
+
+static int grow_host(void** p, size_t* n, size_t want) {
+  if (*n >= want) return SFFT_OK;
+  if (*p) cudaFreeHost(*p);
+  *p = nullptr;
+  *n = 0;
+  SFFT_CUDA(cudaHostAlloc(p, want, cudaHostAllocPortable));
+  *n = want;
+  return SFFT_OK;
+}
+static int grow_dev(void** p, size_t* n, size_t want) {
+  if (*n >= want) return SFFT_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *n = 0;
+  SFFT_CUDA(cudaMalloc(p, want));
+  *n = want;
+  return SFFT_OK;
+}
+
+// caller holds g_host_mu: staging of the current device, h_in free to write
+static int stage_begin(int dev) {
+  Staging& S = g_stage;
+  if (S.h_free) SFFT_CUDA(cudaEventSynchronize(S.h_free));
+  if (S.device != dev) {  // device buffers of another device: drop them
+    if (S.d_in) cudaFree(S.d_in);
+    if (S.d_out) cudaFree(S.d_out);
+    if (S.d_slot) cudaFree(S.d_slot);
+    if (S.h_free) cudaEventDestroy(S.h_free);
+    S.d_in = S.d_out = S.d_slot = nullptr;
+    S.d_in_n = S.d_out_n = S.d_slot_n = 0;
+    S.h_free = nullptr;
+    S.device = dev;
+  }
+  if (!S.h_free) SFFT_CUDA(cudaEventCreateWithFlags(&S.h_free, cudaEventDisableTiming));
+  return SFFT_OK;
+}
+
+static bool is_pinned_host(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// sample locations of a plan, shift0 applied: slot order (hidft.py:155-158)
+// or ascending pattern order (pattern position u holds slot brev_s(u))
+static std::vector<int64_t> plan_locations(const sfft_plan* p, int64_t shift0, bool pattern_order) {
+  const int64_t N = 1ll << p->M, A = p->A;
+  const int64_t sh = ((shift0 % N) + N) % N;
+  std::vector<int64_t> loc(A);
+  for (int64_t u = 0; u < A; ++u) {
+    int64_t v = 0;
+    for (int i = 0; i < p->s; ++i) {
+      const int bit = pattern_order ? (int)((u >> (p->s - 1 - i)) & 1) : (int)((u >> i) & 1);
+      v += (int64_t)bit << (p->M - 1 - p->used[i]);
+    }
+    loc[u] = (v - sh + N) & (N - 1);
+  }
+  return loc;
+}
+
+}  // namespace sfft
+
+using namespace sfft;
+
+extern "C" int sfft_host_gather(const void* signals, int64_t B, int64_t ld, int esz, const int64_t* locations,
+                                int64_t A, void* out, int nthreads) {
+  if (!signals || !locations || !out) return fail(SFFT_ERR_INVALID, "null pointer");
+  if (esz != 8 && esz != 16) return fail(SFFT_ERR_INVALID, "element size must be 8 or 16 bytes");
+  if (B < 0 || A < 0 || ld < 0) return fail(SFFT_ERR_INVALID, "negative size");
+  if (B == 0 || A == 0) return SFFT_OK;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  HostPool& p = pool(nthreads);
+  RowJob job;
+  job.sig = (const char*)signals;
+  job.ld_bytes = ld * esz;
+  job.B = B;
+  job.A = A;
+  job.in_esz = job.out_esz = esz;
+  job.loc = locations;
+  job.out = (char*)out;
+  job.grain = std::max<int64_t>(1, 4096 / A);
+  const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
+  p.start(&fn);
+  while (job.step()) {}
+  p.wait();
+  return SFFT_OK;
+}
+
+extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int64_t shift,
+                               int out_kind, void* out, int64_t ld_out, void* slot_out, int64_t ld_slot,
+                               int64_t chunk_rows, int nthreads, sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (B < 0) return fail(SFFT_ERR_INVALID, "negative batch");
+  const int32_t* map = nullptr;
+  int64_t n_out = 0;
+  double scale = 1.0;
+  int rc = out_spec(plan, out_kind, &map, &n_out, &scale);
+  if (rc) return rc;
+  if (B == 0) return SFFT_OK;
+  if (!signals || !out) return fail(SFFT_ERR_INVALID, "null signal or output pointer");
+  const int64_t N = 1ll << plan->M, A = plan->A;
+  if (ld < N) return fail(SFFT_ERR_INVALID, "signal row stride too small");
+  if (ld_out < n_out) return fail(SFFT_ERR_INVALID, "output row stride too small");
+  if (slot_out && ld_slot < A) return fail(SFFT_ERR_INVALID, "slot row stride too small");
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  if (dev != plan->device) return fail(SFFT_ERR_INVALID, "plan belongs to another device");
+  const int esz = plan->dtype == SFFT_C64 ? 8 : 16;
+  // the cluster transform reads pre-gathered rows in pattern order: stage
+  // them that way there (coalesced on the device, ascending on the host)
+  const bool sorted = gathered_sorted(plan);
+  const std::vector<int64_t> loc = plan_locations(plan, shift, sorted);
+
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  if ((rc = stage_begin(dev))) return rc;
+  Staging& S = g_stage;
+  const bool out_pinned = is_pinned_host(out);
+  const bool slot_pinned = !slot_out || is_pinned_host(slot_out);
+  const size_t in_bytes = (size_t)B * A * esz, out_bytes = (size_t)B * n_out * esz;
+  const size_t slot_bytes = slot_out ? (size_t)B * A * esz : 0;
+  if ((rc = grow_host(&S.h_in, &S.h_in_n, in_bytes))) return rc;
+  if ((rc = grow_dev(&S.d_in, &S.d_in_n, in_bytes))) return rc;
+  if ((rc = grow_dev(&S.d_out, &S.d_out_n, out_bytes))) return rc;
+  if (slot_out && (rc = grow_dev(&S.d_slot, &S.d_slot_n, slot_bytes))) return rc;
+  if ((!out_pinned || !slot_pinned) &&
+      (rc = grow_host(&S.h_out, &S.h_out_n, (out_pinned ? 0 : out_bytes) + (slot_pinned ? 0 : slot_bytes))))
+    return rc;
+  char* out_tgt = out_pinned ? (char*)out : (char*)S.h_out;
+  const int64_t ldo_tgt = out_pinned ? ld_out : n_out;
+  char* slot_tgt = slot_out ? (slot_pinned ? (char*)slot_out : (char*)S.h_out + (out_pinned ? 0 : out_bytes)) : nullptr;
+  const int64_t lds_tgt = slot_pinned ? ld_slot : A;
+
+  RowJob job;
+  job.sig = (const char*)signals;
+  job.ld_bytes = ld * esz;
+  job.B = B;
+  job.A = A;
+  job.in_esz = job.out_esz = esz;
+  job.loc = loc.data();
+  job.out = (char*)S.h_in;
+  job.set_chunking(chunk_rows);
+
+  HostPool& p = pool(nthreads);
+  const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
+  p.start(&fn);
+  for (int64_t c = 0; c < job.nchunks() && rc == SFFT_OK; ++c) {
+    job.await(c);
+    const int64_t b0 = c * job.chunk, rows = job.chunk_rows(c);
+    const size_t ib = (size_t)b0 * A * esz;
+    char* din = (char*)S.d_in + ib;
+    char* dout = (char*)S.d_out + (size_t)b0 * n_out * esz;
+    char* dslot = slot_out ? (char*)S.d_slot + ib : nullptr;
+    cudaError_t e = cudaMemcpyAsync(din, (char*)S.h_in + ib, (size_t)rows * A * esz, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "host->device chunk copy"); break; }
+    rc = hidft_gathered(plan, din, rows, A, sorted, out_kind, dout, n_out, dslot, A, st);
+    if (rc) break;
+    e = cudaMemcpy2DAsync(out_tgt + (size_t)b0 * ldo_tgt * esz, (size_t)ldo_tgt * esz, dout, (size_t)n_out * esz,
+                          (size_t)n_out * esz, rows, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && slot_out)
+      e = cudaMemcpy2DAsync(slot_tgt + (size_t)b0 * lds_tgt * esz, (size_t)lds_tgt * esz, dslot, (size_t)A * esz,
+                            (size_t)A * esz, rows, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "device->host chunk copy");
+  }
+  while (job.step()) {}  // on error: drain so no worker still reads the caller's rows
+  p.wait();
+  cudaEventRecord(S.h_free, st);
+  const cudaError_t es = cudaStreamSynchronize(st);
+  if (rc) return rc;
+  if (es != cudaSuccess) return cuda_fail(es, "host transform");
+  // pageable outputs: copy out of the pinned result staging
+  for (int k = 0; k < 2; ++k) {
+    const bool slot = k == 1;
+    if (slot ? (!slot_out || slot_pinned) : out_pinned) continue;
+    const char* src = slot ? slot_tgt : out_tgt;
+    char* dst = (char*)(slot ? slot_out : out);
+    const int64_t w = slot ? A : n_out, ldd = slot ? ld_slot : ld_out;
+    for (int64_t b = 0; b < B; ++b) std::memcpy(dst + (size_t)b * ldd * esz, src + (size_t)b * w * esz, (size_t)w * esz);
+  }
+  return SFFT_OK;
+}
+
+extern "C" int sfft_host_stage(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int in_dtype,
+                               int64_t shift0, int64_t nshift, int order, int out_dtype, void* dev_out,
+                               int64_t ld_out, int nthreads, sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (B < 0 || nshift < 1) return fail(SFFT_ERR_INVALID, "negative batch or nshift < 1");
+  if (in_dtype != SFFT_C64 && in_dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown input dtype");
+  if (out_dtype != SFFT_C64 && out_dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown output dtype");
+  if (in_dtype == SFFT_C128 && out_dtype == SFFT_C64)
+    return fail(SFFT_ERR_INVALID, "complex128 signals cannot be staged as complex64");
+  if (order != SFFT_ORDER_SLOT && order != SFFT_ORDER_PATTERN) return fail(SFFT_ERR_INVALID, "unknown sample order");
+  if (B == 0) return SFFT_OK;
+  if (!signals || !dev_out) return fail(SFFT_ERR_INVALID, "null signal or output pointer");
+  const int64_t N = 1ll << plan->M, A = plan->A;
+  if (ld < N) return fail(SFFT_ERR_INVALID, "signal row stride too small");
+  if (ld_out < A) return fail(SFFT_ERR_INVALID, "output row stride too small");
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  if (dev != plan->device) return fail(SFFT_ERR_INVALID, "plan belongs to another device");
+  const int iesz = in_dtype == SFFT_C64 ? 8 : 16, oesz = out_dtype == SFFT_C64 ? 8 : 16;
+  const std::vector<int64_t> loc = plan_locations(plan, shift0, order == SFFT_ORDER_PATTERN);
+
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  int rc = stage_begin(dev);
+  if (rc) return rc;
+  Staging& S = g_stage;
+  const int64_t rowlen = nshift * A;  // output elements per source row
+  if ((rc = grow_host(&S.h_in, &S.h_in_n, (size_t)B * rowlen * oesz))) return rc;
+  RowJob job;
+  job.sig = (const char*)signals;
+  job.ld_bytes = ld * iesz;
+  job.B = B;
+  job.A = A;
+  job.nshift = nshift;
+  job.nmask = (uint64_t)(N - 1);
+  job.in_esz = iesz;
+  job.out_esz = oesz;
+  job.loc = loc.data();
+  job.out = (char*)S.h_in;
+  job.set_chunking(0);
+
+  HostPool& p = pool(nthreads);
+  const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
+  p.start(&fn);
+  for (int64_t c = 0; c < job.nchunks() && rc == SFFT_OK; ++c) {
+    job.await(c);
+    const int64_t r0 = c * job.chunk * nshift, rows = job.chunk_rows(c) * nshift;  // output rows
+    const cudaError_t e = cudaMemcpy2DAsync((char*)dev_out + (size_t)r0 * ld_out * oesz, (size_t)ld_out * oesz,
+                                            (char*)S.h_in + (size_t)r0 * A * oesz, (size_t)A * oesz,
+                                            (size_t)A * oesz, rows, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host->device staging copy");
+  }
+  while (job.step()) {}
+  p.wait();
+  cudaEventRecord(S.h_free, st);
+  return rc;
+}

@@ -30,6 +30,11 @@ int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld
                       int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st,
                       int64_t nshift = 1, int in_c64 = 0);
 int max_supported_s(int dtype);
+// pre-gathered rows (identity loads): slot order, or sorted order when
+// gathered_sorted(plan) (the cluster transform, 2^s beyond one CTA)
+bool gathered_sorted(const sfft_plan* p);
+int hidft_gathered(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld, int sorted, int out_kind,
+                   void* out, int64_t ld_out, void* slot_out, int64_t ld_slot, cudaStream_t st);
 int out_spec(const sfft_plan* plan, int out_kind, const int32_t** map, int64_t* n_out, double* scale,
              const int32_t** inv = nullptr);
 }  // namespace sfft

@@ -9,9 +9,10 @@ runs the butterfly and writes (Ff)_J in ascending-J order.
 Sources (hidft.py:34-49):
   * CUDA tensor (N,) or (B, N), complex64 / complex128 -> computed in that
     precision (complex64 signals run the float32 kernels);
-  * page-locked CPU tensor -> zero-copy gather over PCIe (only the 2^s
-    samples per signal cross the bus);
-  * pageable numpy / CPU tensor -> copied to the device once;
+  * host-resident numpy / CPU tensor -> the library's host thread pool
+    gathers the 2^s samples per signal into pinned staging, pipelined with
+    their DMA, the device transform and the copy back (only those samples
+    cross PCIe; per-signal supports read page-locked rows zero-copy);
   * callable loc -> samples, or an object with `sample_block(loc)` (e.g. the
     reference's BandlimitedSignal) -> evaluated at the plan's offsets on the
     host, then transformed on the device.
@@ -21,6 +22,7 @@ Results are CUDA tensors for CUDA sources and numpy arrays otherwise.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Any, Sequence
 
@@ -146,9 +148,7 @@ def _prepare_source(source, N: int) -> _Src:
             t2 = t2.contiguous()
         if t2.is_cuda:
             return _Src("device", t2, batched, _DT[t2.dtype], t2.device)
-        if t2.is_pinned():
-            return _Src("pinned", t2, batched, _DT[t2.dtype], dev)
-        return _Src("host", t2.to(dev), batched, _DT[t2.dtype], dev)
+        return _Src("host", t2, batched, _DT[t2.dtype], dev)  # gathered on the host, see _host_gather
     if hasattr(source, "support") and hasattr(source, "coeffs") and hasattr(source, "sample_block"):
         # BandlimitedSignal (ours or the reference's): synthesise on the device
         from .signals import BandlimitedSignal
@@ -166,12 +166,40 @@ def _prepare_source(source, N: int) -> _Src:
     if arr.ndim not in (1, 2) or arr.shape[-1] != N:
         raise InvalidInputError("dense signal must be a length-N vector or a (B, N) batch")
     batched = arr.ndim == 2
-    t = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1, N))).to(dev)
+    t = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1, N)))
     return _Src("host", t, batched, _DT[t.dtype], dev)
 
 
 def _signal_ptr(src: _Src) -> int:
     return src.tensor.data_ptr()
+
+
+HOST_GATHER_THREADS = 0   # host gather workers besides the caller; 0: every other core
+HOST_CHUNK_ROWS = 0       # rows per pipelined chunk; 0: B/8 (at least 16)
+
+
+def _host_threads() -> int:
+    return HOST_GATHER_THREADS
+
+
+def _host_transform(sig, plan: "ButterflyPlan", shift: int, out_kind: int, n_out: int, with_slots=False):
+    """Transform host-resident rows through sfft_hidft_host: native host
+    threads gather each row's 2^s samples into page-locked staging while
+    earlier row chunks are copied to the device, transformed
+    (sfft_hidft_gathered) and copied back, all on the current stream.
+    Returns the (B, n_out) result (and the (B, A) slot values) in pinned host
+    memory."""
+    torch = _torch()
+    lib = _lib.load()
+    B = sig.shape[0]
+    out_host = torch.empty((B, n_out), dtype=sig.dtype, pin_memory=True)
+    slots = torch.empty((B, plan.A), dtype=sig.dtype, pin_memory=True) if with_slots else None
+    with torch.cuda.device(plan.device):
+        sp = _lib.stream_ptr(plan.device)
+        _lib.check(lib.sfft_hidft_host(plan.handle, sig.data_ptr(), B, sig.stride(0), int(shift), out_kind,
+                                       out_host.data_ptr(), n_out, slots.data_ptr() if with_slots else None,
+                                       plan.A, HOST_CHUNK_ROWS, HOST_GATHER_THREADS, sp))
+    return (out_host, slots) if with_slots else out_host
 
 
 def _gathered_samples(src: _Src, plan: "ButterflyPlan", shift: int):
@@ -281,6 +309,10 @@ def hidft(source, J, r: Sequence[int], height: int = 0, shift: int = 0, counter=
         _lib.check(lib.sfft_hidft_gathered(plan.handle, samples.data_ptr(), B, plan.A, _lib.OUT_NODES,
                                            nodes.data_ptr(), nodes.shape[1], slots.data_ptr(), plan.A,
                                            stream))
+    elif src.kind == "host":
+        sig = src.tensor
+        B = sig.shape[0]
+        nodes, slots = _host_transform(sig, plan, shift, _lib.OUT_NODES, max(plan.n_nodes, 1), with_slots=True)
     else:
         sig = src.tensor
         B = sig.shape[0]
@@ -334,8 +366,9 @@ def hidft_to_dft(res: HiDftResult, counter=None):
 def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
     """Fused hidft(f_b, J_b, pivots(J_b)) + hidft_to_dft for a batch.
 
-    signals: (B, N) complex64/complex128 CUDA tensor, or a page-locked CPU
-    tensor (zero-copy gather; the result is then returned on the host).
+    signals: (B, N) complex64/complex128 CUDA tensor, or a CPU tensor (the
+    needed samples are gathered on the host and the result returned on the
+    host; with per-signal supports a page-locked tensor is read zero-copy).
     J: one SupportSet shared by all rows, or a (B, k) int64 tensor with one
     sorted support per row (config 4).  Per-row statuses land in `status`
     (int32 device tensor) when given; with check=True a non-homogeneous or
@@ -355,9 +388,6 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
     if N & (N - 1):
         raise InvalidInputError(f"N={N} is not a power of two")
     host_out = not sig.is_cuda
-    if host_out and not sig.is_pinned():
-        sig = sig.to(dev)
-        host_out = True
     run_dev = sig.device if sig.is_cuda else dev
     if not torch.is_tensor(J) and (isinstance(J, SupportSet) or hasattr(J, "indices")):
         Js = as_support(J)
@@ -373,7 +403,7 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         nsup, k = B, jt.shape[1]
         Js = None
     code = _DT[sig.dtype]
-    if out is None:
+    if out is None and not (host_out and Js is not None):
         out = torch.empty((B, k), dtype=sig.dtype, device=run_dev)
     lib = _lib.load()
     stream = _lib.stream_ptr(run_dev)
@@ -385,10 +415,14 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         if not cls.is_homogeneous:
             raise ContractViolationError("hidft_to_dft requires a homogeneous support")
         plan = get_plan(Js, cls.pivots, 0, code, run_dev)
+        if host_out:  # host-resident signals: host gather of the needed samples, pipelined DMA
+            res = _host_transform(sig, plan, 0, _lib.OUT_DFT, k)
+            return res[0] if single else res
         _lib.check(lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_DFT,
                                   out.data_ptr(), out.stride(0), None, 0, stream))
-        res = out[0] if single else out
-        return res.cpu() if host_out else res
+        return out[0] if single else out
+    if host_out and not sig.is_pinned():
+        sig = sig.to(run_dev)  # per-signal plans are derived on chip: the kernel reads the rows
     if st is None and check:
         st = torch.zeros(nsup, dtype=torch.int32, device=run_dev)
     _lib.check(lib.sfft_hidft_to_dft_fused(jt.data_ptr(), k, nsup, M, sig.data_ptr(), B, sig.stride(0),

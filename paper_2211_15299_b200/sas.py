@@ -24,7 +24,8 @@ from . import _lib
 from .congruence import (SupportSet, as_support, assert_part_homogeneous, pivots as support_pivots,
                          validate_pivot_vector)
 from .errors import InvalidInputError
-from .hidft import _count, _finish, _gathered_samples, _prepare_source, _torch, get_plan
+from .hidft import (_count, _finish, _gathered_samples, _host_threads, _host_transform, _prepare_source, _torch,
+                    get_plan)
 
 C1 = 1.5  # per-stage butterfly constant (sas.py:38)
 C2 = 6.0  # Vandermonde constant (sas.py:39)
@@ -236,6 +237,8 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
             out = torch.empty((1, k), dtype=cdt, device=dev)
             _lib.check(lib.sfft_hidft_gathered(plan.handle, samples.data_ptr(), 1, plan.A, _lib.OUT_SAS,
                                                out.data_ptr(), k, None, 0, stream))
+        elif src.kind == "host":  # host rows: host gather of the 2^s samples, pipelined DMA
+            out = _host_transform(src.tensor, plan, 0, _lib.OUT_SAS, k)
         else:
             sig = src.tensor
             out = torch.empty((B, k), dtype=cdt, device=dev)
@@ -263,6 +266,18 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
                 vals = np.asarray(src.fn(locs.reshape(-1)), dtype=np.complex128).reshape(mu, A)
                 table_t = torch.from_numpy(vals).to(dev)
                 table = table_t.data_ptr()
+        elif src.kind == "host":
+            # host rows: the host pool stages the mu* shifted sample sets per
+            # signal (pattern order, promoted to complex128) on the device;
+            # they feed the shifted transforms and the escalation re-measure
+            sig = src.tensor
+            table_t = torch.empty((B * mu, A), dtype=torch.complex128, device=dev)
+            _lib.check(lib.sfft_host_stage(plan64.handle, sig.data_ptr(), B, sig.stride(0), src.dtype_code, 0, mu,
+                                           _lib.ORDER_PATTERN, _lib.C128, table_t.data_ptr(), A,
+                                           _host_threads(), stream))
+            _lib.check(lib.sfft_hidft_staged(plan64.handle, table_t.data_ptr(), B * mu, A, _lib.ORDER_PATTERN,
+                                             _lib.OUT_NODES, nodevals.data_ptr(), nn, None, 0, stream))
+            table = table_t.data_ptr()
         else:
             sig = src.tensor
             _lib.check(lib.sfft_hidft_shifts(plan64.handle, sig.data_ptr(), B, sig.stride(0), src.dtype_code, 0, mu,

@@ -269,6 +269,112 @@ def test_pinned_zero_copy(S, torch):
         assert rel_l2(got[b].numpy(), O.hidft_to_dft(f[b], J, M)) < 1e-5
 
 
+def _check_stage(torch, lib, _lib, plan, f, shift, code, tdt):
+    """sfft_host_stage (two shifts, pattern order) + sfft_hidft_staged equal
+    the direct-gather transform at shift and shift + 1, bit for bit."""
+    B, N = f.shape
+    A, nn = plan.A, max(plan.n_nodes, 1)
+    sp = _lib.stream_ptr(0)
+    rows = torch.empty((2 * B, A), dtype=tdt, device="cuda")
+    _lib.check(lib.sfft_host_stage(plan.handle, f.ctypes.data, B, N, code, shift, 2, _lib.ORDER_PATTERN, code,
+                                   rows.data_ptr(), A, 3, sp))
+    got = torch.empty((2 * B, nn), dtype=tdt, device="cuda")
+    _lib.check(lib.sfft_hidft_staged(plan.handle, rows.data_ptr(), 2 * B, A, _lib.ORDER_PATTERN, _lib.OUT_NODES,
+                                     got.data_ptr(), nn, None, 0, sp))
+    d = torch.from_numpy(f).cuda()
+    for j in range(2):
+        want = torch.empty((B, nn), dtype=tdt, device="cuda")
+        _lib.check(lib.sfft_hidft(plan.handle, d.data_ptr(), B, N, shift + j, _lib.OUT_NODES, want.data_ptr(), nn,
+                                  None, 0, sp))
+        assert torch.equal(got[j::2], want)
+
+
+@pytest.mark.parametrize("dt,pinned", [(np.complex64, False), (np.complex128, True)])
+def test_hidft_host_capi(S, torch, dt, pinned):
+    """sfft_hidft_host: host rows in, host results out (pageable or pinned),
+    chunked pipeline with a few workers; bit-identical to the device path."""
+    from paper_2211_15299_b200 import _lib
+    from paper_2211_15299_b200.hidft import get_plan
+    J, M = O.config_support(1)
+    N, B, shift = 1 << M, 37, 5
+    rng = np.random.default_rng(7)
+    f = (rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(dt)
+    Js = S.SupportSet(N, J)
+    code = _lib.C64 if dt == np.complex64 else _lib.C128
+    plan = get_plan(Js, S.pivots(Js), 0, code, torch.device("cuda", 0))
+    lib = _lib.load()
+    tdt = torch.complex64 if dt == np.complex64 else torch.complex128
+    sig = torch.from_numpy(f)
+    if pinned:
+        sig = sig.pin_memory()
+    nn = max(plan.n_nodes, 1)
+    out = torch.zeros((B, nn + 3), dtype=tdt, pin_memory=pinned)
+    slots = torch.zeros((B, plan.A), dtype=tdt, pin_memory=pinned)
+    sp = _lib.stream_ptr(0)
+    _lib.check(lib.sfft_hidft_host(plan.handle, sig.data_ptr(), B, N, shift, _lib.OUT_NODES, out.data_ptr(),
+                                   nn + 3, slots.data_ptr(), plan.A, 5, 3, sp))
+    d = sig.cuda()
+    want = torch.zeros((B, nn), dtype=tdt, device="cuda")
+    want_s = torch.zeros((B, plan.A), dtype=tdt, device="cuda")
+    _lib.check(lib.sfft_hidft(plan.handle, d.data_ptr(), B, N, shift, _lib.OUT_NODES, want.data_ptr(), nn,
+                              want_s.data_ptr(), plan.A, sp))
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, :nn], want.cpu())
+    assert torch.equal(out[:, nn:], torch.zeros((B, 3), dtype=tdt))
+    assert torch.equal(slots, want_s.cpu())
+    # DFT output kind, default chunking and threads
+    coeffs = torch.zeros((B, len(J)), dtype=tdt)
+    _lib.check(lib.sfft_hidft_host(plan.handle, sig.data_ptr(), B, N, 0, _lib.OUT_DFT, coeffs.data_ptr(),
+                                   len(J), None, 0, 0, 0, sp))
+    for b in (0, B - 1):
+        assert rel_l2(coeffs[b].numpy(), O.hidft_to_dft(f[b], J, M)) < TOL[dt]
+    _check_stage(torch, lib, _lib, plan, f, shift, code, tdt)
+
+
+@pytest.mark.parametrize("dt,s", [(np.complex64, 15), (np.complex64, 16), (np.complex128, 14)])
+def test_gathered_cluster_paths(S, torch, dt, s):
+    """2^s beyond one CTA (thread-block cluster transform): host rows through
+    sfft_hidft_host (sorted-order staging) and device rows pre-gathered in
+    slot order through sfft_hidft_gathered match the direct-gather launch
+    bit for bit."""
+    from paper_2211_15299_b200 import _lib
+    from paper_2211_15299_b200.hidft import get_plan
+    M, B, shift = 20, 3, 11
+    N = 1 << M
+    J = np.arange(1 << s, dtype=np.int64) * 4 + 1  # homogeneous, pivots 2..s+1
+    rng = np.random.default_rng(s)
+    f = (rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(dt)
+    Js = S.SupportSet(N, J)
+    code = _lib.C64 if dt == np.complex64 else _lib.C128
+    tdt = torch.complex64 if dt == np.complex64 else torch.complex128
+    plan = get_plan(Js, S.pivots(Js), 0, code, torch.device("cuda", 0))
+    assert plan.A == 1 << s
+    lib = _lib.load()
+    sp = _lib.stream_ptr(0)
+    d = torch.from_numpy(f).cuda()
+    want = torch.empty((B, len(J)), dtype=tdt, device="cuda")
+    _lib.check(lib.sfft_hidft(plan.handle, d.data_ptr(), B, N, 0, _lib.OUT_DFT, want.data_ptr(), len(J),
+                              None, 0, sp))
+    host = torch.empty((B, len(J)), dtype=tdt)
+    _lib.check(lib.sfft_hidft_host(plan.handle, torch.from_numpy(f).data_ptr(), B, N, 0, _lib.OUT_DFT,
+                                   host.data_ptr(), len(J), None, 0, 0, 0, sp))
+    assert torch.equal(host, want.cpu())
+    # slot-order pre-gathered rows, with a shift
+    loc = torch.from_numpy((plan.tables()["offsets"] - shift) % N).cuda()
+    g = d[:, loc].contiguous()
+    nodes_d = torch.empty((B, plan.n_nodes), dtype=tdt, device="cuda")
+    nodes_g = torch.empty_like(nodes_d)
+    _lib.check(lib.sfft_hidft(plan.handle, d.data_ptr(), B, N, shift, _lib.OUT_NODES, nodes_d.data_ptr(),
+                              plan.n_nodes, None, 0, sp))
+    _lib.check(lib.sfft_hidft_gathered(plan.handle, g.data_ptr(), B, plan.A, _lib.OUT_NODES, nodes_g.data_ptr(),
+                                       plan.n_nodes, None, 0, sp))
+    torch.cuda.synchronize()
+    assert torch.equal(nodes_g, nodes_d)
+    b = B - 1
+    assert rel_l2(want[b].cpu().numpy(), O.hidft_to_dft(f[b], J, M)) < TOL[dt]
+    _check_stage(torch, lib, _lib, plan, f, shift, code, tdt)
+
+
 # ------------------------------------------------- configs at full size ---
 
 def _synth(torch, S, cfg, B, per_signal_rows=None):

@@ -117,6 +117,32 @@ def test_config3_reference_policies(S, golden_sas, pol):
     assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-8
 
 
+def test_config3_host_rows(S, golden_sas):
+    """Config 3 rows resident in host memory (pinned and pageable): the host
+    pool stages the mu* shifted sample sets (sfft_host_stage) and the result
+    matches the device-resident path."""
+    import torch
+    import structfft_oracle as O
+    g = golden_sas
+    J, M = O.config_support(3)
+    Js = S.SupportSet(1 << M, J)
+    B = 2
+    coef = np.stack([O.config_coefficients(3, b, J.size) for b in range(B)])
+    f = np.stack([O.synthesize(J, coef[b], M) for b in range(B)]).astype(np.complex64)
+    base = tuple(int(x) for x in g["cfg3_base_pivots"])
+    meta = {"base_pivots": base}
+    dev = S.sas_transform(torch.from_numpy(f).cuda(), Js, policy="auto", family_meta=meta)
+    want = dev.coeffs.cpu().numpy()
+    for host in (torch.from_numpy(f).pin_memory(), f):
+        res = S.sas_transform(host, Js, policy="auto", family_meta=meta)
+        assert res.plan.mu_star == dev.plan.mu_star > 1
+        got = np.asarray(res.coeffs)
+        assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+        assert res.report.escalated_nodes == dev.report.escalated_nodes
+    for b in range(B):
+        assert np.linalg.norm(want[b] - coef[b]) / np.linalg.norm(coef[b]) < 1e-4
+
+
 def test_select_pivots_policies(S):
     # reference tests/test_sas.py TestSelectPivots
     import math
