@@ -355,13 +355,19 @@ def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
 
         def call():
             return S.hidft_to_dft_batched(host, J)
-    for _ in range(2):
-        call()
+    res = None
+    for _ in range(max(3, args.warmup)):  # same pattern as the timed loop: warms the pinned host cache
+        res = call()
     steps = max(3, min(args.steps, args.e2e_steps))
+    per = []
     t0 = time.perf_counter()
     for _ in range(steps):
+        t1 = time.perf_counter()
         res = call()
+        per.append(time.perf_counter() - t1)
     dt = (time.perf_counter() - t0) / steps
+    print(f"e2e per-step ms: min {min(per) * 1e3:.3f} median {sorted(per)[len(per) // 2] * 1e3:.3f} "
+          f"max {max(per) * 1e3:.3f}", file=sys.stderr)
     del host
     return {"value": B * wl.k / dt, "unit": UNIT, "h2d_bytes_per_step": int(B * A * esz + support_bytes),
             "d2h_bytes_per_step": int(np.asarray(res).size * esz), "seconds_per_step": dt,
