@@ -60,6 +60,17 @@ int main(void) {
   for (int i = 0; i < 2 * k; ++i) err = fmax(err, fabs(out[i] - c[i]));
   printf("max |coeff - planted| = %.3e\n", err);
 
+  /* the same transform from a plain host array, results to a host array */
+  double* hsig = (double*)malloc(16 * N);
+  cudaMemcpy(hsig, dsig, 16 * N, cudaMemcpyDeviceToHost);
+  double hout[16];
+  CHECK(sfft_hidft_host(plan, hsig, 1, N, 0, SFFT_OUT_DFT, hout, k, NULL, 0, 0, 0, 0));
+  double herr = 0;
+  for (int i = 0; i < 2 * k; ++i) herr = fmax(herr, fabs(hout[i] - out[i]));
+  printf("host-array path: max |diff| vs device path = %.3e\n", herr);
+  free(hsig);
+  if (herr != 0.0) return 4;
+
   /* the contract errors come back as status codes */
   int32_t bad[1] = {5};
   sfft_plan* p2 = NULL;

@@ -191,6 +191,34 @@ class SasResult:
         return {int(j): complex(v) for j, v in zip(self.support.indices, c)}
 
 
+def _sas_static(plan64, J: SupportSet, rt: tuple[int, ...], dev, stream) -> dict:
+    """Per-plan constants of sas_transform, computed once and cached on the
+    (immutable) plan: node membership CSR, node weights, the SasPlan, the
+    samples-touched count and the per-signal solve/read op counts."""
+    st = getattr(plan64, "_sas_static", None)
+    if st is not None:
+        return st
+    lib = _lib.load()
+    k, mu, N, A = len(J), plan64.mu_star, J.N, plan64.A
+    off = np.empty(plan64.n_nodes + 1, np.int32)
+    mem = np.empty(k, np.int32)
+    _lib.check(lib.sfft_plan_nodes(plan64.handle, off.ctypes.data, mem.ctypes.data, stream))
+    w = np.diff(off).astype(np.int64)
+    weights = tuple(int(x) for x in w)
+    splan = SasPlan(rt, plan64.level, mu, weights, predicted_cost(len(rt), mu, weights))
+    from .sampling import pivoted_pattern_tensor
+    pat = pivoted_pattern_tensor(rt, J.M, dev).cpu().numpy() if rt else np.zeros(1, np.int64)
+    single, multi = w == 1, w >= 2
+    half = w * (w - 1) // 2
+    st = {"off": off, "mem": mem, "w": w, "splan": splan, "touched": _samples_touched(pat, mu, N),
+          "read_mul": int(single.sum()) if N != A else 0,
+          "solve_mul": (int(w[multi].sum()) if N != A else 0) + int((w * (w - 1))[multi].sum() + half[w >= 3].sum()),
+          "solve_add": int((3 * half)[multi].sum() + half[w >= 3].sum())}
+    plan64._sas_static = st
+    plan64._nodes = (off, mem)
+    return st
+
+
 def _samples_touched(pattern: np.ndarray, mu: int, N: int) -> int:
     """|union_{j < mu} (I - j) mod N| from the sorted pattern's circular gaps."""
     if pattern.size == 1:
@@ -217,14 +245,8 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
     plan64 = get_plan(J, rt, 0, _lib.C128, dev)
     mu, level, A, N, k = plan64.mu_star, plan64.level, plan64.A, J.N, len(J)
     scale = N / A
-    if getattr(plan64, "_nodes", None) is None:
-        off = np.empty(plan64.n_nodes + 1, np.int32)
-        mem = np.empty(k, np.int32)
-        _lib.check(lib.sfft_plan_nodes(plan64.handle, off.ctypes.data, mem.ctypes.data, stream))
-        plan64._nodes = (off, mem)
-    off, mem = plan64._nodes
-    weights = tuple(int(w) for w in np.diff(off))
-    splan = SasPlan(rt, level, mu, weights, predicted_cost(len(rt), mu, weights))
+    st = _sas_static(plan64, J, rt, dev, stream)
+    off, mem, splan = st["off"], st["mem"], st["splan"]
     counter.count_bit_ops(k * max(level, 1))  # build_tree(J, level) as SasPlan.plan does
     B = 1 if src.kind in ("callable", "synth") else src.tensor.shape[0]
     nn = plan64.n_nodes
@@ -245,8 +267,7 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
             _lib.check(lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_SAS,
                                       out.data_ptr(), k, None, 0, stream))
         n_esc = n_fb = 0
-        resid_h = np.zeros(nn)
-        flags_h = np.zeros(nn, np.int32)
+        resid_h = flags_h = None
     else:
         if mu > 64:
             raise NotImplementedError(f"node weight mu*={mu} above the device decoder's 64")
@@ -298,28 +319,25 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
     if plan64.s:  # mu* shifted Hi-DFTs per signal: A/2 mults + A adds per stage (hidft.py:165-167)
         counter.mul((A // 2) * plan64.s * mu * B, phase="hidft")
         counter.add(A * plan64.s * mu * B, phase="hidft")
-    fb_per_node = (flags.cpu().numpy() == 2).sum(0) if flags is not None else np.zeros(nn, np.int64)
-    w = np.asarray(weights, np.int64)
-    single, multi = w == 1, w >= 2
-    half = w * (w - 1) // 2
-    if scale != 1.0:
-        counter.mul(int(single.sum()) * B, phase="read")
-        counter.mul(int(w[multi].sum()) * B, phase="solve")
-    counter.mul(int((w * (w - 1))[multi].sum() + half[w >= 3].sum()) * B, phase="solve")
-    counter.add(int((3 * half)[multi].sum() + half[w >= 3].sum()) * B, phase="solve")
-    nfb = int((fb_per_node * w ** 3).sum())
-    if nfb:
+    if st["read_mul"]:
+        counter.mul(st["read_mul"] * B, phase="read")
+    counter.mul(st["solve_mul"] * B, phase="solve")
+    counter.add(st["solve_add"] * B, phase="solve")
+    if n_fb:
+        fb_per_node = (flags.cpu().numpy() == 2).sum(0)
+        nfb = int((fb_per_node * st["w"] ** 3).sum())
         counter.mul(nfb, phase="solve")
         counter.add(nfb, phase="solve")
-    from .sampling import pivoted_pattern_tensor
-    pat = pivoted_pattern_tensor(rt, J.M, dev).cpu().numpy() if rt else np.zeros(1, np.int64)
-    report = CostReport.from_counter(counter, samples_touched=_samples_touched(pat, mu, N),
+    report = CostReport.from_counter(counter, samples_touched=st["touched"],
                                      bound_alg1bnd=splan.predicted_cost, bound_hidft=C1 * len(rt) * (1 << len(rt)),
                                      escalated_nodes=n_esc, dense_fallbacks=n_fb)
+
     def systems():
         node_res = plan64.tables()["node_residues"].tolist()
         members = np.split(J._arr[mem], off[1:-1])
-        return [NodeSystem(node_res[v], tuple(members[v].tolist()), escalated=bool(flags_h[v] == 1),
-                           dense_fallback=bool(flags_h[v] == 2), residual=float(resid_h[v])) for v in range(nn)]
+        fl = flags_h if flags_h is not None else np.zeros(nn, np.int32)
+        rs = resid_h if resid_h is not None else np.zeros(nn)
+        return [NodeSystem(node_res[v], tuple(members[v].tolist()), escalated=bool(fl[v] == 1),
+                           dense_fallback=bool(fl[v] == 2), residual=float(rs[v])) for v in range(nn)]
 
     return SasResult(J, _finish(out, src), splan, report, systems, flags)
