@@ -292,8 +292,20 @@ __device__ unsigned long long g_phase_stamps[1 << 20][8];
   do {                                                                              \
     if (threadIdx.x == 0 && blockIdx.x < (1u << 20)) g_phase_stamps[blockIdx.x][i] = clock64(); \
   } while (0)
+// accumulate time since the previous mark into slot i (thread 0)
+#define SFFT_ACC_INIT() unsigned long long acc_t0__ = clock64()
+#define SFFT_ACC(i)                                                                   \
+  do {                                                                                \
+    if (threadIdx.x == 0 && blockIdx.x < (1u << 20)) {                               \
+      const unsigned long long t__ = clock64();                                        \
+      g_phase_stamps[blockIdx.x][i] += t__ - acc_t0__;                                 \
+      acc_t0__ = t__;                                                                  \
+    }                                                                                 \
+  } while (0)
 #else
 #define SFFT_STAMP(i) do {} while (0)
+#define SFFT_ACC_INIT() do {} while (0)
+#define SFFT_ACC(i) do {} while (0)
 #endif
 
 // 16-byte remote async store into another CTA's shared memory, completing on
@@ -773,14 +785,566 @@ static int run_cluster_kernel(const PlanArgs& a, const int32_t* inv1, cudaStream
   return SFFT_OK;
 }
 
-// largest s handled on one CTA (data for one signal resident in shared memory)
-constexpr int kMaxPlanS_c64 = 14, kMaxPlanS_c128 = 13;
+// ------------------------------------------ two-pass split for large A ---
+//
+// 2^s slots beyond one SM (configs 5/6) run as two kernels per chunk of
+// rows, exchanging through an L2-resident scratch instead of DSMEM:
+//
+//  front (k_split_front): stage k pairs slot bit k-1, i.e. sorted-order bit
+//    s-k, so the first lc stages pair samples 2^(s-lc), 2^(s-lc+1), ...
+//    apart in SORTED order.  A thread owns one sorted low position p and
+//    its 2^lc partners u = x*2^(s-lc) + p, loads them (warps read
+//    consecutive p: contiguous runs of the pattern, full lines), runs the
+//    lc stages in registers (the 2^lc - 1 twiddles depend only on x), and
+//    stores value x to scratch block x at position p (coalesced).
+//  back (k_split_back): block t = the sorted range [t*2^(s-lc), ...) =
+//    the slots whose low lc bits are brev(t); its remaining s - lc stages
+//    pair bits lc.. s-1 only, i.e. they are local.  One CTA per (row, t)
+//    loads the block (coalesced) into shared memory at slot positions,
+//    runs the single-CTA butterfly with the block's twiddle slice
+//    (plan->d_tw_blk) and stores through the block-major inverse map.
+//
+// Chunks of rows keep the scratch (rows x 2^s complex) within ~32 MiB so it
+// stays in L2 between the two kernels: HBM sees the samples once and the
+// results once (measured L2-resident streaming: ~12 TB/s read, ~7 TB/s write,
+// tools/l2_probe.cu).
+template <int B>
+__host__ __device__ constexpr uint32_t brev_c(uint32_t x) {
+  uint32_t r = 0;
+  for (int i = 0; i < B; ++i) r |= ((x >> i) & 1u) << (B - 1 - i);
+  return r;
+}
+
+template <typename T, int S, int LC>
+struct SplitGeo {
+  static constexpr int SL = S - LC, EX = 1 << LC;
+  static constexpr int NT1 = 256;                    // front: threads per CTA
+  static constexpr int NSEG = (1 << SL) / NT1;       // front CTAs per row
+  using G = Geo<T, SL>;                              // back: single-CTA geometry
+  static_assert(G::SPC == 1, "back pass: one block per CTA");
+#ifndef SFFT_BACK_BMIN
+#define SFFT_BACK_BMIN 2
+#endif
+  static constexpr int BMIN = G::NT <= 256 ? SFFT_BACK_BMIN : 1;  // back: CTAs per SM
+  // back: double-buffered rows + inverse map in shared memory when 1-2 CTAs
+  // fit per SM; one row buffer (more CTAs hide each other's loads) otherwise
+  static constexpr bool DB = BMIN < 3;
+  static constexpr size_t SMEM = (size_t)(1 << SL) * ((DB ? 3 : 2) * sizeof(Cx<T>) + (DB ? sizeof(int32_t) : 0));
+};
+
+template <typename T, int S, int LC>
+__global__ void __launch_bounds__(256) k_split_front(const PlanArgs args, Cx<T>* __restrict__ scratch,
+                                                     int64_t row0) {
+  using SG = SplitGeo<T, S, LC>;
+  constexpr int SL = SG::SL, EX = SG::EX;
+  const int64_t rr = blockIdx.x / SG::NSEG;  // row within the chunk
+  const uint32_t p = (blockIdx.x % SG::NSEG) * SG::NT1 + threadIdx.x;
+  const int64_t r = row0 + rr;               // output row
+  const int64_t bs = (args.debug_skip & 16) ? (r & 1) : r / args.nshift;  // bit 4: footprint probe
+  // slot bit i -> sample stride d_i (hidft.py:155-158), or the pre-gathered layouts
+  uint32_t d[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i)
+    d[i] = args.identity == 1   ? (1u << i)
+           : args.identity == 2 ? (1u << (S - 1 - i))
+                                : (1u << (args.M - 1 - args.used[i]));
+  const uint32_t nmask = args.identity ? (uint32_t)((1u << S) - 1u)
+                                       : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
+  // sorted bit j <-> slot bit S-1-j
+  uint32_t off = args.identity ? 0u : ((args.negshift - (uint32_t)(r % args.nshift)) & nmask);
+#pragma unroll
+  for (int j = 0; j < SL; ++j)
+    if ((p >> j) & 1u) off += d[S - 1 - j];
+  Cx<T> v[EX];
+#pragma unroll
+  for (int x = 0; x < EX; ++x) {
+    uint32_t o = off;
+#pragma unroll
+    for (int j = 0; j < LC; ++j)
+      if ((x >> j) & 1) o += d[LC - 1 - j];
+    if (sizeof(T) == 8 && args.in_c64) {
+      const Cx<float> sv = load_sample(reinterpret_cast<const Cx<float>*>(args.sig) + bs * args.ld + (o & nmask));
+      v[x] = Cx<T>{(T)sv.x, (T)sv.y};
+    } else {
+      v[x] = load_sample(reinterpret_cast<const Cx<T>*>(args.sig) + bs * args.ld + (o & nmask));
+    }
+  }
+  // stages 1..LC: stage k pairs slot bit k-1 = x bit LC-k; twiddle index
+  // a mod 2^(k-1) = brev_LC(x) mod 2^(k-1) (hidft.py:160-167)
+  const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(args.tw);
+#pragma unroll
+  for (int k = 1; k <= LC; ++k) {
+    const int lb = LC - k;
+#pragma unroll
+    for (int x = 0; x < EX; ++x) {
+      if (x & (1 << lb)) continue;
+      const uint32_t h = brev_c<LC>((uint32_t)x) & ((1u << (k - 1)) - 1u);
+      bfly(v[x], v[x | (1 << lb)], tw[(1 << (k - 1)) - 1 + h]);
+    }
+  }
+  Cx<T>* dst = scratch + ((rr * EX) << SL) + p;
+#pragma unroll
+  for (int x = 0; x < EX; ++x) dst[(int64_t)x << SL] = v[x];
+}
+
+// cp.async of one element (8 B c64 / 16 B c128) global -> shared, L2 only
+__device__ __forceinline__ void cp_async_elem(void* sdst, const Cx<float>* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_addr(sdst)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_elem(void* sdst, const Cx<double>* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(sdst)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+// Persistent: CTA i serves block tb = i mod 2^lc for rows i / 2^lc, + nper, ...
+// of the chunk.  The block's twiddle slice and inverse map are staged in
+// shared memory once (the same for every row); rows are double-buffered:
+// the next row's block is copied (cp.async, straight into its bit-reversed
+// slot positions) while this row's butterfly and stores run.
+template <typename T, int S, int LC>
+__global__ void __launch_bounds__(SplitGeo<T, S, LC>::G::NT, SplitGeo<T, S, LC>::BMIN)
+k_split_back(const PlanArgs args, const Cx<T>* __restrict__ scratch, int64_t row0, int64_t nrows, int nper,
+             const Cx<T>* __restrict__ tw_blk, const int32_t* __restrict__ inv_blk) {
+  using SG = SplitGeo<T, S, LC>;
+  using G = typename SG::G;
+  constexpr int SL = SG::SL, EX = SG::EX, AL = 1 << SL, NT = G::NT, PT = AL / NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool DB = SG::DB;
+  Cx<T>* sbuf = reinterpret_cast<Cx<T>*>(smem_raw);  // (DB ? 2 : 1) x AL
+  Cx<T>* stw = sbuf + (DB ? 2 : 1) * AL;
+  int32_t* sinv = reinterpret_cast<int32_t*>(stw + AL);  // DB only
+  const int tid = threadIdx.x;
+  const int tb = blockIdx.x % EX;
+  const int64_t first = blockIdx.x / EX;
+  if (first >= nrows) return;
+  // block tb in sorted order: position j holds local slot brev_SL(j)
+  auto issue = [&](int64_t rr, Cx<T>* dst) {
+    const Cx<T>* src = scratch + ((rr * EX + tb) << SL);
+#pragma unroll
+    for (int n = 0; n < PT; ++n) {
+      const int j = tid + n * NT;
+      cp_async_elem(dst + swz<T, SL>((int)(__brev((uint32_t)j) >> (32 - SL))), src + j);
+    }
+    cp_async_commit();
+  };
+  issue(first, sbuf);
+  {
+    const Cx<T>* twg = tw_blk + (int64_t)tb * (AL - 1);
+    Cx<T> t[PT];
+    int32_t e[PT];
+#pragma unroll
+    for (int n = 0; n < PT; ++n) {
+      const int i = tid + n * NT;
+      t[n] = i < AL - 1 ? twg[i] : Cx<T>{T(0), T(0)};
+      e[n] = (DB && inv_blk) ? __ldg(inv_blk + ((int64_t)tb << SL) + i) : 0;
+    }
+#pragma unroll
+    for (int n = 0; n < PT; ++n) {
+      const int i = tid + n * NT;
+      if (i < AL - 1) stw[i] = t[n];
+      if (DB) sinv[i] = e[n];
+    }
+  }
+  const T scale = (T)args.scale1;
+  const uint32_t lowbits = brev_c<LC>((uint32_t)tb);  // fixed low slot bits of this block
+  int cur = 0;
+  for (int64_t rr = first; rr < nrows; rr += nper, cur ^= 1) {
+    const int64_t r = row0 + rr;
+    Cx<T>* sd = sbuf + (DB ? cur * AL : 0);
+    if (!DB) {
+      if (rr != first) issue(rr, sbuf);
+      cp_async_wait<0>();
+    } else if (rr + nper < nrows) {
+      issue(rr + nper, sbuf + (cur ^ 1) * AL);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // this row's block (and the tables) visible to all threads
+    Cx<T> v[G::E];
+    if (!(args.debug_skip & 4)) butterfly<T, SL, true>(v, tid, sd, stw);
+    Cx<T> val[PT];
+    int32_t e[PT];
+#pragma unroll
+    for (int n = 0; n < PT; ++n) {
+      const int l = tid + n * NT;
+      val[n] = sd[swz<T, SL>(l)];
+      e[n] = DB ? sinv[l] : (inv_blk ? __ldg(inv_blk + ((int64_t)tb << SL) + l) : 0);
+    }
+    Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + r * args.ld1;
+    if (args.debug_skip & 2) {
+#pragma unroll
+      for (int n = 0; n < PT; ++n)
+        if (e[n] == -7) o1[n] = val[n];
+    } else if (args.debug_skip & 8) {  // coalesced stores (timing probe only)
+#pragma unroll
+      for (int n = 0; n < PT; ++n) o1[(tb << SL) + tid + n * NT] = val[n];
+    } else if (inv_blk) {
+#pragma unroll
+      for (int n = 0; n < PT; ++n)
+        if (e[n] >= 0) o1[e[n]] = cscale(val[n], scale);
+    } else {  // slot order output
+#pragma unroll
+      for (int n = 0; n < PT; ++n) o1[((uint32_t)(tid + n * NT) << LC) | lowbits] = cscale(val[n], scale);
+    }
+    if (args.out2) {
+      Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + r * args.ld2;
+#pragma unroll
+      for (int n = 0; n < PT; ++n) o2[((uint32_t)(tid + n * NT) << LC) | lowbits] = val[n];
+    }
+    __syncthreads();  // sd is refilled (two rows on when double-buffered)
+  }
+}
+
+// ------------------------------------------------ fused persistent split ---
+//
+// One cooperative (all CTAs co-resident) launch runs both passes as a
+// software pipeline.  CTAs form groups of 2^lc; group g owns rows g, g + G,
+// ...; CTA q of a group does front segment q and back block q of each of
+// the group's rows.  Per row i a CTA: issues the cp.async gather of row
+// i+1's front segment into shared memory; waits (global counter, acquire)
+// until the group's 2^lc front segments of row i are in the scratch ring;
+// stages its back block; runs the butterfly and the scattered stores
+// (row i+1's samples arrive meanwhile); then finishes row i+1's front
+// stages and publishes them (release).  The ring (2 rows per group) stays
+// in L2, so HBM sees the samples once and the results once, and the HBM
+// gather overlaps the shared-memory butterfly of the previous row.
+static int scratch_pool(int dev, cudaMemPool_t* pool);
+
+struct SplitSync {
+  unsigned int* front;  // [G][2]: front segments stored, cumulative per slot
+  unsigned int* back;   // [G][2]: back blocks staged (slot consumed), cumulative
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+// thread 0 waits for *p >= target; co-residency (cooperative launch) makes
+// this deadlock-free; the bound only turns a logic error into a fault
+__device__ __forceinline__ void wait_count(const unsigned int* p, unsigned int target) {
+  if (threadIdx.x == 0) {
+    unsigned int spins = 0;
+    while (ld_acquire_gpu(p) < target) {
+      __nanosleep(40);
+      if (++spins > (1u << 28)) __trap();
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ Cx<float> ld_cg(const Cx<float>* p) {
+  Cx<float> r;
+  asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Cx<double> ld_cg(const Cx<double>* p) {
+  Cx<double> r;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+template <typename T, int S, int LC, typename In>
+struct FusedSplitGeo {
+  using SG = SplitGeo<T, S, LC>;
+  using G = typename SG::G;
+  static constexpr int SL = SG::SL, EX = SG::EX, AL = 1 << SL, NT = G::NT;
+  static constexpr int PQ = AL / EX;  // front positions per CTA
+  static constexpr size_t SMEM = (size_t)AL * (2 * sizeof(Cx<T>) + sizeof(int32_t) + sizeof(Cx<In>));
+  static constexpr int BMIN = SMEM * 2 <= 227 * 1024 && NT <= 256 ? 2 : 1;
+};
+
+template <typename T, int S, int LC, typename In>
+__global__ void __launch_bounds__(FusedSplitGeo<T, S, LC, In>::NT, FusedSplitGeo<T, S, LC, In>::BMIN)
+k_split_fused(const PlanArgs args, Cx<T>* __restrict__ ring, SplitSync sync, const Cx<T>* __restrict__ tw_blk,
+              const int32_t* __restrict__ inv_blk) {
+  using FG = FusedSplitGeo<T, S, LC, In>;
+  using G = typename FG::G;
+  constexpr int SL = FG::SL, EX = FG::EX, AL = FG::AL, NT = FG::NT, PQ = FG::PQ, PT = AL / NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* sd = reinterpret_cast<Cx<T>*>(smem_raw);
+  Cx<T>* stw = sd + AL;
+  int32_t* sinv = reinterpret_cast<int32_t*>(stw + AL);
+  Cx<In>* sf = reinterpret_cast<Cx<In>*>(sinv + AL);  // front samples [x][p - q*PQ]
+  const int tid = threadIdx.x;
+  const int q = blockIdx.x % EX;
+  const int64_t g = blockIdx.x / EX, ngroups = gridDim.x / EX;
+  const int64_t rows = args.B * args.nshift;
+  if (g >= rows) return;
+  const int64_t nmine = (rows - g + ngroups - 1) / ngroups;
+  Cx<T>* myring = ring + (g * 2) * ((int64_t)EX << SL);
+  unsigned int* fcnt = sync.front + g * 2;
+  unsigned int* bcnt = sync.back + g * 2;
+
+  // sample strides: slot bit i -> d_i (hidft.py:155-158) or pre-gathered layouts
+  uint32_t d[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i)
+    d[i] = args.identity == 1   ? (1u << i)
+           : args.identity == 2 ? (1u << (S - 1 - i))
+                                : (1u << (args.M - 1 - args.used[i]));
+  const uint32_t nmask = args.identity ? (uint32_t)((1u << S) - 1u)
+                                       : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
+  // front gather of row i: cp.async of this CTA's PQ positions x 2^lc
+  // partners; the offsets (without the row's shift) are fixed per thread
+  constexpr int FPT = EX * PQ / NT;  // front samples per thread
+  static_assert(EX * PQ % NT == 0, "front split");
+  uint32_t foff[FPT];
+#pragma unroll
+  for (int n = 0; n < FPT; ++n) {
+    const int idx = tid + n * NT;
+    const int x = idx / PQ;
+    const uint32_t p = (uint32_t)(q * PQ + idx % PQ);
+    uint32_t o = 0;
+    for (int j = 0; j < SL; ++j)
+      if ((p >> j) & 1u) o += d[S - 1 - j];
+    for (int j = 0; j < LC; ++j)
+      if ((x >> j) & 1) o += d[LC - 1 - j];
+    foff[n] = o;
+  }
+  auto front_issue = [&](int64_t i) {
+    const int64_t r = g + i * ngroups;
+    const int64_t bs = r / args.nshift;
+    const uint32_t base = args.identity ? 0u : ((args.negshift - (uint32_t)(r % args.nshift)) & nmask);
+    const Cx<In>* row = reinterpret_cast<const Cx<In>*>(args.sig) + bs * args.ld;
+#pragma unroll
+    for (int n = 0; n < FPT; ++n) cp_async_elem(sf + tid + n * NT, row + ((base + foff[n]) & nmask));
+    cp_async_commit();
+  };
+  // front stages of row i (samples in sf), stored to the ring and published
+  auto front_finish = [&](int64_t i) {
+    const int slot = (int)(i & 1);
+    Cx<T>* dst = myring + (int64_t)slot * ((int64_t)EX << SL);
+    // slot reuse: row i-2's blocks must have been staged by the whole group
+    if (i >= 2) wait_count(bcnt + slot, (unsigned)(EX * (i / 2)));
+    const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(args.tw);
+    for (int pl = tid; pl < PQ; pl += NT) {
+      Cx<T> v[EX];
+#pragma unroll
+      for (int x = 0; x < EX; ++x) {
+        const Cx<In> sv = sf[x * PQ + pl];
+        v[x] = Cx<T>{(T)sv.x, (T)sv.y};
+      }
+#pragma unroll
+      for (int k = 1; k <= LC; ++k) {
+        const int lb = LC - k;
+#pragma unroll
+        for (int x = 0; x < EX; ++x) {
+          if (x & (1 << lb)) continue;
+          const uint32_t h = brev_c<LC>((uint32_t)x) & ((1u << (k - 1)) - 1u);
+          bfly(v[x], v[x | (1 << lb)], tw[(1 << (k - 1)) - 1 + h]);
+        }
+      }
+      const int p = q * PQ + pl;
+#pragma unroll
+      for (int x = 0; x < EX; ++x) dst[((int64_t)x << SL) + p] = v[x];
+    }
+    __syncthreads();  // every thread's stores precede thread 0's (cumulative) release
+  };
+  // publish row i's front segment: released late so the ring stores have
+  // drained by then (the release waits for them)
+  auto front_publish = [&](int64_t i) {
+    if (tid == 0) red_release_gpu(fcnt + (int)(i & 1), 1u);
+  };
+
+  // tables of back block q, staged once
+  {
+    const Cx<T>* twg = tw_blk + (int64_t)q * (AL - 1);
+    for (int i = tid; i < AL - 1; i += NT) stw[i] = twg[i];
+    for (int i = tid; i < AL; i += NT) sinv[i] = inv_blk ? __ldg(inv_blk + ((int64_t)q << SL) + i) : 0;
+  }
+  front_issue(0);
+  cp_async_wait<0>();
+  __syncthreads();
+  front_finish(0);
+  front_publish(0);
+  const T scale = (T)args.scale1;
+  const uint32_t lowbits = brev_c<LC>((uint32_t)q);
+  SFFT_ACC_INIT();
+  for (int64_t i = 0; i < nmine; ++i) {
+    const int64_t r = g + i * ngroups;
+    const int slot = (int)(i & 1);
+    const bool more = i + 1 < nmine;
+    if (more) front_issue(i + 1);  // samples of the next row fly during this row's back pass
+    if (i > 0) front_publish(i);   // row i's front segment, finished last iteration
+    SFFT_ACC(0);
+    wait_count(fcnt + slot, (unsigned)(EX * (i / 2 + 1)));
+    SFFT_ACC(1);
+    {  // stage back block q of row i (sorted order -> slot positions), L2 loads
+      const Cx<T>* src = myring + (int64_t)slot * ((int64_t)EX << SL) + ((int64_t)q << SL);
+      Cx<T> t[PT];
+#pragma unroll
+      for (int n = 0; n < PT; ++n) t[n] = ld_cg(src + tid + n * NT);
+#pragma unroll
+      for (int n = 0; n < PT; ++n) {
+        const int j = tid + n * NT;
+        sd[swz<T, SL>((int)(__brev((uint32_t)j) >> (32 - SL)))] = t[n];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) red_release_gpu(bcnt + slot, 1u);  // slot may be refilled once all 2^lc staged
+    SFFT_ACC(2);
+    Cx<T> v[G::E];
+    butterfly<T, SL, true>(v, tid, sd, stw);
+    SFFT_ACC(3);
+    Cx<T> val[PT];
+    int32_t e[PT];
+#pragma unroll
+    for (int n = 0; n < PT; ++n) {
+      const int l = tid + n * NT;
+      val[n] = sd[swz<T, SL>(l)];
+      e[n] = sinv[l];
+    }
+    Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + r * args.ld1;
+    if (inv_blk) {
+#pragma unroll
+      for (int n = 0; n < PT; ++n)
+        if (e[n] >= 0) o1[e[n]] = cscale(val[n], scale);
+    } else {
+#pragma unroll
+      for (int n = 0; n < PT; ++n) o1[((uint32_t)(tid + n * NT) << LC) | lowbits] = cscale(val[n], scale);
+    }
+    if (args.out2) {
+      Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + r * args.ld2;
+#pragma unroll
+      for (int n = 0; n < PT; ++n) o2[((uint32_t)(tid + n * NT) << LC) | lowbits] = val[n];
+    }
+    SFFT_ACC(4);
+    if (more) {
+      cp_async_wait<0>();
+      __syncthreads();  // next row's samples landed; sd reads of this row done
+      SFFT_ACC(5);
+      front_finish(i + 1);
+      SFFT_ACC(6);
+    } else {
+      __syncthreads();
+    }
+  }
+}
+
+template <typename T, int S, int LC, typename In>
+static int run_split_fused(const sfft_plan* p, const PlanArgs& a, const int32_t* inv_blk, cudaStream_t st) {
+  using FG = FusedSplitGeo<T, S, LC, In>;
+  auto kern = k_split_fused<T, S, LC, In>;
+  static_assert(FG::SMEM <= 227 * 1024, "fused split smem");
+  int occ = 0, rc;
+  if ((rc = kernel_occupancy(kern, FG::NT, FG::SMEM, &occ))) return rc;
+  const int64_t rows = a.B * a.nshift;
+  if (rows == 0) return SFFT_OK;
+  const int64_t G = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)num_sms() * occ / FG::EX));
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  if ((rc = scratch_pool(dev, &pool))) return rc;
+  const size_t ring_bytes = (size_t)G * 2 * (sizeof(Cx<T>) << S);
+  const size_t sync_bytes = (size_t)G * 4 * sizeof(unsigned int);
+  void* buf = nullptr;
+  SFFT_CUDA(cudaMallocFromPoolAsync(&buf, ring_bytes + sync_bytes, pool, st));
+  unsigned int* cnt = reinterpret_cast<unsigned int*>((char*)buf + ring_bytes);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, sync_bytes, st);
+  if (e == cudaSuccess) {
+    PlanArgs aa = a;
+    Cx<T>* ring = reinterpret_cast<Cx<T>*>(buf);
+    SplitSync sy{cnt, cnt + 2 * G};
+    const Cx<T>* twb = reinterpret_cast<const Cx<T>*>(p->d_tw_blk);
+    void* params[] = {(void*)&aa, (void*)&ring, (void*)&sy, (void*)&twb, (void*)&inv_blk};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)(G * FG::EX)), dim3(FG::NT), params, FG::SMEM,
+                                    st);
+  }
+  cudaFreeAsync(buf, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fused split launch");
+  return SFFT_OK;
+}
+
+// stream-ordered scratch from a library-owned pool that keeps its memory
+static int scratch_pool(int dev, cudaMemPool_t* pool) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) {
+    *pool = it->second;
+    return SFFT_OK;
+  }
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t p;
+  SFFT_CUDA(cudaMemPoolCreate(&p, &props));
+  uint64_t keep = ~0ull;
+  SFFT_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep));
+  pools[dev] = p;
+  *pool = p;
+  return SFFT_OK;
+}
+
+template <typename T, int S, int LC>
+static int run_split(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
+  using SG = SplitGeo<T, S, LC>;
+  using G = typename SG::G;
+  if (p->split_lc != LC || !p->d_tw_blk) return fail(SFFT_ERR_INVALID, "plan has no split tables");
+  const int32_t* inv_blk = inv1 == p->d_inv_elem ? p->d_inv_elem_blk
+                           : inv1 == p->d_inv_node ? p->d_inv_node_blk
+                                                   : nullptr;
+  if (inv1 && !inv_blk) return fail(SFFT_ERR_INVALID, "no block-major map for this output");
+  // the fused persistent pipeline measured slower than two launches on config 5
+  // (200 vs 185 us, tools/split_time.py); kept selectable for study
+  static const bool fused = [] { const char* e = getenv("SFFT_SPLIT"); return e && std::string(e) == "fused"; }();
+  if (fused) {
+    if (sizeof(T) == 8 && a.in_c64) return run_split_fused<T, S, LC, float>(p, a, inv_blk, st);
+    return run_split_fused<T, S, LC, T>(p, a, inv_blk, st);
+  }
+  auto front = k_split_front<T, S, LC>;
+  auto back = k_split_back<T, S, LC>;
+  PlanArgs ab = a;
+  static const int dbg = [] { const char* e = getenv("SFFT_SPLIT_DEBUG"); return e ? atoi(e) : 0; }();
+  ab.debug_skip = dbg;
+  int occ = 0, rc;
+  if ((rc = kernel_occupancy(back, G::NT, SG::SMEM, &occ))) return rc;
+  const int64_t rows = a.B * a.nshift;
+  if (rows == 0) return SFFT_OK;
+  const size_t row_bytes = sizeof(Cx<T>) << S;
+  static const int64_t scr_mb = [] {
+    const char* e = getenv("SFFT_SPLIT_SCRATCH_MB");
+    return (int64_t)(e ? std::max(1, atoi(e)) : 128);  // measured best for config 5 (tools/cfg5_sweep.sh)
+  }();
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(rows, (scr_mb << 20) / (int64_t)row_bytes));
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  if ((rc = scratch_pool(dev, &pool))) return rc;
+  void* scr = nullptr;
+  SFFT_CUDA(cudaMallocFromPoolAsync(&scr, (size_t)chunk * row_bytes, pool, st));
+  const Cx<T>* twb = reinterpret_cast<const Cx<T>*>(p->d_tw_blk);
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t n = std::min(chunk, rows - r0);
+    front<<<(unsigned)(n * SG::NSEG), SG::NT1, 0, st>>>(ab, (Cx<T>*)scr, r0);
+    const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)num_sms() * occ / SG::EX));
+    back<<<(unsigned)(nper * SG::EX), G::NT, SG::SMEM, st>>>(ab, (const Cx<T>*)scr, r0, n, nper, twb, inv_blk);
+  }
+  const cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(scr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "split transform launch");
+  return SFFT_OK;
+}
+
+static bool use_cluster_path() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_LARGE");
+    return e && std::string(e) == "cluster";
+  }();
+  return v;
+}
+
 constexpr int kMaxFusedS_c64 = 13, kMaxFusedS_c128 = 12;
 
-// cluster path: slices of 2^13 (c64) / 2^12 (c128) slots, C = 4..16 CTAs
-constexpr int kMaxClusterS_c64 = 17, kMaxClusterS_c128 = 16;
-
-int max_supported_s(int dtype) { return dtype == SFFT_C64 ? kMaxClusterS_c64 : kMaxClusterS_c128; }
+int max_supported_s(int dtype) { return dtype == SFFT_C64 ? kMaxSplitS_c64 : kMaxSplitS_c128; }
 
 #define SFFT_CASES_12(M_, ...) \
   M_(0, __VA_ARGS__) M_(1, __VA_ARGS__) M_(2, __VA_ARGS__) M_(3, __VA_ARGS__) M_(4, __VA_ARGS__) \
@@ -790,7 +1354,25 @@ int max_supported_s(int dtype) { return dtype == SFFT_C64 ? kMaxClusterS_c64 : k
 #define PLAN_CASE(S_, T_) case S_: return run_plan_kernel<T_, S_>(a, st);
 #define FUSED_CASE(S_, T_, PS_) case S_: return run_fused_kernel<T_, S_, PS_>(a, st);
 
-static int dispatch_plan(int dtype, int s, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
+static int dispatch_plan(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
+  const int dtype = p->dtype, s = p->s;
+  if (p->split_lc && !use_cluster_path()) {
+    if (dtype == SFFT_C64) {
+      switch (s) {
+        case 15: return run_split<float, 15, 3>(p, a, inv1, st);
+        case 16: return run_split<float, 16, 4>(p, a, inv1, st);
+        case 17: return run_split<float, 17, 4>(p, a, inv1, st);
+        default: break;
+      }
+    } else {
+      switch (s) {
+        case 14: return run_split<double, 14, 2>(p, a, inv1, st);
+        case 15: return run_split<double, 15, 3>(p, a, inv1, st);
+        case 16: return run_split<double, 16, 4>(p, a, inv1, st);
+        default: break;
+      }
+    }
+  }
   if (dtype == SFFT_C64) {
     switch (s) {
       SFFT_CASES_12(PLAN_CASE, float)
@@ -864,7 +1446,7 @@ int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld
   a.ld1 = ld1;
   a.out2 = out2;
   a.ld2 = ld2;
-  return dispatch_plan(p->dtype, p->s, a, inv1, st);
+  return dispatch_plan(p, a, inv1, st);
 }
 
 // 2^s beyond one CTA: the cluster kernel gathers in sorted order, so
@@ -1081,6 +1663,12 @@ extern "C" int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_su
 extern "C" SFFT_API int sfft_debug_stamps(unsigned long long* out, int nblocks) {
   SFFT_CUDA(cudaDeviceSynchronize());
   SFFT_CUDA(cudaMemcpyFromSymbol(out, sfft::g_phase_stamps, sizeof(unsigned long long) * 8 * nblocks));
+  return SFFT_OK;
+}
+extern "C" SFFT_API int sfft_debug_reset(int nblocks) {
+  void* p = nullptr;
+  SFFT_CUDA(cudaGetSymbolAddress(&p, sfft::g_phase_stamps));
+  SFFT_CUDA(cudaMemset(p, 0, sizeof(unsigned long long) * 8 * nblocks));
   return SFFT_OK;
 }
 #endif

@@ -472,6 +472,30 @@ extern "C" int sfft_pivoted_pattern(const int32_t* r, int n_r, int M, int64_t* o
   return SFFT_OK;
 }
 
+// Block-major tables of the split transform: block t (2^lc of them) holds the
+// slots a = (l << lc) | brev_lc(t); its local stage k' (global stage lc + k')
+// twiddle h' is tw_{lc+k'}[(h' << lc) | brev_lc(t)] (hidft.py:160-167).
+template <typename T>
+__global__ void k_split_tables(const Cx<T>* __restrict__ tw, const int32_t* __restrict__ inv_elem,
+                               const int32_t* __restrict__ inv_node, int s, int lc, Cx<T>* __restrict__ tw_blk,
+                               int32_t* __restrict__ inv_elem_blk, int32_t* __restrict__ inv_node_blk) {
+  const int sl = s - lc;
+  const int64_t A = 1ll << s, AL = 1ll << sl;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(i >> sl), l = (uint32_t)(i & (AL - 1));
+    const uint32_t low = lc ? (__brev(t) >> (32 - lc)) : 0u;
+    const uint32_t a = (l << lc) | low;
+    inv_elem_blk[i] = inv_elem[a];
+    inv_node_blk[i] = inv_node[a];
+    if (l + 1 < AL) {  // local stage-major index m = l: stage k' = floor(log2(m+1)) + 1
+      const int kp = 32 - __clz(l + 1);
+      const uint32_t hp = l + 1 - (1u << (kp - 1));
+      const int k = lc + kp;
+      tw_blk[(int64_t)t * (AL - 1) + l] = tw[((int64_t)1 << (k - 1)) - 1 + ((hp << lc) | low)];
+    }
+  }
+}
+
 static void plan_free(sfft_plan* p) {
   if (!p) return;
   cudaFree(p->d_element_slots);
@@ -484,6 +508,9 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_inv_node);
   cudaFree(p->d_node_off);
   cudaFree(p->d_node_mem);
+  cudaFree(p->d_tw_blk);
+  cudaFree(p->d_inv_elem_blk);
+  cudaFree(p->d_inv_node_blk);
   delete p;
 }
 
@@ -593,6 +620,22 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
                                              (const uint32_t*)R.bitmap.p, (const uint32_t*)R.wprefix.p,
                                              (const uint32_t*)R.bsum.p, p->d_node_slots, p->d_node_residues,
                                              p->d_inv_node);
+  }
+  p->split_lc = split_lc(dtype, s);
+  if (p->split_lc) {  // block-major tables of the two-pass transform (sfft_hidft.cu, k_split_*)
+    const int lc = p->split_lc, sl = s - lc;
+    M_(&p->d_tw_blk, csz * ((size_t)1 << lc) * (((size_t)1 << sl) - 1));
+    M_((void**)&p->d_inv_elem_blk, 4 * A);
+    M_((void**)&p->d_inv_node_blk, 4 * A);
+    if (e != cudaSuccess) return done(cuda_fail(e, "split table allocation"));
+    if (dtype == SFFT_C64)
+      k_split_tables<float><<<grid_1d(A), 256, 0, st>>>((const Cx<float>*)p->d_twiddles, p->d_inv_elem, p->d_inv_node,
+                                                        s, lc, (Cx<float>*)p->d_tw_blk, p->d_inv_elem_blk,
+                                                        p->d_inv_node_blk);
+    else
+      k_split_tables<double><<<grid_1d(A), 256, 0, st>>>((const Cx<double>*)p->d_twiddles, p->d_inv_elem,
+                                                         p->d_inv_node, s, lc, (Cx<double>*)p->d_tw_blk,
+                                                         p->d_inv_elem_blk, p->d_inv_node_blk);
   }
   unsigned long long h[2];
   if (cudaGetLastError() != cudaSuccess ||

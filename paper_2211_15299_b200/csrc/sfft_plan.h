@@ -21,9 +21,25 @@ struct sfft_plan {
   int32_t* d_inv_node;       // A   slot -> node rank (-1: virtual)
   int32_t* d_node_off;       // n_nodes+1  node membership CSR (built on first SAS decode)
   int32_t* d_node_mem;       // k          member element indices, ascending per node
+  // two-pass (split) transform for 2^s beyond one CTA (sfft_hidft.cu, k_split_*):
+  // block t of 2^lc holds the slots whose low lc bits are brev_lc(t)
+  int split_lc;              // lc (0: single-CTA plan)
+  void* d_tw_blk;            // 2^lc x (2^(s-lc) - 1) twiddles of the local stages, per block, stage-major
+  int32_t* d_inv_elem_blk;   // A   d_inv_elem, block-major: [t][l] = inv_elem[(l << lc) | brev_lc(t)]
+  int32_t* d_inv_node_blk;   // A   d_inv_node, block-major
 };
 
 namespace sfft {
+// largest s handled on one CTA (one signal's slots resident in shared memory)
+constexpr int kMaxPlanS_c64 = 14, kMaxPlanS_c128 = 13;
+// largest s of the device transform (two-pass split beyond kMaxPlanS)
+constexpr int kMaxSplitS_c64 = 17, kMaxSplitS_c128 = 16;
+// split for 2^s beyond one CTA: the first lc stages run across 2^lc blocks,
+// the remaining s - lc (12, or 13 for s = 17) inside one CTA per block
+inline int split_lc(int dtype, int s) {
+  if (dtype == SFFT_C64) return (s > kMaxPlanS_c64 && s <= kMaxSplitS_c64) ? (s == 17 ? 4 : s - 12) : 0;
+  return (s > kMaxPlanS_c128 && s <= kMaxSplitS_c128) ? s - 12 : 0;
+}
 // transform launchers (sfft_hidft.cu)
 int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld, int64_t shift,
                       const int32_t* map1, const int32_t* inv1, int64_t n1, double scale1, void* out1,
