@@ -375,6 +375,42 @@ def test_gathered_cluster_paths(S, torch, dt, s):
     _check_stage(torch, lib, _lib, plan, f, shift, code, tdt)
 
 
+@pytest.mark.parametrize("s", [10, 14, 16])
+def test_hidft_shifts_promoted(S, torch, s):
+    """sfft_hidft_shifts (the SAS shifted transforms, sas.py:343-345): a
+    complex128 plan over complex64 rows, nshift shifts in one launch, equals
+    per-shift transforms of the promoted rows bit for bit, on the single-CTA
+    (s = 10) and split (s = 14, 16) paths."""
+    from paper_2211_15299_b200 import _lib
+    from paper_2211_15299_b200.hidft import get_plan
+    M, B, mu, shift0 = 20, 3, 3, 5
+    N = 1 << M
+    J = np.arange(1 << s, dtype=np.int64) * 8 + 3
+    rng = np.random.default_rng(100 + s)
+    f = (rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(np.complex64)
+    Js = S.SupportSet(N, J)
+    plan = get_plan(Js, S.pivots(Js), 0, _lib.C128, torch.device("cuda", 0))
+    lib = _lib.load()
+    sp = _lib.stream_ptr(0)
+    nn = plan.n_nodes
+    d64 = torch.from_numpy(f).cuda()
+    d128 = d64.to(torch.complex128)
+    got = torch.empty((B * mu, nn), dtype=torch.complex128, device="cuda")
+    _lib.check(lib.sfft_hidft_shifts(plan.handle, d64.data_ptr(), B, N, _lib.C64, shift0, mu, _lib.OUT_NODES,
+                                     got.data_ptr(), nn, sp))
+    for j in range(mu):
+        want = torch.empty((B, nn), dtype=torch.complex128, device="cuda")
+        _lib.check(lib.sfft_hidft(plan.handle, d128.data_ptr(), B, N, shift0 + j, _lib.OUT_NODES, want.data_ptr(),
+                                  nn, None, 0, sp))
+        assert torch.equal(got[j::mu], want), j
+    # and against the oracle for one row / shift: node values x N/k = planted DFT of the shifted row
+    b, j = B - 1, mu - 1
+    fs = np.roll(f[b].astype(np.complex128), shift0 + j)
+    want_dft = O.hidft_to_dft(fs, J, M)
+    got_dft = got[b * mu + j].cpu().numpy() * (N / len(J))
+    assert rel_l2(got_dft, want_dft) < 1e-11
+
+
 # ------------------------------------------------- configs at full size ---
 
 def _synth(torch, S, cfg, B, per_signal_rows=None):
