@@ -92,7 +92,7 @@ typedef struct sfft_plan_info {
   int s;               /* pivots merged by the butterfly           */
   int level;           /* output nodes live at this tree level     */
   int homogeneous;     /* classify(J).is_homogeneous               */
-  int reserved;
+  int per_signal;      /* 1: sfft_plan_batched plan (one support per signal) */
   int64_t k;           /* |J|                                      */
   int64_t A;           /* 2^s slots = |I|                          */
   int64_t n_nodes;     /* real slots = nodes at `level`            */
@@ -107,6 +107,18 @@ typedef struct sfft_plan_info {
  * failures return SFFT_ERR_CONTRACT with the offending pivot in the message. */
 SFFT_API int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_t* r, int n_r,
                      int height, int dtype, sfft_stream_t stream, sfft_plan** plan);
+
+/* Plan for PER-SIGNAL supports (config 4): n_supports rows of k indices
+ * (int64, host or device, each a valid homogeneous SupportSet of Z_{2^M},
+ * k = 2^s).  Nothing is derived on the host: pivots, pattern, tables and
+ * twiddles of each support are built on chip by the transform (the fused
+ * kernel of sfft_hidft_to_dft_fused).  Such a plan serves sfft_hidft with
+ * SFFT_OUT_DFT, shift 0, no slot output, and B == n_supports (or
+ * n_supports == 1); invalid or non-homogeneous supports are reported by
+ * sfft_hidft as status 2 / 3 naming the support.  Every other entry point
+ * rejects it with SFFT_ERR_INVALID. */
+SFFT_API int sfft_plan_batched(const int64_t* J, int64_t k, int64_t n_supports, int M, int dtype,
+                               sfft_stream_t stream, sfft_plan** plan);
 SFFT_API int sfft_plan_destroy(sfft_plan* plan);
 SFFT_API int sfft_plan_get_info(const sfft_plan* plan, sfft_plan_info* info);
 

@@ -31,7 +31,7 @@ _I32 = _c.c_int32
 class PlanInfo(_c.Structure):
     _fields_ = [("M", _c.c_int), ("dtype", _c.c_int), ("n_r", _c.c_int), ("height", _c.c_int),
                 ("s", _c.c_int), ("level", _c.c_int), ("homogeneous", _c.c_int),
-                ("reserved", _c.c_int), ("k", _I64), ("A", _I64), ("n_nodes", _I64),
+                ("per_signal", _c.c_int), ("k", _I64), ("A", _I64), ("n_nodes", _I64),
                 ("mu_star", _I64), ("pivot_mask", _c.c_uint64), ("used", _I32 * 32)]
 
 
@@ -57,6 +57,7 @@ SIGNATURES = [
     ("sfft_sas_decode", _c.c_int, [_P, _P, _I64, _c.c_int, _I64, _I64, _c.c_double, _P, _I64, _c.c_int, _P, _P,
                                    _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     ("sfft_host_gather", _c.c_int, [_P, _I64, _I64, _c.c_int, _P, _I64, _P, _c.c_int]),
+    ("sfft_plan_batched", _c.c_int, [_P, _I64, _I64, _c.c_int, _c.c_int, _P, _P]),
     ("sfft_hidft_host", _c.c_int, [_P, _P, _I64, _I64, _I64, _c.c_int, _P, _I64, _P, _I64, _I64, _c.c_int, _P]),
     ("sfft_host_stage", _c.c_int, [_P, _P, _I64, _I64, _c.c_int, _I64, _I64, _c.c_int, _c.c_int, _P, _I64,
                                    _c.c_int, _P]),

@@ -1519,6 +1519,15 @@ static int hidft_common(const sfft_plan* plan, const void* signals, int64_t B, i
                         int64_t min_ld, int64_t shift, int out_kind, void* out, int64_t ld_out,
                         void* slot_out, int64_t ld_slot, int identity, cudaStream_t st) {
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (plan->per_signal) {  // sfft_plan_batched: supports derived on chip per signal
+    if (identity) return reject_per_signal(plan, "sfft_hidft_gathered");
+    if (out_kind != SFFT_OUT_DFT || shift != 0 || slot_out)
+      return fail(SFFT_ERR_INVALID, "a per-signal plan serves SFFT_OUT_DFT at shift 0 without slot output");
+    if (plan->n_supports != 1 && plan->n_supports != B)
+      return fail(SFFT_ERR_INVALID, "batch size must equal the plan's number of supports");
+    return fused_to_dft(plan->d_J, plan->k, plan->n_supports, plan->M, signals, B, ld, plan->dtype, out, ld_out,
+                        nullptr, st);
+  }
   if (B < 0) return fail(SFFT_ERR_INVALID, "negative batch");
   const int32_t* map = nullptr;
   const int32_t* inv = nullptr;
@@ -1576,6 +1585,7 @@ extern "C" int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const vo
                                    sfft_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (int rj = reject_per_signal(plan, "sfft_plan_apply_map")) return rj;
   const int32_t* map = nullptr;
   int64_t n_out = 0;
   double scale = 1.0;
@@ -1596,11 +1606,24 @@ extern "C" int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const vo
   return SFFT_OK;
 }
 
+namespace sfft {
+int reject_per_signal(const sfft_plan* p, const char* entry) {
+  if (p && p->per_signal)
+    return fail(SFFT_ERR_INVALID, std::string(entry) + ": a per-signal plan (sfft_plan_batched) only serves "
+                                                       "sfft_hidft with SFFT_OUT_DFT");
+  return SFFT_OK;
+}
+}  // namespace sfft
+
 extern "C" int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_supports, int M,
                                        const void* signals, int64_t B, int64_t ld, int dtype,
                                        void* out, int64_t ld_out, int32_t* status,
                                        sfft_stream_t stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return fused_to_dft(J, k, n_supports, M, signals, B, ld, dtype, out, ld_out, status, (cudaStream_t)stream);
+}
+
+int sfft::fused_to_dft(const int64_t* J, int64_t k, int64_t n_supports, int M, const void* signals, int64_t B,
+                       int64_t ld, int dtype, void* out, int64_t ld_out, int32_t* status, cudaStream_t st) {
   if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
   if (dtype != SFFT_C64 && dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown dtype");
   if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");

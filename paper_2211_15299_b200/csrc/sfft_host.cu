@@ -274,6 +274,7 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
                                int64_t chunk_rows, int nthreads, sfft_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (int rj = reject_per_signal(plan, "sfft_hidft_host")) return rj;
   if (B < 0) return fail(SFFT_ERR_INVALID, "negative batch");
   const int32_t* map = nullptr;
   int64_t n_out = 0;
@@ -368,6 +369,7 @@ extern "C" int sfft_host_stage(const sfft_plan* plan, const void* signals, int64
                                int64_t ld_out, int nthreads, sfft_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (int rj = reject_per_signal(plan, "sfft_host_stage")) return rj;
   if (B < 0 || nshift < 1) return fail(SFFT_ERR_INVALID, "negative batch or nshift < 1");
   if (in_dtype != SFFT_C64 && in_dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown input dtype");
   if (out_dtype != SFFT_C64 && out_dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown output dtype");

@@ -511,6 +511,7 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_tw_blk);
   cudaFree(p->d_inv_elem_blk);
   cudaFree(p->d_inv_node_blk);
+  cudaFree(p->d_J);
   delete p;
 }
 
@@ -648,6 +649,43 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   return SFFT_OK;
 }
 
+extern "C" int sfft_plan_batched(const int64_t* J, int64_t k, int64_t n_supports, int M, int dtype,
+                                 sfft_stream_t stream, sfft_plan** out_plan) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!out_plan) return fail(SFFT_ERR_INVALID, "null plan output");
+  *out_plan = nullptr;
+  if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
+  if (dtype != SFFT_C64 && dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown dtype");
+  if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
+  if (n_supports < 1) return fail(SFFT_ERR_INVALID, "n_supports must be >= 1");
+  if (!J) return fail(SFFT_ERR_INVALID, "null support pointer");
+  if (k & (k - 1)) return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a homogeneous support");
+  sfft_plan* p = new sfft_plan();
+  std::memset(p, 0, sizeof(*p));
+  SFFT_CUDA(cudaGetDevice(&p->device));
+  p->per_signal = 1;
+  p->n_supports = n_supports;
+  p->M = M;
+  p->dtype = dtype;
+  p->k = k;
+  p->A = k;
+  p->s = 63 - __builtin_clzll((unsigned long long)k);
+  p->n_r = p->s;
+  p->n_nodes = k;
+  p->mu_star = 1;
+  p->homogeneous = 1;
+  const size_t bytes = sizeof(int64_t) * (size_t)k * (size_t)n_supports;
+  cudaError_t e = cudaMalloc((void**)&p->d_J, bytes);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_J, J, bytes, cudaMemcpyDefault, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    plan_free(p);
+    return cuda_fail(e, "per-signal plan");
+  }
+  *out_plan = p;
+  return SFFT_OK;
+}
+
 extern "C" int sfft_plan_destroy(sfft_plan* plan) {
   plan_free(plan);
   return SFFT_OK;
@@ -668,6 +706,7 @@ extern "C" int sfft_plan_get_info(const sfft_plan* p, sfft_plan_info* info) {
   info->n_nodes = p->n_nodes;
   info->mu_star = p->mu_star;
   info->pivot_mask = p->pivot_mask;
+  info->per_signal = p->per_signal;
   for (int i = 0; i < 32; ++i) info->used[i] = i < p->s ? p->used[i] : 0;
   return SFFT_OK;
 }
@@ -682,6 +721,7 @@ extern "C" int sfft_plan_tables(const sfft_plan* p, int64_t* element_slots, int6
                                 sfft_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!p) return fail(SFFT_ERR_INVALID, "null plan");
+  if (int rj = reject_per_signal(p, "sfft_plan_tables")) return rj;
   int rc;
   DevBuf w, du;
   const int64_t big = std::max(std::max(p->k, p->A), p->n_nodes);

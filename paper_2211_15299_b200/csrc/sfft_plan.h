@@ -27,6 +27,10 @@ struct sfft_plan {
   void* d_tw_blk;            // 2^lc x (2^(s-lc) - 1) twiddles of the local stages, per block, stage-major
   int32_t* d_inv_elem_blk;   // A   d_inv_elem, block-major: [t][l] = inv_elem[(l << lc) | brev_lc(t)]
   int32_t* d_inv_node_blk;   // A   d_inv_node, block-major
+  // per-signal supports (sfft_plan_batched): tables derived on chip per signal
+  int per_signal;
+  int64_t n_supports;
+  int64_t* d_J;              // n_supports x k
 };
 
 namespace sfft {
@@ -46,6 +50,11 @@ int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld
                       int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st,
                       int64_t nshift = 1, int in_c64 = 0);
 int max_supported_s(int dtype);
+// per-signal plans only serve sfft_hidft(SFFT_OUT_DFT)
+int reject_per_signal(const sfft_plan* p, const char* entry);
+// hidft_to_dft for per-signal supports (sfft_hidft_to_dft_fused's body)
+int fused_to_dft(const int64_t* J, int64_t k, int64_t n_supports, int M, const void* signals, int64_t B,
+                 int64_t ld, int dtype, void* out, int64_t ld_out, int32_t* status, cudaStream_t st);
 // pre-gathered rows (identity loads): slot order, or sorted order when
 // gathered_sorted(plan) (the cluster transform, 2^s beyond one CTA)
 bool gathered_sorted(const sfft_plan* p);

@@ -587,6 +587,7 @@ static std::mutex g_nodes_mu;
 extern "C" int sfft_plan_nodes(sfft_plan* p, int32_t* off_out, int32_t* mem_out, sfft_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!p) return fail(SFFT_ERR_INVALID, "null plan");
+  if (int rj = reject_per_signal(p, "sfft_plan_nodes")) return rj;
   std::lock_guard<std::mutex> lk(g_nodes_mu);  // the table is built once, lazily
   if (!p->d_node_off) {
     int32_t *cnt = nullptr, *cand = nullptr;
@@ -622,6 +623,7 @@ extern "C" int sfft_hidft_shifts(const sfft_plan* plan, const void* signals, int
                                  int64_t shift0, int64_t nshift, int out_kind, void* out, int64_t ld_out,
                                  sfft_stream_t stream) {
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
+  if (int rj = reject_per_signal(plan, "sfft_hidft_shifts")) return rj;
   if (nshift < 1) return fail(SFFT_ERR_INVALID, "nshift must be >= 1");
   if (in_dtype != plan->dtype && !(in_dtype == SFFT_C64 && plan->dtype == SFFT_C128))
     return fail(SFFT_ERR_INVALID, "complex128 signals need a complex128 plan");
@@ -648,6 +650,7 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
                                int64_t* n_fallback, sfft_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!p) return fail(SFFT_ERR_INVALID, "null plan");
+  if (int rj = reject_per_signal(p, "sfft_sas_decode")) return rj;
   if (p->height != 0) return fail(SFFT_ERR_CONTRACT, "sas decode needs height 0");
   if (mu != p->mu_star) return fail(SFFT_ERR_INVALID, "mu must equal the plan's mu*");
   if (mu > kMaxMu) return fail(SFFT_ERR_UNSUPPORTED, "node weight above " + std::to_string(kMaxMu));

@@ -411,6 +411,59 @@ def test_hidft_shifts_promoted(S, torch, s):
     assert rel_l2(got_dft, want_dft) < 1e-11
 
 
+def test_plan_batched_capi(S, torch):
+    """sfft_plan_batched (per-signal supports, config 4 shape) + sfft_hidft
+    equals sfft_hidft_to_dft_fused bit for bit; the plan is rejected by every
+    other entry point and bad supports come back as status 2 / 3."""
+    import ctypes
+    from paper_2211_15299_b200 import _lib, workloads as W
+    wl = W.make_workload(4, 8)
+    B, k, M = wl.B, wl.k, wl.M
+    N = 1 << M
+    sig = torch.empty((B, N), dtype=torch.complex64, device="cuda")
+    W.synthesize_into(sig, wl.support, wl.coeffs)
+    lib = _lib.load()
+    sp = _lib.stream_ptr(0)
+    Jh = np.ascontiguousarray(wl.support, dtype=np.int64)
+    plan = ctypes.c_void_p()
+    _lib.check(lib.sfft_plan_batched(Jh.ctypes.data, k, B, M, _lib.C64, sp, ctypes.byref(plan)))
+    try:
+        info = _lib.PlanInfo()
+        _lib.check(lib.sfft_plan_get_info(plan, ctypes.byref(info)))
+        assert info.per_signal == 1 and info.k == k and info.A == k
+        got = torch.empty((B, k), dtype=torch.complex64, device="cuda")
+        _lib.check(lib.sfft_hidft(plan, sig.data_ptr(), B, N, 0, _lib.OUT_DFT, got.data_ptr(), k, None, 0, sp))
+        want = torch.empty_like(got)
+        Jd = torch.from_numpy(Jh).cuda()
+        _lib.check(lib.sfft_hidft_to_dft_fused(Jd.data_ptr(), k, B, M, sig.data_ptr(), B, N, _lib.C64,
+                                               want.data_ptr(), k, None, sp))
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
+        for b in (0, B - 1):
+            assert rel_l2(got[b].cpu().numpy(), wl.coeffs[b]) < 1e-5
+        # wrong kinds / sizes / entry points
+        assert lib.sfft_hidft(plan, sig.data_ptr(), B, N, 0, _lib.OUT_NODES, got.data_ptr(), k, None, 0, sp) == 2
+        assert lib.sfft_hidft(plan, sig.data_ptr(), B - 1, N, 0, _lib.OUT_DFT, got.data_ptr(), k, None, 0, sp) == 2
+        assert lib.sfft_hidft_gathered(plan, sig.data_ptr(), B, N, _lib.OUT_DFT, got.data_ptr(), k, None, 0, sp) == 2
+        assert lib.sfft_plan_tables(plan, None, None, None, None, None, None, sp) == 2
+        assert lib.sfft_plan_nodes(plan, None, None, sp) == 2
+    finally:
+        lib.sfft_plan_destroy(plan)
+    # a non-homogeneous row: contract status naming the support
+    bad = Jh.copy()
+    bad[3, 0] = (bad[3, 0] + 1) % N
+    bad[3].sort()
+    if len(np.unique(bad[3])) == k:
+        p2 = ctypes.c_void_p()
+        _lib.check(lib.sfft_plan_batched(bad.ctypes.data, k, B, M, _lib.C64, sp, ctypes.byref(p2)))
+        try:
+            out = torch.empty((B, k), dtype=torch.complex64, device="cuda")
+            rc = lib.sfft_hidft(p2, sig.data_ptr(), B, N, 0, _lib.OUT_DFT, out.data_ptr(), k, None, 0, sp)
+            assert rc in (2, 3) and b"support 3" in lib.sfft_last_error()
+        finally:
+            lib.sfft_plan_destroy(p2)
+
+
 # ------------------------------------------------- configs at full size ---
 
 def _synth(torch, S, cfg, B, per_signal_rows=None):
