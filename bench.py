@@ -152,8 +152,17 @@ def run_b200(args) -> None:
 
     cfg = args.config
     spec = W.CONFIGS[cfg]
-    B = args.batch or spec["B"]
-    wl = W.make_workload(cfg, B, b0=rank * B)
+    if args.scaling == "strong":  # fixed total batch, sharded over the ranks
+        from paper_2211_15299_b200.dist import shard_range
+        B_total = args.batch or spec["B"]
+        b0, b1 = shard_range(B_total, rank, world)
+        B = b1 - b0
+        if B < 1:
+            raise SystemExit(f"strong scaling: {B_total} signals cannot feed {world} ranks")
+    else:  # fixed batch per rank
+        B = args.batch or spec["B"]
+        b0, B_total = rank * B, B * world
+    wl = W.make_workload(cfg, B, b0=b0)
     cdt = torch.complex64 if wl.dtype == "complex64" else torch.complex128
     esz = 8 if cdt == torch.complex64 else 16
     N = wl.N
@@ -173,7 +182,7 @@ def run_b200(args) -> None:
     else:
         ub_sum = 0
         for b in range(B):
-            pat = W.pattern_of(W.config_pivots(cfg, rank * B + b), wl.M)
+            pat = W.pattern_of(W.config_pivots(cfg, b0 + b), wl.M)
             gb, ub = gather_bytes(pat, esz)
             per_sig_sector.append(gb)
             ub_sum += ub
@@ -250,7 +259,7 @@ def run_b200(args) -> None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     ms_per_step = ms / args.steps
-    coeffs_per_step = B * wl.k * world
+    coeffs_per_step = B_total * wl.k
     value = coeffs_per_step / (ms_per_step / 1e3)
 
     # roofline of the one kernel a step launches
@@ -305,12 +314,14 @@ def run_b200(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (f32)" if esz == 8 else "c128 (f64)",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "c64 (f32)" if esz == 8 else "c128 (f64)",
             "data": "synthetic: seeded supports (reference generators) and complex-Gaussian spectra, "
                     "signals = inverse DFT synthesised on device",
-            "config": {"workload": f"config {cfg}: N=2^{wl.M}, k={wl.k}, B={B} per GPU, {wl.dtype}, "
+            "config": {"workload": f"config {cfg}: N=2^{wl.M}, k={wl.k}, "
+                                   + (f"B={B_total} total" if args.scaling == "strong" else f"B={B} per GPU")
+                                   + f", {wl.dtype}, "
                                    + ("shared support" if wl.support.ndim == 1 else "per-signal supports"),
-                       "global_batch": B * world, "N": N, "k": wl.k, "parallelism": f"batch shard x{world}",
+                       "global_batch": B_total, "N": N, "k": wl.k, "parallelism": f"batch shard x{world}",
                        "l2": f"rotating {R} input sets, gather footprint {R * footprint / 2**20:.0f} MiB "
                              f"vs 126 MB L2"},
             "gpu_launches": args.steps,
@@ -485,7 +496,7 @@ def run_reference(args) -> None:
     B = spec["B"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": B * k / value * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "c64 input, f64 compute (reference upcasts)" if spec["dtype"] == "complex64" else "c128 (f64)",
             "data": "synthetic, same seeds as the b200 arm",
             "config": {"workload": f"config {cfg}: N=2^{spec['M']}, k={k}, B={B}", "global_batch": B,
@@ -501,7 +512,10 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6])
-    ap.add_argument("--batch", type=int, default=0, help="signals per GPU (default: config's B)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="signals per GPU (weak) or in total (strong); default: the config's B")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: the config's B per GPU (default); strong: the config's B split over the GPUs")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--max-sets", type=int, default=8)
     ap.add_argument("--soak", type=float, default=1.0)
