@@ -205,6 +205,17 @@ def run_b200(args) -> None:
     out = torch.empty((B, wl.k), dtype=cdt, device=dev)
     status = torch.zeros(wl.support.shape[0] if wl.support.ndim == 2 else 1, dtype=torch.int32, device=dev)
 
+    # kernels one step launches (2 per row chunk for the split transform of large A)
+    launches_per_step = 1
+    if wl.support.ndim == 1:
+        import ctypes
+        from paper_2211_15299_b200 import _lib
+        from paper_2211_15299_b200.hidft import get_plan
+        lp = get_plan(J, S.pivots(J), 0, _lib.C64 if cdt == torch.complex64 else _lib.C128, dev)
+        n_l = ctypes.c_int64(0)
+        _lib.check(_lib.load().sfft_launch_count(lp.handle, B, ctypes.byref(n_l)))
+        launches_per_step = int(n_l.value)
+
     if cfg == 3:  # sas_transform(f, J, r=pivots(J)): the mu*=1 read, x N/|I|
         r_sas = S.pivots(J)
 
@@ -262,7 +273,8 @@ def run_b200(args) -> None:
     coeffs_per_step = B_total * wl.k
     value = coeffs_per_step / (ms_per_step / 1e3)
 
-    # roofline of the one kernel a step launches
+    # roofline of the step: one kernel (configs 1-4), or the split transform's
+    # front + back pair (config 5), whose bytes are counted once per step
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
@@ -271,6 +283,7 @@ def run_b200(args) -> None:
     achieved = G / (ms_per_step / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
+            "kernels_per_step": launches_per_step,
             "algorithmic_bytes_per_launch": int(G),
             "element_bytes_per_launch": int(B * (pattern_bytes[1] if pattern_bytes else 0) + B * wl.k * esz)}
     # the same kernel against HBM bytes at the measured 128 B access granularity
@@ -324,7 +337,7 @@ def run_b200(args) -> None:
                        "global_batch": B_total, "N": N, "k": wl.k, "parallelism": f"batch shard x{world}",
                        "l2": f"rotating {R} input sets, gather footprint {R * footprint / 2**20:.0f} MiB "
                              f"vs 126 MB L2"},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * launches_per_step,
             "roofline": roof,
             "clocks": clocks,
             "parity": {"rel_l2_vs_planted_max": err, "tol": tol},

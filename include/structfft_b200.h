@@ -140,6 +140,11 @@ SFFT_API int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B, i
                int64_t shift, int out_kind, void* out, int64_t ld_out, void* slot_out,
                int64_t ld_slot, sfft_stream_t stream);
 
+/* Number of kernel launches sfft_hidft / sfft_hidft_gathered issue on the
+ * stream for `rows` rows with this plan (1, or 2 per row chunk of the split
+ * transform for 2^s beyond one CTA). */
+SFFT_API int sfft_launch_count(const sfft_plan* plan, int64_t rows, int64_t* launches);
+
 /* Same transform on samples already gathered in slot order (B rows of A
  * complex, row stride ld >= A): the path for callable / synthesised sources
  * (hidft.py:41-45, where the caller evaluates the signal at the offsets). */

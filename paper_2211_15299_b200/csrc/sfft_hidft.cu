@@ -1284,6 +1284,41 @@ static int scratch_pool(int dev, cudaMemPool_t* pool) {
   return SFFT_OK;
 }
 
+// rows per chunk of the two-kernel split: scratch up to SFFT_SPLIT_SCRATCH_MB
+// (default 128 MiB, measured best for config 5, tools/cfg5_sweep.sh), rounded
+// to a multiple of the back pass's rows per wave so its persistent CTAs all
+// get the same number of rows
+static int64_t split_chunk_rows(int64_t rows, size_t row_bytes, int occ, int ex) {
+  static const int64_t scr_mb = [] {
+    const char* e = getenv("SFFT_SPLIT_SCRATCH_MB");
+    return (int64_t)(e ? std::max(1, atoi(e)) : 128);
+  }();
+  const int64_t per_wave = std::max<int64_t>(1, (int64_t)num_sms() * occ / ex);
+  int64_t chunk = std::max<int64_t>(1, (scr_mb << 20) / (int64_t)row_bytes);
+  return std::max<int64_t>(1, std::min<int64_t>(rows, (chunk + per_wave - 1) / per_wave * per_wave));
+}
+
+static bool split_fused_selected() {
+  static const bool fused = [] { const char* e = getenv("SFFT_SPLIT"); return e && std::string(e) == "fused"; }();
+  return fused;
+}
+
+// kernel launches run_split issues for `rows` rows (sfft_launch_count)
+template <typename T, int S, int LC>
+static int split_launches(int64_t rows, int64_t* n) {
+  using SG = SplitGeo<T, S, LC>;
+  if (split_fused_selected()) {
+    *n = rows > 0 ? 1 : 0;
+    return SFFT_OK;
+  }
+  int occ = 0;
+  int rc = kernel_occupancy(k_split_back<T, S, LC>, SG::G::NT, SG::SMEM, &occ);
+  if (rc) return rc;
+  const int64_t chunk = split_chunk_rows(rows, sizeof(Cx<T>) << S, occ, SG::EX);
+  *n = rows > 0 ? 2 * ((rows + chunk - 1) / chunk) : 0;
+  return SFFT_OK;
+}
+
 template <typename T, int S, int LC>
 static int run_split(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
   using SG = SplitGeo<T, S, LC>;
@@ -1295,8 +1330,7 @@ static int run_split(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1,
   if (inv1 && !inv_blk) return fail(SFFT_ERR_INVALID, "no block-major map for this output");
   // the fused persistent pipeline measured slower than two launches on config 5
   // (200 vs 185 us, tools/split_time.py); kept selectable for study
-  static const bool fused = [] { const char* e = getenv("SFFT_SPLIT"); return e && std::string(e) == "fused"; }();
-  if (fused) {
+  if (split_fused_selected()) {
     if (sizeof(T) == 8 && a.in_c64) return run_split_fused<T, S, LC, float>(p, a, inv_blk, st);
     return run_split_fused<T, S, LC, T>(p, a, inv_blk, st);
   }
@@ -1310,11 +1344,7 @@ static int run_split(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1,
   const int64_t rows = a.B * a.nshift;
   if (rows == 0) return SFFT_OK;
   const size_t row_bytes = sizeof(Cx<T>) << S;
-  static const int64_t scr_mb = [] {
-    const char* e = getenv("SFFT_SPLIT_SCRATCH_MB");
-    return (int64_t)(e ? std::max(1, atoi(e)) : 128);  // measured best for config 5 (tools/cfg5_sweep.sh)
-  }();
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(rows, (scr_mb << 20) / (int64_t)row_bytes));
+  const int64_t chunk = split_chunk_rows(rows, row_bytes, occ, SG::EX);
   int dev = 0;
   SFFT_CUDA(cudaGetDevice(&dev));
   cudaMemPool_t pool;
@@ -1545,6 +1575,29 @@ static int hidft_common(const sfft_plan* plan, const void* signals, int64_t B, i
   if (dev != plan->device) return fail(SFFT_ERR_INVALID, "plan belongs to another device");
   return launch_hidft_plan(plan, signals, B, ld, shift, map, inv, n_out, scale, out, ld_out, slot_out,
                            ld_slot, identity, st);
+}
+
+extern "C" int sfft_launch_count(const sfft_plan* plan, int64_t rows, int64_t* launches) {
+  if (!plan || !launches) return fail(SFFT_ERR_INVALID, "null plan or output");
+  if (rows < 0) return fail(SFFT_ERR_INVALID, "negative batch");
+  *launches = rows > 0 ? 1 : 0;
+  if (plan->per_signal || !plan->split_lc || use_cluster_path() || rows == 0) return SFFT_OK;
+  if (plan->dtype == SFFT_C64) {
+    switch (plan->s) {
+      case 15: return split_launches<float, 15, 3>(rows, launches);
+      case 16: return split_launches<float, 16, 4>(rows, launches);
+      case 17: return split_launches<float, 17, 4>(rows, launches);
+      default: break;
+    }
+  } else {
+    switch (plan->s) {
+      case 14: return split_launches<double, 14, 2>(rows, launches);
+      case 15: return split_launches<double, 15, 3>(rows, launches);
+      case 16: return split_launches<double, 16, 4>(rows, launches);
+      default: break;
+    }
+  }
+  return SFFT_OK;
 }
 
 extern "C" int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld,
