@@ -375,8 +375,8 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
     invalid support raises like the reference would."""
     torch = _torch()
     dev = _lib.require_device()
-    if not torch.is_tensor(signals):
-        signals = torch.from_numpy(np.ascontiguousarray(np.asarray(signals))).to(dev)
+    if not torch.is_tensor(signals):  # numpy rows stay on the host: only the needed samples move
+        signals = torch.from_numpy(np.ascontiguousarray(np.asarray(signals)))
     single = signals.dim() == 1
     sig = signals.unsqueeze(0) if single else signals
     if sig.dtype not in (torch.complex64, torch.complex128):

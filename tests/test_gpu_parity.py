@@ -464,6 +464,59 @@ def test_plan_batched_capi(S, torch):
             lib.sfft_plan_destroy(p2)
 
 
+def test_edge_batches_strides_shifts(S, torch):
+    """Empty batch, padded rows (ld > N), numpy input, and shifts outside
+    [0, N) (taken mod N, as the reference's (I - a) mod N does)."""
+    from paper_2211_15299_b200 import _lib
+    from paper_2211_15299_b200.hidft import get_plan
+    J, M = O.config_support(2)
+    N = 1 << M
+    Js = S.SupportSet(N, J)
+    empty = torch.empty((0, N), dtype=torch.complex64, device="cuda")
+    assert S.hidft_to_dft_batched(empty, Js).shape == (0, len(J))
+    coef = np.stack([O.config_coefficients(2, b, len(J)) for b in range(3)])
+    f = np.stack([O.synthesize(J, coef[b], M) for b in range(3)]).astype(np.complex64)
+    wide = torch.zeros((3, N + 64), dtype=torch.complex64, device="cuda")
+    wide[:, :N] = torch.from_numpy(f).cuda()
+    got = S.hidft_to_dft_batched(wide[:, :N], Js)           # row stride N + 64, no copy
+    want = S.hidft_to_dft_batched(torch.from_numpy(f).cuda(), Js)
+    assert torch.equal(got, want)
+    assert torch.equal(torch.as_tensor(S.hidft_to_dft_batched(f, Js)), want.cpu())  # numpy rows
+    plan = get_plan(Js, S.pivots(Js), 0, _lib.C64, torch.device("cuda", 0))
+    lib, sp = _lib.load(), _lib.stream_ptr(0)
+    d = torch.from_numpy(f).cuda()
+    outs = []
+    for shift in (5, 5 - N, 5 + 3 * N, -(1 << 40) + 5 + (1 << 40) // N * N):
+        o = torch.empty((3, plan.n_nodes), dtype=torch.complex64, device="cuda")
+        _lib.check(lib.sfft_hidft(plan.handle, d.data_ptr(), 3, N, shift, _lib.OUT_NODES, o.data_ptr(),
+                                  plan.n_nodes, None, 0, sp))
+        outs.append(o)
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_largest_modulus(S, torch):
+    """N = 2^31 (the device path's int32 index limit): one complex64 row of
+    16 GiB, samples planted at the pattern offsets, planted spectrum back."""
+    free = torch.cuda.mem_get_info()[0]
+    if free < 20 * 2**30:
+        pytest.skip("needs 20 GiB of free device memory")
+    M, N = 31, 1 << 31
+    J = O.gen_homogeneous((0, 5, 17, 30), M, 7)
+    Js = S.SupportSet(N, J)
+    rng = np.random.default_rng(31)
+    c = rng.standard_normal(len(J)) + 1j * rng.standard_normal(len(J))
+    pat = S.pivoted_pattern(S.pivots(Js), M).as_array()
+    n = pat.astype(np.int64)
+    vals = (np.exp(2j * np.pi * ((n[:, None] * J[None, :]) % N) / N) @ c) / N   # f at the samples
+    sig = torch.zeros((1, N), dtype=torch.complex64, device="cuda")
+    sig[0, torch.from_numpy(n).cuda()] = torch.from_numpy(vals.astype(np.complex64)).cuda()
+    got = S.hidft_to_dft_batched(sig, Js)[0].cpu().numpy()
+    assert rel_l2(got, c) < 1e-5
+    del sig
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------- configs at full size ---
 
 def _synth(torch, S, cfg, B, per_signal_rows=None):
