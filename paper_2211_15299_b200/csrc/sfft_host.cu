@@ -315,10 +315,33 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
   char* slot_tgt = slot_out ? (slot_pinned ? (char*)slot_out : (char*)S.h_out + (out_pinned ? 0 : out_bytes)) : nullptr;
   const int64_t lds_tgt = slot_pinned ? ld_slot : A;
 
+  // Optionally (SFFT_HOST_GPU_FRACTION) the device reads the first g0
+  // page-locked rows itself, zero-copy over PCIe, while the host threads
+  // gather the rest.  Measured on config 2 (tools/e2e_probe.py): 0.1 / 0.2 /
+  // 0.3 of the rows -> 1.31 / 1.52 / 1.87 ms against 1.1 ms host-only (the
+  // per-sample PCIe reads are slow and compete for host memory), so 0.
+  static const double gpu_frac = [] {
+    const char* e = getenv("SFFT_HOST_GPU_FRACTION");
+    return e ? std::min(1.0, std::max(0.0, atof(e))) : 0.0;
+  }();
+  const int64_t g0 = is_pinned_host(signals) ? (int64_t)(gpu_frac * (double)B) : 0;
+  if (g0 > 0) {
+    rc = sfft_hidft(plan, signals, g0, ld, shift, out_kind, S.d_out, n_out, slot_out ? S.d_slot : nullptr, A,
+                    stream);
+    cudaError_t e = rc ? cudaSuccess
+                       : cudaMemcpy2DAsync(out_tgt, (size_t)ldo_tgt * esz, S.d_out, (size_t)n_out * esz,
+                                           (size_t)n_out * esz, g0, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && !rc && slot_out)
+      e = cudaMemcpy2DAsync(slot_tgt, (size_t)lds_tgt * esz, S.d_slot, (size_t)A * esz, (size_t)A * esz, g0,
+                            cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "device->host copy");
+    if (rc) return rc;
+  }
+
   RowJob job;
-  job.sig = (const char*)signals;
+  job.sig = (const char*)signals + (size_t)g0 * ld * esz;
   job.ld_bytes = ld * esz;
-  job.B = B;
+  job.B = B - g0;
   job.A = A;
   job.in_esz = job.out_esz = esz;
   job.loc = loc.data();
@@ -327,14 +350,15 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
 
   HostPool& p = pool(nthreads);
   const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
-  p.start(&fn);
-  for (int64_t c = 0; c < job.nchunks() && rc == SFFT_OK; ++c) {
+  if (job.B > 0) p.start(&fn);
+  for (int64_t c = 0; c < job.nchunks() && job.B > 0 && rc == SFFT_OK; ++c) {
     job.await(c);
-    const int64_t b0 = c * job.chunk, rows = job.chunk_rows(c);
-    const size_t ib = (size_t)b0 * A * esz;
+    const int64_t rows = job.chunk_rows(c);
+    const int64_t hb = c * job.chunk, b0 = g0 + hb;  // row in the staging / in the batch
+    const size_t ib = (size_t)hb * A * esz;
     char* din = (char*)S.d_in + ib;
     char* dout = (char*)S.d_out + (size_t)b0 * n_out * esz;
-    char* dslot = slot_out ? (char*)S.d_slot + ib : nullptr;
+    char* dslot = slot_out ? (char*)S.d_slot + (size_t)b0 * A * esz : nullptr;
     cudaError_t e = cudaMemcpyAsync(din, (char*)S.h_in + ib, (size_t)rows * A * esz, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) { rc = cuda_fail(e, "host->device chunk copy"); break; }
     rc = hidft_gathered(plan, din, rows, A, sorted, out_kind, dout, n_out, dslot, A, st);
@@ -346,8 +370,10 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
                             (size_t)A * esz, rows, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) rc = cuda_fail(e, "device->host chunk copy");
   }
-  while (job.step()) {}  // on error: drain so no worker still reads the caller's rows
-  p.wait();
+  if (job.B > 0) {
+    while (job.step()) {}  // on error: drain so no worker still reads the caller's rows
+    p.wait();
+  }
   cudaEventRecord(S.h_free, st);
   const cudaError_t es = cudaStreamSynchronize(st);
   if (rc) return rc;
