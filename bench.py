@@ -236,6 +236,28 @@ def run_b200(args) -> None:
     if not (err < tol) or worst != 0:
         raise SystemExit(f"bench parity gate failed: rel L2 {err:.3e} status {worst}")
 
+    # CUDA graphs: one graph per rotation set, captured from the same step
+    # call, so a timed step is the step's kernels without host launch gaps
+    # (config 1 is launch-bound); --no-graph times the eager calls
+    run = step
+    if not args.no_graph:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for i in range(R):
+                step(i)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        graphs = []
+        for i in range(R):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(i)
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+        def run(i):
+            graphs[i % R].replay()
+
     vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
     sampler = ClockSampler(vis[local] if local < len(vis) else local)
     sampler.start()
@@ -244,11 +266,11 @@ def run_b200(args) -> None:
     i = 0
     while time.time() < t_end:
         for _ in range(64):
-            step(i)
+            run(i)
             i += 1
         torch.cuda.synchronize()
     for w in range(args.warmup):
-        step(w)
+        run(w)
     stream = torch.cuda.current_stream(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -257,7 +279,7 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
     ev0.record(stream)
     for t in range(args.steps):
-        step(t)
+        run(t)
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -335,6 +357,7 @@ def run_b200(args) -> None:
                                    + f", {wl.dtype}, "
                                    + ("shared support" if wl.support.ndim == 1 else "per-signal supports"),
                        "global_batch": B_total, "N": N, "k": wl.k, "parallelism": f"batch shard x{world}",
+                       "launch": "eager calls" if args.no_graph else "CUDA graph replay of the step call",
                        "l2": f"rotating {R} input sets, gather footprint {R * footprint / 2**20:.0f} MiB "
                              f"vs 126 MB L2"},
             "gpu_launches": args.steps * launches_per_step,
@@ -527,6 +550,7 @@ def main() -> None:
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6])
     ap.add_argument("--batch", type=int, default=0,
                     help="signals per GPU (weak) or in total (strong); default: the config's B")
+    ap.add_argument("--no-graph", action="store_true", help="time eager calls instead of CUDA-graph replays")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="weak: the config's B per GPU (default); strong: the config's B split over the GPUs")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
