@@ -94,6 +94,9 @@ static HostPool& pool(int want) {  // caller holds g_host_mu
   return *g_pool;
 }
 
+// below this many samples a job runs on the calling thread alone
+constexpr int64_t kPoolMinSamples = 1 << 13;
+
 struct C64b { uint64_t v; };
 struct C128b { uint64_t lo, hi; };
 
@@ -348,9 +351,11 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
   job.out = (char*)S.h_in;
   job.set_chunking(chunk_rows);
 
+  // small jobs: the calling thread alone (waking the pool costs more)
+  const bool use_pool = job.B > 0 && job.B * A >= kPoolMinSamples;
   HostPool& p = pool(nthreads);
   const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
-  if (job.B > 0) p.start(&fn);
+  if (use_pool) p.start(&fn);
   for (int64_t c = 0; c < job.nchunks() && job.B > 0 && rc == SFFT_OK; ++c) {
     job.await(c);
     const int64_t rows = job.chunk_rows(c);
@@ -370,7 +375,7 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
                             (size_t)A * esz, rows, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) rc = cuda_fail(e, "device->host chunk copy");
   }
-  if (job.B > 0) {
+  if (use_pool) {
     while (job.step()) {}  // on error: drain so no worker still reads the caller's rows
     p.wait();
   }
@@ -432,9 +437,10 @@ extern "C" int sfft_host_stage(const sfft_plan* plan, const void* signals, int64
   job.out = (char*)S.h_in;
   job.set_chunking(0);
 
+  const bool use_pool = B * rowlen >= kPoolMinSamples;
   HostPool& p = pool(nthreads);
   const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
-  p.start(&fn);
+  if (use_pool) p.start(&fn);
   for (int64_t c = 0; c < job.nchunks() && rc == SFFT_OK; ++c) {
     job.await(c);
     const int64_t r0 = c * job.chunk * nshift, rows = job.chunk_rows(c) * nshift;  // output rows
@@ -443,8 +449,10 @@ extern "C" int sfft_host_stage(const sfft_plan* plan, const void* signals, int64
                                             (size_t)A * oesz, rows, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) rc = cuda_fail(e, "host->device staging copy");
   }
-  while (job.step()) {}
-  p.wait();
+  if (use_pool) {
+    while (job.step()) {}
+    p.wait();
+  }
   cudaEventRecord(S.h_free, st);
   return rc;
 }
