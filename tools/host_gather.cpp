@@ -27,10 +27,12 @@ int main(int argc, char** argv) {
 #pragma omp parallel for
   for (int64_t i = 0; i < N * B; ++i) sig[i] = i;
   uint64_t* out = (uint64_t*)aligned_alloc(4096, sizeof(uint64_t) * B * A);
-  const int thr_list[] = {4, 8, 10, 12, 16};
-  const int dist_list[] = {0, 8, 16, 32, 64};
+  const int thr_list[] = {16};
+  const int dist_list[] = {0, 4, 8, 16, 32};
   for (int nt : thr_list) {
+   for (int hint = 0; hint < 4; ++hint) {
     for (int D : dist_list) {
+      if (D == 0 && hint) continue;
       double best = 1e9;
       for (int rep = 0; rep < 5; ++rep) {
         auto t0 = std::chrono::steady_clock::now();
@@ -44,7 +46,13 @@ int main(int argc, char** argv) {
           } else {
             for (int64_t i = i0; i < i1; ++i) {
               const int64_t j = i + D;
-              if (j < i1) __builtin_prefetch(sig + (j / A) * N + off[j % A], 0, 0);
+              if (j < i1) {
+                const uint64_t* q = sig + (j / A) * N + off[j % A];
+                if (hint == 0) __builtin_prefetch(q, 0, 0);
+                else if (hint == 1) __builtin_prefetch(q, 0, 1);
+                else if (hint == 2) __builtin_prefetch(q, 0, 2);
+                else __builtin_prefetch(q, 0, 3);
+              }
               out[i] = sig[(i / A) * N + off[i % A]];
             }
           }
@@ -52,8 +60,9 @@ int main(int argc, char** argv) {
         auto t1 = std::chrono::steady_clock::now();
         best = std::min(best, std::chrono::duration<double, std::milli>(t1 - t0).count());
       }
-      printf("threads %2d prefetch %2d: %.3f ms\n", nt, D, best);
+      printf("threads %2d prefetch locality-hint %d distance %2d: %.3f ms\n", nt, hint, D, best);
     }
+   }
   }
   return (int)(out[12345] & 1);
 }
