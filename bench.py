@@ -418,10 +418,13 @@ def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
     del host
     return {"value": B * wl.k / dt, "unit": UNIT, "h2d_bytes_per_step": int(B * A * esz + support_bytes),
             "d2h_bytes_per_step": int(np.asarray(res).size * esz), "seconds_per_step": dt,
-            "path": "public API on a page-locked host tensor -> sfft_hidft_host: native host threads gather "
-                    "the 2^s needed samples per signal into pinned staging while earlier row chunks are "
-                    "copied to the device, transformed and copied back (one stream); per-signal supports "
-                    "(config 4) read the rows zero-copy"}
+            "path": ("public API on page-locked host rows and supports -> sfft_hidft_to_dft_fused_host: host "
+                     "threads derive each support's pivots and gather its 2^s samples while earlier row chunks "
+                     "(samples + supports) are copied, transformed with on-chip plans and copied back"
+                     if wl.support.ndim == 2 else
+                     "public API on a page-locked host tensor -> sfft_hidft_host: native host threads gather "
+                     "the 2^s needed samples per signal into pinned staging while earlier row chunks are "
+                     "copied to the device, transformed and copied back (one stream)")}
 
 
 # ------------------------------------------------------- CPU reference ---

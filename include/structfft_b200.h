@@ -250,6 +250,16 @@ SFFT_API int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_supp
                             void* out, int64_t ld_out, int32_t* status,
                             sfft_stream_t stream);
 
+/* sfft_hidft_to_dft_fused for per-signal supports (n_supports = B) with
+ * signals, supports and results all in HOST memory: host threads derive each
+ * support's pivots, gather its 2^s samples and stage the support, pipelined
+ * with the copies; the device rebuilds each plan on chip from the support
+ * and transforms the staged samples.  Synchronous; returns the worst support
+ * status like the fused call with status = NULL.  k <= 2^13. */
+SFFT_API int sfft_hidft_to_dft_fused_host(const int64_t* J, int64_t k, int M, const void* signals, int64_t B,
+                                          int64_t ld, int dtype, void* out, int64_t ld_out, int nthreads,
+                                          sfft_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -525,6 +525,7 @@ struct FusedArgs {
   void* out;
   int64_t ld_out;
   int32_t* status;  // n_supports
+  int identity;     // rows pre-gathered in each row's own slot order (ld >= A)
 };
 
 // Plan for one support on `nthr` threads (tid in [0, nthr)).  Every thread
@@ -665,9 +666,9 @@ k_fused_to_dft(const FusedArgs args) {
     if (ok) {
       uint32_t d[S > 0 ? S : 1];
 #pragma unroll
-      for (int i = 0; i < S; ++i) d[i] = 1u << (args.M - 1 - spiv[i]);
+      for (int i = 0; i < S; ++i) d[i] = args.identity ? (1u << i) : (1u << (args.M - 1 - spiv[i]));
       const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
-      gather<T, S>(v, t, row, d, 0u, nmask);
+      gather<T, S>(v, t, row, d, 0u, args.identity ? (uint32_t)(A - 1) : nmask);
     } else {
 #pragma unroll
       for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
@@ -1676,7 +1677,8 @@ extern "C" int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_su
 }
 
 int sfft::fused_to_dft(const int64_t* J, int64_t k, int64_t n_supports, int M, const void* signals, int64_t B,
-                       int64_t ld, int dtype, void* out, int64_t ld_out, int32_t* status, cudaStream_t st) {
+                       int64_t ld, int dtype, void* out, int64_t ld_out, int32_t* status, cudaStream_t st,
+                       int identity) {
   if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
   if (dtype != SFFT_C64 && dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown dtype");
   if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
@@ -1684,7 +1686,7 @@ int sfft::fused_to_dft(const int64_t* J, int64_t k, int64_t n_supports, int M, c
     return fail(SFFT_ERR_INVALID, "n_supports must be 1 or B");
   if (B == 0) return SFFT_OK;
   if (!J || !signals || !out) return fail(SFFT_ERR_INVALID, "null pointer");
-  if (ld < (1ll << M)) return fail(SFFT_ERR_INVALID, "signal row stride smaller than N");
+  if (ld < (identity ? k : (1ll << M))) return fail(SFFT_ERR_INVALID, "signal row stride too small");
   if (ld_out < k) return fail(SFFT_ERR_INVALID, "output row stride too small");
   if (k & (k - 1)) return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a homogeneous support");
   const int s = 63 - __builtin_clzll((unsigned long long)k);
@@ -1717,6 +1719,7 @@ int sfft::fused_to_dft(const int64_t* J, int64_t k, int64_t n_supports, int M, c
   a.out = out;
   a.ld_out = ld_out;
   a.status = dstat;
+  a.identity = identity;
   int rc = (n_supports == 1 && B >= 1) ? dispatch_fused<false>(dtype, s, a, st)
                                        : dispatch_fused<true>(dtype, s, a, st);
   if (rc == SFFT_OK && tmpStat) {

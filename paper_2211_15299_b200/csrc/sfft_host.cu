@@ -120,6 +120,7 @@ struct RowJob {
   char* out = nullptr;
   std::atomic<int64_t> next{0};
   std::unique_ptr<std::atomic<int64_t>[]> done;  // source rows finished per chunk
+  const std::function<void(int64_t)>* row_fn = nullptr;  // custom per-row work (replaces the gather)
 
   template <typename In, typename Out>
   void rows(int64_t r0, int64_t r1) const {
@@ -141,7 +142,8 @@ struct RowJob {
     const int64_t r0 = next.fetch_add(grain, std::memory_order_relaxed);
     if (r0 >= B) return false;
     const int64_t r1 = std::min(B, r0 + grain);
-    if (in_esz == 8 && out_esz == 8) rows<C64b, C64b>(r0, r1);
+    if (row_fn) for (int64_t r = r0; r < r1; ++r) (*row_fn)(r);
+    else if (in_esz == 8 && out_esz == 8) rows<C64b, C64b>(r0, r1);
     else if (in_esz == 8) rows<float2, double2>(r0, r1);
     else rows<C128b, C128b>(r0, r1);
     // grains never straddle chunks (chunk is a multiple of grain)
@@ -176,6 +178,9 @@ struct Staging {
   void* d_in = nullptr;  size_t d_in_n = 0;
   void* d_out = nullptr; size_t d_out_n = 0;
   void* d_slot = nullptr; size_t d_slot_n = 0;
+  void* h_J = nullptr;   size_t h_J_n = 0;   // per-signal supports (fused host path)
+  void* d_J = nullptr;   size_t d_J_n = 0;
+  void* d_stat = nullptr; size_t d_stat_n = 0;
   cudaEvent_t h_free = nullptr;
   int device = -1;
 };
@@ -208,9 +213,11 @@ static int stage_begin(int dev) {
     if (S.d_in) cudaFree(S.d_in);
     if (S.d_out) cudaFree(S.d_out);
     if (S.d_slot) cudaFree(S.d_slot);
+    if (S.d_J) cudaFree(S.d_J);
+    if (S.d_stat) cudaFree(S.d_stat);
     if (S.h_free) cudaEventDestroy(S.h_free);
-    S.d_in = S.d_out = S.d_slot = nullptr;
-    S.d_in_n = S.d_out_n = S.d_slot_n = 0;
+    S.d_in = S.d_out = S.d_slot = S.d_J = S.d_stat = nullptr;
+    S.d_in_n = S.d_out_n = S.d_slot_n = S.d_J_n = S.d_stat_n = 0;
     S.h_free = nullptr;
     S.device = dev;
   }
@@ -455,4 +462,135 @@ extern "C" int sfft_host_stage(const sfft_plan* plan, const void* signals, int64
   }
   cudaEventRecord(S.h_free, st);
   return rc;
+}
+
+// hidft_to_dft for per-signal supports with signals, supports and results in
+// HOST memory (config 4 from numpy): per row the host threads derive the
+// support's pivots (homogeneous: the set bits of OR_j 2^v2(j ^ j_0)), gather
+// the 2^s samples in slot order and stage the support; chunks of rows go to
+// the device, where the fused kernel rebuilds each plan on chip from the
+// support and transforms the staged samples.  Invalid supports are staged as
+// zeros and reported by the device as status 2 / 3 naming the support.
+extern "C" int sfft_hidft_to_dft_fused_host(const int64_t* J, int64_t k, int M, const void* signals, int64_t B,
+                                            int64_t ld, int dtype, void* out, int64_t ld_out, int nthreads,
+                                            sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
+  if (dtype != SFFT_C64 && dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown dtype");
+  if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
+  if (B < 0) return fail(SFFT_ERR_INVALID, "negative batch");
+  if (B == 0) return SFFT_OK;
+  if (!J || !signals || !out) return fail(SFFT_ERR_INVALID, "null pointer");
+  if (is_device_pointer(J) && !is_pinned_host(J)) return fail(SFFT_ERR_INVALID, "supports must be in host memory");
+  const int64_t N = 1ll << M;
+  if (ld < N) return fail(SFFT_ERR_INVALID, "signal row stride smaller than N");
+  if (ld_out < k) return fail(SFFT_ERR_INVALID, "output row stride too small");
+  if (k & (k - 1)) return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a homogeneous support");
+  const int s = 63 - __builtin_clzll((unsigned long long)k);
+  const int64_t A = k;
+  const int esz = dtype == SFFT_C64 ? 8 : 16;
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  int rc = stage_begin(dev);
+  if (rc) return rc;
+  Staging& Sg = g_stage;
+  const bool out_pinned = is_pinned_host(out);
+  const size_t in_bytes = (size_t)B * A * esz, out_bytes = (size_t)B * k * esz, j_bytes = (size_t)B * k * 8;
+  if ((rc = grow_host(&Sg.h_in, &Sg.h_in_n, in_bytes))) return rc;
+  if ((rc = grow_host(&Sg.h_J, &Sg.h_J_n, j_bytes))) return rc;
+  if ((rc = grow_dev(&Sg.d_in, &Sg.d_in_n, in_bytes))) return rc;
+  if ((rc = grow_dev(&Sg.d_out, &Sg.d_out_n, out_bytes))) return rc;
+  if ((rc = grow_dev(&Sg.d_J, &Sg.d_J_n, j_bytes))) return rc;
+  if ((rc = grow_dev(&Sg.d_stat, &Sg.d_stat_n, (size_t)B * 4))) return rc;
+  if (!out_pinned && (rc = grow_host(&Sg.h_out, &Sg.h_out_n, out_bytes))) return rc;
+  char* out_tgt = out_pinned ? (char*)out : (char*)Sg.h_out;
+  const int64_t ldo_tgt = out_pinned ? ld_out : k;
+
+  const char* sig = (const char*)signals;
+  char* h_in = (char*)Sg.h_in;
+  int64_t* h_J = (int64_t*)Sg.h_J;
+  const std::function<void(int64_t)> row_fn = [&](int64_t r) {
+    const int64_t* Jr = J + r * k;
+    std::memcpy(h_J + r * k, Jr, (size_t)k * 8);
+    char* o = h_in + (size_t)r * A * esz;
+    // pivots of a homogeneous support (congruence.py:76-101): the levels v2(j - j_0)
+    bool ok = Jr[0] >= 0 && Jr[0] < N;
+    uint64_t mask = 0;
+    for (int64_t e = 1; e < k && ok; ++e) {
+      ok = Jr[e] > Jr[e - 1] && Jr[e] < N;
+      mask |= 1ull << __builtin_ctzll((unsigned long long)(Jr[e] ^ Jr[0]));
+    }
+    if (!ok || __builtin_popcountll(mask) != s) {  // the device reports it
+      std::memset(o, 0, (size_t)A * esz);
+      return;
+    }
+    int64_t d[32];
+    for (int i = 0; i < s; ++i) {
+      const int piv = __builtin_ctzll(mask);
+      mask &= mask - 1;
+      d[i] = 1ll << (M - 1 - piv);  // hidft.py:155-158
+    }
+    const char* row = sig + (size_t)r * ld * esz;
+    int64_t offs[1 << 13];
+    offs[0] = 0;
+    for (int64_t a = 1; a < A; ++a) offs[a] = offs[a & (a - 1)] + d[__builtin_ctzll((unsigned long long)a)];
+    if (esz == 8) {
+      const C64b* rw = (const C64b*)row;
+      C64b* ow = (C64b*)o;
+      for (int64_t a = 0; a < A; ++a) ow[a] = rw[offs[a]];
+    } else {
+      const C128b* rw = (const C128b*)row;
+      C128b* ow = (C128b*)o;
+      for (int64_t a = 0; a < A; ++a) ow[a] = rw[offs[a]];
+    }
+  };
+  if (A > (1 << 13)) return fail(SFFT_ERR_UNSUPPORTED, "host fused path limited to 2^13 slots");
+
+  RowJob job;
+  job.B = B;
+  job.A = A;
+  job.row_fn = &row_fn;
+  job.set_chunking(0);
+  const bool use_pool = B * A >= kPoolMinSamples;
+  HostPool& p = pool(nthreads);
+  const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
+  if (use_pool) p.start(&fn);
+  int32_t* dstat = (int32_t*)Sg.d_stat;
+  for (int64_t c = 0; c < job.nchunks() && rc == SFFT_OK; ++c) {
+    job.await(c);
+    const int64_t b0 = c * job.chunk, rows = job.chunk_rows(c);
+    char* din = (char*)Sg.d_in + (size_t)b0 * A * esz;
+    int64_t* dJ = (int64_t*)Sg.d_J + b0 * k;
+    char* dout = (char*)Sg.d_out + (size_t)b0 * k * esz;
+    cudaError_t e = cudaMemcpyAsync(din, h_in + (size_t)b0 * A * esz, (size_t)rows * A * esz,
+                                    cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dJ, h_J + b0 * k, (size_t)rows * k * 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "host->device chunk copy"); break; }
+    rc = fused_to_dft(dJ, k, rows, M, din, rows, A, dtype, dout, k, dstat + b0, st, 1);
+    if (rc) break;
+    e = cudaMemcpy2DAsync(out_tgt + (size_t)b0 * ldo_tgt * esz, (size_t)ldo_tgt * esz, dout, (size_t)k * esz,
+                          (size_t)k * esz, rows, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "device->host chunk copy");
+  }
+  if (use_pool) {
+    while (job.step()) {}
+    p.wait();
+  }
+  std::vector<int32_t> hs((size_t)B);
+  cudaEventRecord(Sg.h_free, st);
+  cudaError_t es = rc ? cudaSuccess : cudaMemcpyAsync(hs.data(), dstat, (size_t)B * 4, cudaMemcpyDeviceToHost, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (rc) return rc;
+  if (es != cudaSuccess || e2 != cudaSuccess) return cuda_fail(es != cudaSuccess ? es : e2, "fused host transform");
+  for (int64_t i = 0; i < B; ++i) {
+    if (hs[i] == 2) return fail(SFFT_ERR_INVALID, "support " + std::to_string(i) + " is not a valid SupportSet");
+    if (hs[i] == 3)
+      return fail(SFFT_ERR_CONTRACT, "hidft_to_dft requires a homogeneous support (support " + std::to_string(i) + ")");
+  }
+  if (!out_pinned)
+    for (int64_t b = 0; b < B; ++b)
+      std::memcpy((char*)out + (size_t)b * ld_out * esz, out_tgt + (size_t)b * k * esz, (size_t)k * esz);
+  return SFFT_OK;
 }

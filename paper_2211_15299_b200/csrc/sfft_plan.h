@@ -53,8 +53,10 @@ int max_supported_s(int dtype);
 // per-signal plans only serve sfft_hidft(SFFT_OUT_DFT)
 int reject_per_signal(const sfft_plan* p, const char* entry);
 // hidft_to_dft for per-signal supports (sfft_hidft_to_dft_fused's body)
+// identity: rows pre-gathered in each row's own slot order (row stride >= k)
 int fused_to_dft(const int64_t* J, int64_t k, int64_t n_supports, int M, const void* signals, int64_t B,
-                 int64_t ld, int dtype, void* out, int64_t ld_out, int32_t* status, cudaStream_t st);
+                 int64_t ld, int dtype, void* out, int64_t ld_out, int32_t* status, cudaStream_t st,
+                 int identity = 0);
 // pre-gathered rows (identity loads): slot order, or sorted order when
 // gathered_sorted(plan) (the cluster transform, 2^s beyond one CTA)
 bool gathered_sorted(const sfft_plan* p);

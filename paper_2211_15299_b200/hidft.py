@@ -399,6 +399,14 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         jt = J if torch.is_tensor(J) else torch.as_tensor(np.asarray(J, dtype=np.int64))
         if jt.dim() != 2 or jt.shape[0] != B:
             raise InvalidInputError("per-signal supports must be a (B, k) tensor")
+        if host_out:  # host rows: host threads derive pivots and gather, the device transforms
+            jh = jt.to("cpu", dtype=torch.int64).contiguous()
+            res = torch.empty((B, jh.shape[1]), dtype=sig.dtype, pin_memory=True)
+            with torch.cuda.device(run_dev):
+                _lib.check(_lib.load().sfft_hidft_to_dft_fused_host(
+                    jh.data_ptr(), jh.shape[1], M, sig.data_ptr(), B, sig.stride(0), _DT[sig.dtype], res.data_ptr(),
+                    res.shape[1], _host_threads(), _lib.stream_ptr(run_dev)))
+            return res[0] if single else res
         jt = jt.to(run_dev, dtype=torch.int64, non_blocking=True).contiguous()
         nsup, k = B, jt.shape[1]
         Js = None
@@ -421,8 +429,6 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         _lib.check(lib.sfft_hidft(plan.handle, sig.data_ptr(), B, sig.stride(0), 0, _lib.OUT_DFT,
                                   out.data_ptr(), out.stride(0), None, 0, stream))
         return out[0] if single else out
-    if host_out and not sig.is_pinned():
-        sig = sig.to(run_dev)  # per-signal plans are derived on chip: the kernel reads the rows
     if st is None and check:
         st = torch.zeros(nsup, dtype=torch.int32, device=run_dev)
     _lib.check(lib.sfft_hidft_to_dft_fused(jt.data_ptr(), k, nsup, M, sig.data_ptr(), B, sig.stride(0),
@@ -435,5 +441,4 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         if (bad == 3).any():
             raise ContractViolationError(
                 f"hidft_to_dft requires a homogeneous support (row {int(np.argmax(bad == 3))})")
-    res = out[0] if single else out
-    return res.cpu() if host_out else res
+    return out[0] if single else out

@@ -517,6 +517,33 @@ def test_largest_modulus(S, torch):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_per_signal_host_rows(S, torch, pinned):
+    """Config-4 shape with host rows: host-derived pivots + host gather +
+    on-chip plans (sfft_hidft_to_dft_fused_host) equal the device-resident
+    fused transform bit for bit; a non-homogeneous row raises the contract error."""
+    from paper_2211_15299_b200 import workloads as W
+    wl = W.make_workload(4, 40)
+    sig = torch.empty((wl.B, 1 << wl.M), dtype=torch.complex64, device="cuda")
+    W.synthesize_into(sig, wl.support, wl.coeffs)
+    Jt = torch.from_numpy(wl.support)
+    want = S.hidft_to_dft_batched(sig, Jt.cuda())
+    host = sig.cpu()
+    if pinned:
+        host = host.pin_memory()
+    got = S.hidft_to_dft_batched(host, Jt)
+    assert not got.is_cuda
+    assert torch.equal(got, want.cpu())
+    got_np = S.hidft_to_dft_batched(host.numpy(), wl.support)   # numpy rows and supports
+    assert torch.equal(torch.as_tensor(got_np), want.cpu())
+    bad = wl.support.copy()
+    bad[7, 0] = (bad[7, 0] + 1) % (1 << wl.M)
+    bad[7].sort()
+    if len(np.unique(bad[7])) == bad.shape[1]:
+        with pytest.raises((S.ContractViolationError, S.InvalidInputError)):
+            S.hidft_to_dft_batched(host, torch.from_numpy(bad))
+
+
 # ------------------------------------------------- configs at full size ---
 
 def _synth(torch, S, cfg, B, per_signal_rows=None):
