@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -82,8 +83,13 @@ class HostPool {
 static std::mutex g_host_mu;  // one host job at a time through the shared pool and staging
 static HostPool* g_pool = nullptr;
 
-// default: every core but the calling thread's (which gathers too)
-static int default_threads() { return std::max(1, (int)std::thread::hardware_concurrency() - 1); }
+// default: every core but the calling thread's (which gathers too), shared
+// between the processes of one node under torchrun (LOCAL_WORLD_SIZE)
+static int default_threads() {
+  int hw = (int)std::thread::hardware_concurrency();
+  if (const char* e = getenv("LOCAL_WORLD_SIZE")) hw /= std::max(1, atoi(e));
+  return std::max(1, hw - 1);
+}
 
 static HostPool& pool(int want) {  // caller holds g_host_mu
   const int n = want > 0 ? want : default_threads();
