@@ -303,9 +303,16 @@ def run_b200(args) -> None:
     # gather sectors + coefficient writes + support reads (shared: once; per-signal: B*k int64)
     G = footprint + B * wl.k * esz + wl.support.size * 8
     achieved = G / (ms_per_step / 1e3) / 1e9
+    A_sl = 1 << (len(S.pivots(J)) if wl.support.ndim == 1 else int(math.log2(wl.k)))
+    flops_step = int(B * 5 * A_sl * max(1, int(math.log2(A_sl))))
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
             "kernels_per_step": launches_per_step,
+            # secondary: flops 5 A log2 A per signal against the measured
+            # non-tensor FMA peak (tools/fma_peak.cu: 66.4 TF/s fp32, 32.7 TF/s fp64)
+            "flops": {"per_step": flops_step, "achieved_tflops": round(flops_step / (ms_per_step / 1e3) / 1e12, 3),
+                      "peak_tflops": 66.4 if esz == 8 else 32.7,
+                      "frac": round(flops_step / (ms_per_step / 1e3) / 1e12 / (66.4 if esz == 8 else 32.7), 4)},
             "algorithmic_bytes_per_launch": int(G),
             "element_bytes_per_launch": int(B * (pattern_bytes[1] if pattern_bytes else 0) + B * wl.k * esz)}
     # the same kernel against HBM bytes at the measured 128 B access granularity
