@@ -36,6 +36,8 @@ struct sfft_plan {
 namespace sfft {
 // largest s handled on one CTA (one signal's slots resident in shared memory)
 constexpr int kMaxPlanS_c64 = 14, kMaxPlanS_c128 = 13;
+// largest s of the fused per-signal transform (plan derived on chip)
+constexpr int kMaxFusedS_c64 = 13, kMaxFusedS_c128 = 12;
 // largest s of the device transform (two-pass split beyond kMaxPlanS)
 constexpr int kMaxSplitS_c64 = 17, kMaxSplitS_c128 = 16;
 // split for 2^s beyond one CTA: the first lc stages run across 2^lc blocks,

@@ -332,8 +332,8 @@ def test_hidft_host_capi(S, torch, dt, pinned):
 
 
 @pytest.mark.parametrize("dt,s", [(np.complex64, 15), (np.complex64, 16), (np.complex128, 14)])
-def test_gathered_cluster_paths(S, torch, dt, s):
-    """2^s beyond one CTA (thread-block cluster transform): host rows through
+def test_gathered_split_paths(S, torch, dt, s):
+    """2^s beyond one CTA (two-pass split transform): host rows through
     sfft_hidft_host (sorted-order staging) and device rows pre-gathered in
     slot order through sfft_hidft_gathered match the direct-gather launch
     bit for bit."""
@@ -600,11 +600,11 @@ def test_config3_sas(S, torch, golden_configs):
         assert rel_l2(got[b], golden_configs[f"cfg3_b{b}_out"]) < 1e-5
 
 
-# ----------------------------------------------- cluster path (large A) ---
+# ------------------------------------------------- split path (large A) ---
 
 @pytest.mark.parametrize("dt,s", [(np.complex64, 15), (np.complex64, 16), (np.complex64, 17),
                                   (np.complex128, 14), (np.complex128, 15), (np.complex128, 16)])
-def test_cluster_homogeneous(S, torch, dt, s):
+def test_split_homogeneous(S, torch, dt, s):
     rng = np.random.default_rng(1000 + s)
     M, B = 22, 3
     piv = sorted(rng.choice(M, size=s, replace=False).tolist())
@@ -624,7 +624,7 @@ def test_cluster_homogeneous(S, torch, dt, s):
     assert rel_l2(res.slot_values[0].cpu().numpy(), o.slot_values) < TOL[dt]
 
 
-def test_cluster_part_homogeneous_sas(S, torch):
+def test_split_part_homogeneous_sas(S, torch):
     # config-3 shape at larger scale: a 2^13 subset of a 2^16 homogeneous set
     rng = np.random.default_rng(77)
     M = 24
