@@ -2,27 +2,30 @@
 
 `hidft(source, J, r, height, shift)` and `hidft_to_dft(res)` keep the
 reference signatures and results (hidft.py:135-207); a source may now also be
-a (B, N) batch.  `hidft_to_dft_batched` is the fused hot path: one kernel
-launch derives the plan on chip, gathers the 2^s samples of every signal,
-runs the butterfly and writes (Ff)_J in ascending-J order.
+a (B, N) batch.  `hidft_to_dft_batched` is the batched hot path: for a shared
+support one launch gathers the 2^s samples of every signal through the
+support's cached device plan, runs the butterfly and writes (Ff)_J in
+ascending-J order; for per-signal supports one fused launch also derives each
+signal's plan on chip.
 
 Sources (hidft.py:34-49):
   * CUDA tensor (N,) or (B, N), complex64 / complex128 -> computed in that
     precision (complex64 signals run the float32 kernels);
-  * host-resident numpy / CPU tensor -> the library's host thread pool
-    gathers the 2^s samples per signal into pinned staging, pipelined with
-    their DMA, the device transform and the copy back (only those samples
-    cross PCIe; per-signal supports read page-locked rows zero-copy);
+  * host-resident numpy / CPU tensor (pinned or pageable) -> the library's
+    host thread pool gathers the 2^s samples per signal into pinned staging
+    (deriving per-signal pivots on the host for per-signal supports),
+    pipelined with their DMA, the device transform and the copy back: only
+    those samples cross PCIe;
   * callable loc -> samples, or an object with `sample_block(loc)` (e.g. the
     reference's BandlimitedSignal) -> evaluated at the plan's offsets on the
-    host, then transformed on the device.
-Results are CUDA tensors for CUDA sources and numpy arrays otherwise.
+    host (band-limited sources are synthesised on the device), then
+    transformed on the device.
+Results are CUDA tensors for CUDA sources and host arrays otherwise.
 """
 
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass, field
 from typing import Any, Sequence
 
@@ -123,8 +126,8 @@ def get_plan(J: SupportSet, r: tuple[int, ...], height: int, dtype_code: int, de
 
 @dataclass
 class _Src:
-    kind: str               # "device" | "pinned" | "host" | "callable" | "synth"
-    tensor: Any = None      # 2-D (B, N) view for device/pinned/host
+    kind: str               # "device" | "host" | "callable" | "synth"
+    tensor: Any = None      # 2-D (B, N) view for device/host
     batched: bool = False
     dtype_code: int = _lib.C128
     device: Any = None

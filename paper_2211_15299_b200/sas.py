@@ -15,7 +15,7 @@ Node weights up to 64 are decoded on the device.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Sequence
 
 import numpy as np
@@ -24,7 +24,7 @@ from . import _lib
 from .congruence import (SupportSet, as_support, assert_part_homogeneous, pivots as support_pivots,
                          validate_pivot_vector)
 from .errors import InvalidInputError
-from .hidft import (_count, _finish, _gathered_samples, _host_threads, _host_transform, _prepare_source, _torch,
+from .hidft import (_finish, _gathered_samples, _host_threads, _host_transform, _prepare_source, _torch,
                     get_plan)
 
 C1 = 1.5  # per-stage butterfly constant (sas.py:38)

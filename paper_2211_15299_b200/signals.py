@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .congruence import SupportSet, as_support
+from .congruence import as_support
 from .errors import InvalidInputError
 
 

@@ -7,7 +7,6 @@ import json
 import os
 from contextlib import redirect_stdout
 
-import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
