@@ -207,15 +207,16 @@ __device__ void vandermonde_solve(const C64x* x, const C64x* y, int n, const int
   for (int i = 0; i < n; ++i) out[perm[i]] = c[i];
 }
 
+// out[j] = sum_m x_m^j c_m, the powers by repeated multiplication and each
+// sum in increasing m (the same operations as forming V row by row), O(n^2)
 __device__ void forward_apply(const C64x* x, const C64x* c, int n, C64x* out) {
-  for (int j = 0; j < n; ++j) {
-    C64x acc = {0.0, 0.0};
-    for (int m = 0; m < n; ++m) {
-      C64x p = {1.0, 0.0};
-      for (int e = 0; e < j; ++e) p = cm(p, x[m]);
-      acc = {acc.x + (p.x * c[m].x - p.y * c[m].y), acc.y + (p.x * c[m].y + p.y * c[m].x)};
+  for (int j = 0; j < n; ++j) out[j] = {0.0, 0.0};
+  for (int m = 0; m < n; ++m) {
+    C64x p = {1.0, 0.0};
+    for (int j = 0; j < n; ++j) {
+      if (j) p = cm(p, x[m]);
+      out[j] = {out[j].x + (p.x * c[m].x - p.y * c[m].y), out[j].y + (p.x * c[m].y + p.y * c[m].x)};
     }
-    out[j] = acc;
   }
 }
 
@@ -251,14 +252,17 @@ __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
   const double noise_eps = 100.0 * 2.220446049250313e-16;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = id / a.n_nodes, v = id % a.n_nodes;
+    // node-major: a warp decodes one node for 32 signals, so every lane runs
+    // the same system size (node weights differ from node to node)
+    const int64_t v = id / a.B, b = id % a.B;
+    const int64_t fid = b * a.n_nodes + v;  // flags / resid stay (signal, node) row-major
     const int off = a.node_off[v], m = a.node_off[v + 1] - off;
     C64x* out = reinterpret_cast<C64x*>(a.out) + b * a.ld_out;
     if (m == 1) {
       const C64x raw = nodeval(a, b * a.mu, v);
       out[a.node_mem[off]] = a.scale == 1.0 ? raw : C64x{raw.x * a.scale, raw.y * a.scale};
-      a.flags[id] = 0;
-      a.resid[id] = 0.0;
+      a.flags[fid] = 0;
+      a.resid[fid] = 0.0;
       continue;
     }
     C64x x[kMaxMu], y[kMaxMu], c[kMaxMu], r[kMaxMu], d[kMaxMu];
@@ -333,8 +337,8 @@ __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
       if (res > fmax(a.tol, 1e-9)) flag = 2;
     }
     for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = c[i];
-    a.flags[id] = flag;
-    a.resid[id] = res;
+    a.flags[fid] = flag;
+    a.resid[fid] = res;
   }
 }
 
@@ -375,8 +379,8 @@ __device__ __forceinline__ dd shfl_dd(dd v, int d) {
 }
 
 // one WARP per escalated node: re-measure (sas.py:290-310) with the A-term dd
-// dot products split across the lanes (butterfly-reduced in dd), then lane 0
-// solves in dd (_ddc.py:235-254)
+// dot products split across the lanes (butterfly-reduced in dd), then the
+// warp solves in dd across its lanes (_ddc.py:235-254)
 __global__ void k_sas_decode_dd(const SasDDArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -387,31 +391,109 @@ __global__ void k_sas_decode_dd(const SasDDArgs a) {
     const int off = s.node_off[v], m = s.node_off[v + 1] - off;
     const uint64_t resid = (uint64_t)(int64_t)a.node_res[v];
     cdd y[kMaxMu];
-    for (int j = 0; j < m; ++j) {
-      cdd acc = {{0.0, 0.0}, {0.0, 0.0}};
+    // shifts in groups of JG: each root kernel value serves JG shifts (per
+    // shift the lane still sums its terms in increasing i, as before)
+    constexpr int JG = 4;
+    for (int j0 = 0; j0 < m; j0 += JG) {
+      cdd acc[JG];
+#pragma unroll
+      for (int g = 0; g < JG; ++g) acc[g] = {{0.0, 0.0}, {0.0, 0.0}};
       for (int64_t i = lane; i < a.A; i += 32) {
         const cdd kern = a.tab.get((uint64_t)(-(int64_t)(resid * (uint64_t)a.pattern[i])));
-        acc = cdd_add(acc, cdd_mul(dd_sample(a, b, j, i), kern));
+#pragma unroll
+        for (int g = 0; g < JG; ++g)
+          if (j0 + g < m) acc[g] = cdd_add(acc[g], cdd_mul(dd_sample(a, b, j0 + g, i), kern));
       }
-      for (int d = 16; d > 0; d >>= 1) {
-        const cdd o = {shfl_dd(acc.re, d), shfl_dd(acc.im, d)};
-        acc = cdd_add(acc, o);
+#pragma unroll
+      for (int g = 0; g < JG; ++g) {
+        if (j0 + g >= m) break;
+        cdd t = acc[g];
+        for (int d = 16; d > 0; d >>= 1) {
+          const cdd o = {shfl_dd(t.re, d), shfl_dd(t.im, d)};
+          t = cdd_add(t, o);
+        }
+        y[j0 + g] = cdd_mul_complex(t, s.scale, 0.0);
       }
-      y[j] = cdd_mul_complex(acc, s.scale, 0.0);
     }
-    if (lane != 0) continue;
-    // solve_vandermonde_dd: x_m = root((-l) mod N), BP, no Leja
-    cdd x[kMaxMu];
-    for (int i = 0; i < m; ++i) x[i] = a.tab.get((uint64_t)(-(int64_t)s.J[s.node_mem[off + i]]));
-    for (int k = 0; k < m - 1; ++k)
-      for (int j = m - 1; j > k; --j) y[j] = cdd_sub(y[j], cdd_mul(x[k], y[j - 1]));
+    // solve_vandermonde_dd (x_m = root((-l) mod N), BP, no Leja), the lanes
+    // holding the unknowns: inside each BP sweep every update reads only
+    // values from before the sweep, so lane j (and j + 32) updates its own
+    // entries from shuffled neighbours -- the same dd operations per entry as
+    // the sequential loops, in the same order
+    constexpr int Q = (kMaxMu + 31) / 32;
+    cdd yl[Q], xl[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = lane + 32 * q;
+      yl[q] = j < m ? y[j] : cdd{{0.0, 0.0}, {0.0, 0.0}};
+      xl[q] = j < m ? a.tab.get((uint64_t)(-(int64_t)s.J[s.node_mem[off + j]])) : cdd{{0.0, 0.0}, {0.0, 0.0}};
+    }
+    // value of entry j - 1 (dir -1) or j + 1 (dir +1) from before the sweep
+    auto neighbour = [&](const cdd (&v)[Q], int q, int dir) -> cdd {
+      const int src = (lane + dir) & 31;
+      cdd r;
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) {
+        const cdd t = {{__shfl_sync(0xffffffffu, v[qq].re.hi, src), __shfl_sync(0xffffffffu, v[qq].re.lo, src)},
+                       {__shfl_sync(0xffffffffu, v[qq].im.hi, src), __shfl_sync(0xffffffffu, v[qq].im.lo, src)}};
+        const int want = q + ((dir < 0 && lane == 0) ? -1 : (dir > 0 && lane == 31) ? 1 : 0);
+        if (qq == want) r = t;
+      }
+      return r;
+    };
+    auto xat = [&](int idx) -> cdd {  // x[idx] broadcast from its lane
+      cdd r = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) {
+        const cdd t = {{__shfl_sync(0xffffffffu, xl[qq].re.hi, idx & 31), __shfl_sync(0xffffffffu, xl[qq].re.lo, idx & 31)},
+                       {__shfl_sync(0xffffffffu, xl[qq].im.hi, idx & 31), __shfl_sync(0xffffffffu, xl[qq].im.lo, idx & 31)}};
+        if (qq == (idx >> 5)) r = t;
+      }
+      return r;
+    };
+    for (int k = 0; k < m - 1; ++k) {  // y[j] -= x[k] y[j-1], j = m-1 .. k+1
+      const cdd xk = xat(k);
+      cdd prev[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) prev[q] = neighbour(yl, q, -1);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int j = lane + 32 * q;
+        if (j > k && j < m) yl[q] = cdd_sub(yl[q], cdd_mul(xk, prev[q]));
+      }
+    }
     for (int k = m - 2; k >= 0; --k) {
-      for (int j = k + 1; j < m; ++j) y[j] = cdd_div(y[j], cdd_sub(x[j], x[j - k - 1]));
-      for (int j = k; j < m - 1; ++j) y[j] = cdd_sub(y[j], y[j + 1]);
+      // y[j] /= x[j] - x[j-k-1], j = k+1 .. m-1
+      cdd xs[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int j = lane + 32 * q;
+        const int src = j - k - 1;
+        const cdd t = xat(src < 0 ? 0 : src);
+        xs[q] = t;
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int j = lane + 32 * q;
+        if (j > k && j < m) yl[q] = cdd_div(yl[q], cdd_sub(xl[q], xs[q]));
+      }
+      // y[j] -= y[j+1], j = k .. m-2 (old y[j+1])
+      cdd nxt[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) nxt[q] = neighbour(yl, q, +1);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int j = lane + 32 * q;
+        if (j >= k && j < m - 1) yl[q] = cdd_sub(yl[q], nxt[q]);
+      }
     }
     C64x* out = reinterpret_cast<C64x*>(s.out) + b * s.ld_out;
-    for (int i = 0; i < m; ++i)
-      out[s.node_mem[off + i]] = {__dadd_rn(y[i].re.hi, y[i].re.lo), __dadd_rn(y[i].im.hi, y[i].im.lo)};
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = lane + 32 * q;
+      if (j < m)
+        out[s.node_mem[off + j]] = {__dadd_rn(yl[q].re.hi, yl[q].re.lo), __dadd_rn(yl[q].im.hi, yl[q].im.lo)};
+    }
   }
 }
 

@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2211_15299_b200 as S  # noqa: E402
 from paper_2211_15299_b200 import workloads as W  # noqa: E402
-import paper_2211_15299_b200.sas as sasmod  # noqa: E402
+
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 wl = W.make_workload(3, B)
