@@ -508,6 +508,9 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_inv_node);
   cudaFree(p->d_node_off);
   cudaFree(p->d_node_mem);
+  cudaFree(p->d_node_x);
+  cudaFree(p->d_node_perm);
+  cudaFree(p->d_node_amp);
   cudaFree(p->d_tw_blk);
   cudaFree(p->d_inv_elem_blk);
   cudaFree(p->d_inv_node_blk);

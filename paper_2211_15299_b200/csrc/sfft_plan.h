@@ -21,6 +21,9 @@ struct sfft_plan {
   int32_t* d_inv_node;       // A   slot -> node rank (-1: virtual)
   int32_t* d_node_off;       // n_nodes+1  node membership CSR (built on first SAS decode)
   int32_t* d_node_mem;       // k          member element indices, ascending per node
+  void* d_node_x;            // k complex128: e^{-2 pi i J/N} per member (SAS decode, built on first use)
+  int32_t* d_node_perm;      // k          Leja order within each node
+  double* d_node_amp;        // n_nodes    ||inv(V)||_inf per node
   // two-pass (split) transform for 2^s beyond one CTA (sfft_hidft.cu, k_split_*):
   // block t of 2^lc holds the slots whose low lc bits are brev_lc(t)
   int split_lc;              // lc (0: single-CTA plan)

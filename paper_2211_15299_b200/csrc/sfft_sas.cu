@@ -234,6 +234,9 @@ struct SasDecodeArgs {
   int64_t ld_out;
   int32_t* flags;  // B x n_nodes: bit0 escalate, bit1 dense fallback
   double* resid;   // B x n_nodes residual (sas.py:386-388)
+  const C64x* node_x;        // per-plan node tables (k_node_prep)
+  const int32_t* node_perm;
+  const double* node_amp;
 };
 
 __device__ __forceinline__ C64x nodeval(const SasDecodeArgs& a, int64_t row, int64_t node) {
@@ -245,10 +248,66 @@ __device__ __forceinline__ C64x nodeval(const SasDecodeArgs& a, int64_t row, int
   return {v.x, v.y};
 }
 
+// ||inv(V)||_inf in O(m^2): row q of inv(V) (V[j][m] = x_m^j) holds the
+// coefficients of the Lagrange basis L_q(z) = P(z) / ((z - x_q) P'(x_q)),
+// P(z) = prod_i (z - x_i); synthetic division per node (the reference
+// inverts V densely, sas.py:229-233; this is the same norm)
+__device__ double lagrange_inv_norm(const C64x* x, int m) {
+  double amp = 0.0;
+  C64x P[kMaxMu + 1];
+  P[0] = {1.0, 0.0};
+  for (int i = 1; i <= m; ++i) P[i] = {0.0, 0.0};
+  for (int i = 0; i < m; ++i)  // multiply by (z - x_i)
+    for (int e = i + 1; e >= 0; --e) P[e] = cs(e ? P[e - 1] : C64x{0.0, 0.0}, cm(x[i], P[e]));
+  for (int q = 0; q < m; ++q) {
+    C64x qc = P[m];  // Q(z) = P(z) / (z - x_q): leading coefficient
+    C64x den = {1.0, 0.0};
+    for (int i = 0; i < m; ++i)
+      if (i != q) den = cm(den, cs(x[q], x[i]));
+    const double dabs = cabs2(den);
+    double row = cabs2(qc);
+    for (int e = m - 1; e >= 1; --e) {
+      const C64x t = cm(x[q], qc);
+      qc = {P[e].x + t.x, P[e].y + t.y};
+      row += cabs2(qc);
+    }
+    amp = fmax(amp, row / fmax(dabs, 1e-300));
+  }
+  return amp;
+}
+
+// Per-node quantities that do not depend on the signal, computed once per
+// plan: the nodes x_l = e^{-2 pi i l / N} of each member (node-member order),
+// the Leja order (sas.py:135-150) and ||inv(V)||_inf (sas.py:229-233).
+__global__ void k_node_prep(const int32_t* __restrict__ node_off, const int32_t* __restrict__ node_mem,
+                            const int64_t* __restrict__ J, int64_t n_nodes, int M, C64x* __restrict__ node_x,
+                            int32_t* __restrict__ node_perm, double* __restrict__ node_amp) {
+  const double N = ldexp(1.0, M);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_nodes;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int off = node_off[v], m = node_off[v + 1] - off;
+    C64x x[kMaxMu];
+    int perm[kMaxMu];
+    for (int j = 0; j < m; ++j) {
+      const double l = (double)J[node_mem[off + j]];
+      double sn, co;
+      sincospi(-2.0 * l / N, &sn, &co);
+      x[j] = {co, sn};
+      node_x[off + j] = x[j];
+    }
+    if (m >= 3) {
+      leja_order(x, m, perm);
+    } else {
+      for (int i = 0; i < m; ++i) perm[i] = i;
+    }
+    for (int j = 0; j < m; ++j) node_perm[off + j] = perm[j];
+    node_amp[v] = m >= 2 ? lagrange_inv_norm(x, m) : 0.0;
+  }
+}
+
 // one thread per (signal, node)
 __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
   const int64_t total = a.B * a.n_nodes;
-  const double N = ldexp(1.0, a.M);
   const double noise_eps = 100.0 * 2.220446049250313e-16;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
@@ -270,15 +329,8 @@ __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
     for (int j = 0; j < m; ++j) {
       const C64x raw = nodeval(a, b * a.mu + j, v);
       y[j] = {raw.x * a.scale, raw.y * a.scale};
-      const double l = (double)a.J[a.node_mem[off + j]];
-      double sn, co;
-      sincospi(-2.0 * l / N, &sn, &co);  // x_l = e^{-2 pi i l / N}
-      x[j] = {co, sn};
-    }
-    if (m >= 3) {
-      leja_order(x, m, perm);
-    } else {
-      for (int i = 0; i < m; ++i) perm[i] = i;
+      x[j] = a.node_x[off + j];  // per-plan tables (k_node_prep)
+      perm[j] = a.node_perm[off + j];
     }
     vandermonde_solve(x, y, m, perm, c);
     // forward-error estimate (sas.py:214-235)
@@ -294,32 +346,7 @@ __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
     double dmax = 0.0;
     for (int i = 0; i < m; ++i) dmax = fmax(dmax, cabs2(d[i]));
     double est = dmax / denom;
-    // ||inv(V)||_inf in O(m^2): row q of inv(V) (V[j][m] = x_m^j) holds the
-    // coefficients of the Lagrange basis L_q(z) = P(z) / ((z - x_q) P'(x_q)),
-    // P(z) = prod_i (z - x_i); synthetic division per node (the reference
-    // inverts V densely, sas.py:229-233; this is the same norm)
-    double amp = 0.0;
-    {
-      C64x P[kMaxMu + 1];
-      P[0] = {1.0, 0.0};
-      for (int i = 1; i <= m; ++i) P[i] = {0.0, 0.0};
-      for (int i = 0; i < m; ++i)  // multiply by (z - x_i)
-        for (int e = i + 1; e >= 0; --e) P[e] = cs(e ? P[e - 1] : C64x{0.0, 0.0}, cm(x[i], P[e]));
-      for (int q = 0; q < m; ++q) {
-        C64x qc = P[m];  // Q(z) = P(z) / (z - x_q): leading coefficient
-        C64x den = {1.0, 0.0};
-        for (int i = 0; i < m; ++i)
-          if (i != q) den = cm(den, cs(x[q], x[i]));
-        const double dabs = cabs2(den);
-        double row = cabs2(qc);
-        for (int e = m - 1; e >= 1; --e) {
-          const C64x t = cm(x[q], qc);
-          qc = {P[e].x + t.x, P[e].y + t.y};
-          row += cabs2(qc);
-        }
-        amp = fmax(amp, row / fmax(dabs, 1e-300));
-      }
-    }
+    const double amp = a.node_amp[v];
     est = fmax(est, amp * noise_eps * ymax / denom);
     int flag = 0;
     double res = 0.0;
@@ -738,6 +765,18 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
   if (mu > kMaxMu) return fail(SFFT_ERR_UNSUPPORTED, "node weight above " + std::to_string(kMaxMu));
   int rc = sfft_plan_nodes(p, nullptr, nullptr, stream);
   if (rc) return rc;
+  if (!J_dev) return fail(SFFT_ERR_INVALID, "null support pointer");
+  {  // signal-independent node tables, built once per plan
+    std::lock_guard<std::mutex> lk(g_nodes_mu);
+    if (!p->d_node_amp) {
+      SFFT_CUDA(cudaMalloc(&p->d_node_x, sizeof(C64x) * std::max<int64_t>(p->k, 1)));
+      SFFT_CUDA(cudaMalloc((void**)&p->d_node_perm, sizeof(int32_t) * std::max<int64_t>(p->k, 1)));
+      SFFT_CUDA(cudaMalloc((void**)&p->d_node_amp, sizeof(double) * std::max<int64_t>(p->n_nodes, 1)));
+      k_node_prep<<<grid_for(p->n_nodes, 128), 128, 0, st>>>(p->d_node_off, p->d_node_mem, J_dev, p->n_nodes, p->M,
+                                                             (C64x*)p->d_node_x, p->d_node_perm, p->d_node_amp);
+      SFFT_CUDA(cudaGetLastError());
+    }
+  }
   SasDecodeArgs a{};
   a.nodevals = nodevals;
   a.ld_nv = ld_nv;
@@ -756,6 +795,9 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
   a.ld_out = ld_out;
   a.flags = flags;
   a.resid = resid;
+  a.node_x = (const C64x*)p->d_node_x;
+  a.node_perm = p->d_node_perm;
+  a.node_amp = p->d_node_amp;
   k_sas_decode_f64<<<grid_for(B * p->n_nodes), 128, 0, st>>>(a);
   SFFT_CUDA(cudaGetLastError());
   std::vector<int32_t> hf(B * p->n_nodes);
