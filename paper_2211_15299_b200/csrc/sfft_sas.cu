@@ -237,6 +237,9 @@ struct SasDecodeArgs {
   const C64x* node_x;        // per-plan node tables (k_node_prep)
   const int32_t* node_perm;
   const double* node_amp;
+  int32_t* esc_list;         // (signal, node) ids to escalate / to refactor densely,
+  int32_t* fb_list;          // appended in any order (each node is decoded on its own)
+  unsigned int* counts;      // [2] lengths of esc_list / fb_list
 };
 
 __device__ __forceinline__ C64x nodeval(const SasDecodeArgs& a, int64_t row, int64_t node) {
@@ -366,6 +369,8 @@ __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
     for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = c[i];
     a.flags[fid] = flag;
     a.resid[fid] = res;
+    if (flag == 1) a.esc_list[atomicAdd(&a.counts[0], 1u)] = (int32_t)fid;
+    else if (flag == 2) a.fb_list[atomicAdd(&a.counts[1], 1u)] = (int32_t)fid;
   }
 }
 
@@ -798,28 +803,30 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
   a.node_x = (const C64x*)p->d_node_x;
   a.node_perm = p->d_node_perm;
   a.node_amp = p->d_node_amp;
-  k_sas_decode_f64<<<grid_for(B * p->n_nodes), 128, 0, st>>>(a);
+  // escalation / fallback work lists compacted on the device: only their
+  // lengths come back to the host
+  const int64_t total = B * p->n_nodes;
+  int32_t* lists = nullptr;
+  SFFT_CUDA(cudaMallocAsync((void**)&lists, sizeof(int32_t) * (2 * total + 2), st));
+  a.esc_list = lists;
+  a.fb_list = lists + total;
+  a.counts = reinterpret_cast<unsigned int*>(lists + 2 * total);
+  SFFT_CUDA(cudaMemsetAsync(a.counts, 0, 2 * sizeof(unsigned int), st));
+  k_sas_decode_f64<<<grid_for(total), 128, 0, st>>>(a);
   SFFT_CUDA(cudaGetLastError());
-  std::vector<int32_t> hf(B * p->n_nodes);
-  SFFT_CUDA(cudaMemcpyAsync(hf.data(), flags, 4 * hf.size(), cudaMemcpyDeviceToHost, st));
+  unsigned int hc[2] = {0, 0};
+  SFFT_CUDA(cudaMemcpyAsync(hc, a.counts, sizeof(hc), cudaMemcpyDeviceToHost, st));
   SFFT_CUDA(cudaStreamSynchronize(st));
-  std::vector<int32_t> esc, fb;
-  std::vector<int32_t> esc_sigs;
-  for (int64_t i = 0; i < (int64_t)hf.size(); ++i) {
-    if (hf[i] == 1) esc.push_back((int32_t)i);
-    if (hf[i] == 2) fb.push_back((int32_t)i);
-  }
-  *n_escalated = (int64_t)esc.size();
-  *n_fallback = (int64_t)fb.size();
-  if (!esc.empty()) {
+  const int64_t n_esc = hc[0], n_fb = hc[1];
+  *n_escalated = n_esc;
+  *n_fallback = n_fb;
+  if (n_esc > 0) {
     const int M = p->M, h = M / 2;
     cdd *fine = nullptr, *coarse = nullptr, *samples = nullptr;
     if ((rc = root_tables(M, &fine, &coarse, st))) return rc;
     int64_t* pattern = nullptr;
-    int32_t *work = nullptr, *sigs = nullptr;
+    int32_t* sigs = nullptr;
     SFFT_CUDA(cudaMallocAsync(&pattern, 8 * p->A, st));
-    SFFT_CUDA(cudaMallocAsync(&work, 4 * esc.size(), st));
-    SFFT_CUDA(cudaMemcpyAsync(work, esc.data(), 4 * esc.size(), cudaMemcpyHostToDevice, st));
     rc = sfft_pivoted_pattern(p->used, p->s, M, pattern, stream);
     if (rc) return rc;
     SasDDArgs d{};
@@ -832,11 +839,15 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
     d.ld_sig = ld_sig;
     d.sig_c64 = sig_dtype == SFFT_C64;
     d.table = (const double2*)table;
-    d.work = work;
-    d.n_work = (int64_t)esc.size();
+    d.work = a.esc_list;
+    d.n_work = n_esc;
     if (bl_J) {  // band-limited: dd samples for the signals that escalated
+      std::vector<int32_t> esc((size_t)n_esc);
+      SFFT_CUDA(cudaMemcpyAsync(esc.data(), a.esc_list, 4 * esc.size(), cudaMemcpyDeviceToHost, st));
+      SFFT_CUDA(cudaStreamSynchronize(st));
       std::vector<int32_t> s2;
       for (int32_t id : esc) s2.push_back((int32_t)(id / p->n_nodes));
+      std::sort(s2.begin(), s2.end());
       s2.erase(std::unique(s2.begin(), s2.end()), s2.end());
       SFFT_CUDA(cudaMallocAsync(&sigs, 4 * s2.size(), st));
       SFFT_CUDA(cudaMemcpyAsync(sigs, s2.data(), 4 * s2.size(), cudaMemcpyHostToDevice, st));
@@ -848,20 +859,16 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
     k_sas_decode_dd<<<grid_for(d.n_work * 32, 128), 128, 0, st>>>(d);
     SFFT_CUDA(cudaGetLastError());
     cudaFreeAsync(pattern, st);
-    cudaFreeAsync(work, st);
     if (sigs) cudaFreeAsync(sigs, st);
     if (samples) cudaFreeAsync(samples, st);
   }
-  if (!fb.empty()) {
-    int32_t* work = nullptr;
+  if (n_fb > 0) {
     C64x* scratch = nullptr;
-    SFFT_CUDA(cudaMallocAsync(&work, 4 * fb.size(), st));
-    SFFT_CUDA(cudaMemcpyAsync(work, fb.data(), 4 * fb.size(), cudaMemcpyHostToDevice, st));
-    SFFT_CUDA(cudaMallocAsync(&scratch, sizeof(C64x) * kMaxMu * kMaxMu * fb.size(), st));
-    k_sas_dense<<<grid_for((int64_t)fb.size(), 32), 32, 0, st>>>(a, work, (int64_t)fb.size(), scratch);
+    SFFT_CUDA(cudaMallocAsync(&scratch, sizeof(C64x) * kMaxMu * kMaxMu * n_fb, st));
+    k_sas_dense<<<grid_for(n_fb, 32), 32, 0, st>>>(a, a.fb_list, n_fb, scratch);
     SFFT_CUDA(cudaGetLastError());
-    cudaFreeAsync(work, st);
     cudaFreeAsync(scratch, st);
   }
+  cudaFreeAsync(lists, st);
   return SFFT_OK;
 }

@@ -313,8 +313,7 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
                                        J.device_tensor(dev).data_ptr(), out.data_ptr(), k, flags.data_ptr(),
                                        resid.data_ptr(), ctypes.byref(ne), ctypes.byref(nf), stream))
         n_esc, n_fb = int(ne.value), int(nf.value)
-        flags_h = flags[0].cpu().numpy()
-        resid_h = resid[0].cpu().numpy()
+        flags_h, resid_h = flags[0], resid[0]  # device rows, read when node_systems is first used
     # exact counts (sas.py:343-398 with vandermonde_solve's formula, sas.py:196-202)
     if plan64.s:  # mu* shifted Hi-DFTs per signal: A/2 mults + A adds per stage (hidft.py:165-167)
         counter.mul((A // 2) * plan64.s * mu * B, phase="hidft")
@@ -335,8 +334,8 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
     def systems():
         node_res = plan64.tables()["node_residues"].tolist()
         members = np.split(J._arr[mem], off[1:-1])
-        fl = flags_h if flags_h is not None else np.zeros(nn, np.int32)
-        rs = resid_h if resid_h is not None else np.zeros(nn)
+        fl = flags_h.cpu().numpy() if flags_h is not None else np.zeros(nn, np.int32)
+        rs = resid_h.cpu().numpy() if resid_h is not None else np.zeros(nn)
         return [NodeSystem(node_res[v], tuple(members[v].tolist()), escalated=bool(fl[v] == 1),
                            dense_fallback=bool(fl[v] == 2), residual=float(rs[v])) for v in range(nn)]
 
