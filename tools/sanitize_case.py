@@ -22,15 +22,28 @@ S.hidft_to_dft_batched(f, Js)
 # fused per-signal
 sup = np.stack([O.gen_homogeneous(sorted(rng.choice(14, size=6, replace=False).tolist()), 14, int(rng.integers(1 << 30))) for _ in range(4)])
 S.hidft_to_dft_batched(f, torch.from_numpy(sup).cuda())
-# cluster kernel (s = 15, c64)
+# split transform (s = 15 and 16, c64; s = 14 c128), device rows and host rows
 J2 = O.gen_homogeneous(sorted(rng.choice(20, size=15, replace=False).tolist()), 20, 5)
 f2 = torch.randn(2, 1 << 20, dtype=torch.complex64, device="cuda")
 S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J2))
+S.hidft_to_dft_batched(f2.cpu(), S.SupportSet(1 << 20, J2))
+J3 = np.arange(1 << 16, dtype=np.int64) * 4 + 1
+S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J3))
+J4 = np.arange(1 << 14, dtype=np.int64) * 8 + 3
+S.hidft(f2[0].to(torch.complex128), S.SupportSet(1 << 20, J4), S.pivots(S.SupportSet(1 << 20, J4)), shift=9)
+# host paths: shared support, per-signal supports, SAS staging
+S.hidft_to_dft_batched(f.cpu(), Js)
+S.hidft_to_dft_batched(f.cpu(), torch.from_numpy(sup))
 # SAS mu* > 1 with escalation, band-limited source
 H = O.gen_homogeneous((0, 2, 3, 5, 7, 9, 10), 14, 4)
 Jsub = np.sort(H[rng.choice(H.size, size=40, replace=False)])
 Jb = S.SupportSet(1 << 14, Jsub)
 c = rng.normal(size=40) + 1j * rng.normal(size=40)
 S.sas_transform(S.BandlimitedSignal(Jb, c), Jb, policy="random_subset", family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
+fb = S.BandlimitedSignal(Jb, c).synthesize()
+fb = fb.cpu().numpy() if hasattr(fb, "cpu") else np.asarray(fb)
+S.sas_transform(np.stack([fb, fb]), Jb, policy="random_subset", family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
+S.sas_transform(torch.from_numpy(np.stack([fb, fb])).cuda(), Jb, policy="random_subset",
+                family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
 torch.cuda.synchronize()
 print("sanitize case ok")
