@@ -496,6 +496,66 @@ __global__ void k_split_tables(const Cx<T>* __restrict__ tw, const int32_t* __re
   }
 }
 
+// Three-pass split (sfft_split.cu, k_tri_*).  Slot a = (b << (s-4)) | q: the
+// final pass runs the last 4 stages (pairing b's bits) for a fixed q, so its
+// 16 results land at inv[(b << (s-4)) | q].  When the top 4 pivots are the top
+// 4 bits of j (config 5), j = b*2^(M-4) + h(q) and the output position is
+// b*2^(s-4) + sigma(q): ordering q by its mean output position (the key
+// below) makes every final-pass store run contiguous.  Other supports get the
+// same ordering as a heuristic (correctness never depends on it).
+__global__ void k_tri_key(const int32_t* __restrict__ inv, int s, int64_t n_out, double* __restrict__ key) {
+  const int sq = s - 4;
+  const int64_t nq = 1ll << sq;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double per_b = (double)n_out / 16.0;
+  double sum = 0.0;
+  int cnt = 0;
+  for (int b = 0; b < 16; ++b) {
+    const int32_t v = inv[((int64_t)b << sq) | q];
+    if (v >= 0) {
+      sum += (double)v - b * per_b;
+      ++cnt;
+    }
+  }
+  key[q] = cnt ? sum / cnt : 1e18 + (double)q;
+}
+
+// perm[rank(q)] = q, rank by (key, q): O(nq^2) compares, nq <= 8192
+__global__ void k_tri_rank(const double* __restrict__ key, int64_t nq, int32_t* __restrict__ perm) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double kq = key[q];
+  int64_t rank = 0;
+  for (int64_t i = 0; i < nq; ++i) {
+    const double ki = __ldg(key + i);
+    rank += (ki < kq) || (ki == kq && i < q);
+  }
+  perm[rank] = (int32_t)q;
+}
+
+// Final-pass tables in pi order: stage s-4+t (t < 4) pairs slot bit s-4+t
+// with twiddle index a mod 2^(s-4+t) = q | (c << (s-4)), c = b mod 2^t
+// (hidft.py:160-167); j = 2^t - 1 + c.
+template <typename T>
+__global__ void k_tri_tables(const Cx<T>* __restrict__ tw, const int32_t* __restrict__ inv_elem,
+                             const int32_t* __restrict__ inv_node, const int32_t* __restrict__ perm, int s,
+                             Cx<T>* __restrict__ tw_fin, int32_t* __restrict__ inv_elem_fin,
+                             int32_t* __restrict__ inv_node_fin) {
+  const int sq = s - 4;
+  const int64_t nq = 1ll << sq;
+  const int64_t pi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (pi >= nq) return;
+  const int64_t q = perm[pi];
+  for (int b = 0; b < 16; ++b) {
+    inv_elem_fin[b * nq + pi] = inv_elem[((int64_t)b << sq) | q];
+    inv_node_fin[b * nq + pi] = inv_node[((int64_t)b << sq) | q];
+  }
+  for (int t = 0; t < 4; ++t)
+    for (int c = 0; c < (1 << t); ++c)
+      tw_fin[((1 << t) - 1 + c) * nq + pi] = tw[((int64_t)1 << (sq + t)) - 1 + (q | ((int64_t)c << sq))];
+}
+
 static void plan_free(sfft_plan* p) {
   if (!p) return;
   cudaFree(p->d_element_slots);
@@ -514,6 +574,10 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_tw_blk);
   cudaFree(p->d_inv_elem_blk);
   cudaFree(p->d_inv_node_blk);
+  cudaFree(p->d_tri_perm);
+  cudaFree(p->d_tri_tw);
+  cudaFree(p->d_tri_inv_elem);
+  cudaFree(p->d_tri_inv_node);
   cudaFree(p->d_J);
   delete p;
 }
@@ -640,8 +704,32 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
       k_split_tables<double><<<grid_1d(A), 256, 0, st>>>((const Cx<double>*)p->d_twiddles, p->d_inv_elem,
                                                          p->d_inv_node, s, lc, (Cx<double>*)p->d_tw_blk,
                                                          p->d_inv_elem_blk, p->d_inv_node_blk);
+    // three-pass tables (k_tri_*)
+    const int64_t nq = A >> 4;
+    M_((void**)&p->d_tri_perm, 4 * nq);
+    M_(&p->d_tri_tw, csz * 15 * nq);
+    M_((void**)&p->d_tri_inv_elem, 4 * A);
+    M_((void**)&p->d_tri_inv_node, 4 * A);
+    DevBuf key;
+    if (e != cudaSuccess) return done(cuda_fail(e, "split table allocation"));
+    if ((rc = alloc(key, 8 * nq, st))) return done(rc);
+    k_tri_key<<<grid_1d(nq), 256, 0, st>>>(p->homogeneous ? p->d_inv_elem : p->d_inv_node, s,
+                                            p->homogeneous ? k : std::min<int64_t>(A, k), (double*)key.p);
+    k_tri_rank<<<grid_1d(nq), 256, 0, st>>>((const double*)key.p, nq, p->d_tri_perm);
+    if (dtype == SFFT_C64)
+      k_tri_tables<float><<<grid_1d(nq), 256, 0, st>>>((const Cx<float>*)p->d_twiddles, p->d_inv_elem,
+                                                        p->d_inv_node, p->d_tri_perm, s, (Cx<float>*)p->d_tri_tw,
+                                                        p->d_tri_inv_elem, p->d_tri_inv_node);
+    else
+      k_tri_tables<double><<<grid_1d(nq), 256, 0, st>>>((const Cx<double>*)p->d_twiddles, p->d_inv_elem,
+                                                         p->d_inv_node, p->d_tri_perm, s,
+                                                         (Cx<double>*)p->d_tri_tw, p->d_tri_inv_elem,
+                                                         p->d_tri_inv_node);
   }
   unsigned long long h[2];
+  if (p->d_tri_perm && cudaMemcpyAsync(p->tri_front_tw, p->d_twiddles, csz * std::min<int64_t>(15, A - 1),
+                                       cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return done(cuda_fail(cudaGetLastError(), "plan build"));
   if (cudaGetLastError() != cudaSuccess ||
       cudaMemcpyAsync(h, stats.p, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)

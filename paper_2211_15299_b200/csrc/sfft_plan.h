@@ -30,6 +30,13 @@ struct sfft_plan {
   void* d_tw_blk;            // 2^lc x (2^(s-lc) - 1) twiddles of the local stages, per block, stage-major
   int32_t* d_inv_elem_blk;   // A   d_inv_elem, block-major: [t][l] = inv_elem[(l << lc) | brev_lc(t)]
   int32_t* d_inv_node_blk;   // A   d_inv_node, block-major
+  // three-pass split (sfft_split.cu, k_tri_*): slot = (b << (s-4)) | q; the
+  // final pass owns the q of one position pi = rank of q in d_tri_perm order
+  int32_t* d_tri_perm;       // 2^(s-4)  pi -> q, sorted by mean output position
+  void* d_tri_tw;            // 15 x 2^(s-4) twiddles of the last 4 stages, [j][pi]
+  int32_t* d_tri_inv_elem;   // 16 x 2^(s-4)  [b][pi] = d_inv_elem[(b << (s-4)) | perm[pi]]
+  int32_t* d_tri_inv_node;   // 16 x 2^(s-4)  same for d_inv_node
+  unsigned char tri_front_tw[16 * 15];  // host copy of twiddles 0..14 (stages 1..4), plan dtype
   // per-signal supports (sfft_plan_batched): tables derived on chip per signal
   int per_signal;
   int64_t n_supports;

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -229,6 +230,380 @@ k_split_back(const PlanArgs args, const Cx<T>* __restrict__ scratch, int64_t row
   }
 }
 
+// ------------------------------------------ three-pass split (tri) ---
+//
+// The two-pass back block holds fixed LOW slot bits, but the ascending-J
+// output follows the TOP slot bits, so its stores scatter (~9 line requests
+// per 16 results on config 5).  Three passes put the last stages in a pass
+// whose unit varies only the top 4 slot bits:
+//
+//  slot a = (b << (S-4)) | (m << F) | x':  x' = low F bits (front), m = MID
+//  bits (middle), b = top 4 bits (final).  Sorted position u holds slot
+//  brev_S(u); the front's partner index x is the top F sorted bits
+//  (x' = brev_F(x)) and its thread position p the low S-F sorted bits
+//  (m = brev_MID(p >> 4), b = brev_4(p & 15)).
+//
+//  front (k_tri_front): loads as k_split_front (coalesced runs of the
+//    pattern), runs stages 1..F in registers, transposes through shared
+//    memory and writes scratch1[row][p & 15][tri_pos(m, x')]: runs of >= 16
+//    consecutive values.
+//  middle (k_tri_mid): unit (row, b) = the contiguous block
+//    scratch1[row][brev_4(b)] (2^(S-4) values, loaded coalesced straight into
+//    registers in its pass-0 layout); runs stages F+1..S-4 (2^F
+//    independent transforms over m, twiddles staged once per CTA) and writes
+//    scratch2[row][b][pi] with q = perm[pi] (perm: plan->d_tri_perm).
+//  final (k_tri_final): a thread owns one pi for all rows of its CTA: its 15
+//    twiddles and 16 output positions live in registers; per row it reads
+//    scratch2[row][0..15][pi] (coalesced), runs the last 4 stages and stores
+//    value b at inv[(b << (S-4)) | q] -- consecutive pi are consecutive
+//    outputs when the top 4 pivots are the top bits of j.
+// L2-only scratch loads (.cg), last-use loads (.cs) and streaming stores (.cs)
+__device__ __forceinline__ Cx<float> ld_cg(const Cx<float>* p) {
+  Cx<float> r;
+  asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Cx<double> ld_cg(const Cx<double>* p) {
+  Cx<double> r;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Cx<float> ld_cs(const Cx<float>* p) {
+  Cx<float> r;
+  asm volatile("ld.global.cs.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Cx<double> ld_cs(const Cx<double>* p) {
+  Cx<double> r;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_cs(Cx<float>* p, Cx<float> v) {
+  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cs(Cx<double>* p, Cx<double> v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+// streaming store of v at base[i] when i >= 0 (predicated, no branch)
+__device__ __forceinline__ void st_cs_if(Cx<float>* base, int32_t i, Cx<float> v) {
+  asm volatile("{ .reg .pred q; setp.ge.s32 q, %1, 0; @q st.global.cs.v2.f32 [%0], {%2, %3}; }"
+               :: "l"(base + i), "r"(i), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cs_if(Cx<double>* base, int32_t i, Cx<double> v) {
+  asm volatile("{ .reg .pred q; setp.ge.s32 q, %1, 0; @q st.global.cs.v2.f64 [%0], {%2, %3}; }"
+               :: "l"(base + i), "r"(i), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* sdst, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(sdst)), "l"(g) : "memory");
+}
+
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; griddepcontrol.wait blocks until the predecessor has
+// completed and its writes are visible.  Each tri kernel reads only
+// read-only inputs (signals, plan tables) before the wait and releases its
+// dependents only after it, so by induction every earlier kernel in the
+// stream has completed once a kernel passes its wait.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+#ifndef SFFT_TRI_PF  // front: units prefetched into L2 beyond the one in registers
+#define SFFT_TRI_PF 1
+#endif
+#ifndef SFFT_TRI_FRONT_MINB
+#define SFFT_TRI_FRONT_MINB 2
+#endif
+template <typename T, int S, int F>
+struct TriGeo {
+  static constexpr int L = 4, EXL = 1 << L;   // final: top L slot bits
+  static constexpr int MID = S - F - L;        // middle: slot bits [F, F + MID)
+  static constexpr int SQ = S - L, NQ = 1 << SQ;
+  static constexpr int EX = 1 << F;
+  // front
+  static constexpr int SP = S - F, NT1 = 256, NSEG = (1 << SP) / NT1, NH = NT1 >> L;
+  static constexpr size_t SMEM1 = (size_t)EX * EXL * NH * sizeof(Cx<T>);
+  // middle
+  static constexpr int E2 = EMax<T>::v < (1 << MID) ? EMax<T>::v : (1 << MID);
+  static constexpr int LE2 = ilog2c(E2), NT2 = NQ / E2;
+  static constexpr int NPASS2 = (MID + LE2 - 1) / LE2;
+  static constexpr int NTW2 = NQ - EX;  // stage-major twiddles of stages F+1 .. S-L
+  static constexpr size_t SMEM2 = (size_t)NQ * sizeof(Cx<T>) + (size_t)NTW2 * sizeof(Cx<T>) + (size_t)NQ * 4;
+  // final
+  static constexpr int NT3 = 128, NQB = NQ / NT3;
+#ifndef SFFT_TRI_FINAL_MINB
+#define SFFT_TRI_FINAL_MINB 5
+#endif
+  static constexpr int MINB3 = sizeof(T) == 4 ? SFFT_TRI_FINAL_MINB : 3;
+  static_assert(MID >= LE2 && NT1 % EXL == 0 && NQ % NT3 == 0, "tri geometry");
+};
+
+// Position of local slot l = (m << F) | x' inside a middle block: the middle
+// pass-0 register bits (m mod E2) on top, so thread tid = ((m >> LE2) << F) | x'
+// loads register x from position x * NT2 + tid (coalesced, straight into
+// registers).
+template <typename T, int S, int F>
+__device__ __forceinline__ int tri_pos(int m, int xa) {
+  using TG = TriGeo<T, S, F>;
+  return ((m & (TG::E2 - 1)) << (TG::SQ - TG::LE2)) | ((m >> TG::LE2) << F) | xa;
+}
+
+// Front: one CTA per (row, 256 consecutive sorted positions p).  After its
+// F stages a thread holds the values of slots (brev_MID(p >> 4) << F |
+// brev_F(x)) of middle block p & 15 for all x; the CTA's values of one block
+// form runs of >= 16 consecutive positions, written through a staging area
+// [p & 15][x][p >> 4 (local)] whose column is XOR-swizzled by (p & 15) ^ x
+// (conflict-free for both the per-x writes and the per-block reads).
+// twiddles of stages 1..F, passed by value: uniform over the grid, so the
+// butterflies take them straight from the constant bank
+template <typename T> struct FrontTw { Cx<T> w[15]; };
+
+template <typename T, int S, int F>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? SFFT_TRI_FRONT_MINB : 1) k_tri_front(const PlanArgs args, const FrontTw<T> ftw,
+                                                                        Cx<T>* __restrict__ scratch, int64_t row0,
+                                                                        int64_t nrows) {
+  using TG = TriGeo<T, S, F>;
+  constexpr int SP = TG::SP, EX = TG::EX, L = TG::L, EXL = TG::EXL, NH = TG::NH, MID = TG::MID, SQ = TG::SQ;
+  static_assert(NH == 16, "front staging assumes 16 local p_hi values");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* st = reinterpret_cast<Cx<T>*>(smem_raw);
+  // slot bit i -> sample stride (hidft.py:155-158), or the pre-gathered layouts
+  auto dstride = [&](int i) -> uint32_t {
+    return args.identity == 1   ? (1u << i)
+           : args.identity == 2 ? (1u << (S - 1 - i))
+                                : (1u << (args.M - 1 - args.used[i]));
+  };
+  const uint32_t nmask = args.identity ? (uint32_t)((1u << S) - 1u)
+                                       : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
+  const int64_t units = nrows * TG::NSEG;
+  // sorted bit j <-> slot bit S-1-j: the thread's low 8 position bits are
+  // fixed, the CTA-uniform high bits change per unit, partners x add slot
+  // bits 0..F-1
+  constexpr int TB = 8;  // log2(NT1)
+  uint32_t off_t = 0;
+#pragma unroll
+  for (int j = 0; j < TB; ++j)
+    if ((threadIdx.x >> j) & 1u) off_t += dstride(S - 1 - j);
+  uint32_t dx[F];
+#pragma unroll
+  for (int j = 0; j < F; ++j) dx[j] = dstride(F - 1 - j);
+  Cx<T> nx[EX];
+  // sample address of partner x of unit u (pf: L2 prefetch instead of a load)
+  auto unit_off = [&](int64_t u, int64_t& base) {
+    const int64_t r = row0 + u / TG::NSEG;
+    const uint32_t p0 = (uint32_t)(u % TG::NSEG) * TG::NT1;
+#ifdef SFFT_TRI_FOOTPRINT  // timing probe only: every row reads one of two signals
+    base = (r & 1) * args.ld;
+#else
+    base = (r / args.nshift) * args.ld;
+#endif
+    uint32_t off = off_t + (args.identity ? 0u : ((args.negshift - (uint32_t)(r % args.nshift)) & nmask));
+    for (int j = TB; j < SP; ++j)
+      if ((p0 >> j) & 1u) off += dstride(S - 1 - j);
+    return off;
+  };
+  auto fetch = [&](int64_t u) {
+    int64_t base;
+    const uint32_t off = unit_off(u, base);
+#pragma unroll
+    for (int x = 0; x < EX; ++x) {
+      uint32_t o = off;
+#pragma unroll
+      for (int j = 0; j < F; ++j)
+        if ((x >> j) & 1) o += dx[j];
+      if (sizeof(T) == 8 && args.in_c64) {
+        const Cx<float> sv = load_sample(reinterpret_cast<const Cx<float>*>(args.sig) + base + (o & nmask));
+        nx[x] = Cx<T>{(T)sv.x, (T)sv.y};
+      } else {
+        nx[x] = load_sample(reinterpret_cast<const Cx<T>*>(args.sig) + base + (o & nmask));
+      }
+    }
+  };
+  auto prefetch = [&](int64_t u) {
+    int64_t base;
+    const uint32_t off = unit_off(u, base);
+    const size_t esz_in = (sizeof(T) == 8 && args.in_c64) ? sizeof(Cx<float>) : sizeof(Cx<T>);
+    const char* sig = reinterpret_cast<const char*>(args.sig);
+#pragma unroll
+    for (int x = 0; x < EX; ++x) {
+      uint32_t o = off;
+#pragma unroll
+      for (int j = 0; j < F; ++j)
+        if ((x >> j) & 1) o += dx[j];
+      asm volatile("prefetch.global.L2 [%0];" :: "l"(sig + (base + (o & nmask)) * esz_in));
+    }
+  };
+  int64_t u = blockIdx.x;
+  if (u < units) fetch(u);  // signals are read-only here
+#pragma unroll
+  for (int k = 2; k < 2 + SFFT_TRI_PF; ++k)
+    if (u + k * gridDim.x < units) prefetch(u + k * gridDim.x);
+  pdl_wait();               // scratch1 is free (the previous chunk's middle pass completed)
+  pdl_release();
+  for (; u < units; u += gridDim.x) {
+    Cx<T> v[EX];
+#pragma unroll
+    for (int x = 0; x < EX; ++x) v[x] = nx[x];
+    if (u + gridDim.x < units) fetch(u + gridDim.x);
+    if (SFFT_TRI_PF > 0 && u + (1 + SFFT_TRI_PF) * gridDim.x < units) prefetch(u + (1 + SFFT_TRI_PF) * gridDim.x);
+#pragma unroll
+    for (int k = 1; k <= F; ++k) {  // stage k pairs slot bit k-1 = x bit F-k (hidft.py:160-167)
+      const int lb = F - k;
+#pragma unroll
+      for (int x = 0; x < EX; ++x) {
+        if (x & (1 << lb)) continue;
+        const uint32_t h = brev_c<F>((uint32_t)x) & ((1u << (k - 1)) - 1u);
+        bfly(v[x], v[x | (1 << lb)], ftw.w[(1 << (k - 1)) - 1 + h]);
+      }
+    }
+    {
+      const int lo = threadIdx.x & (EXL - 1), hl = threadIdx.x >> L;
+#pragma unroll
+      for (int x = 0; x < EX; ++x) st[(lo * EX + x) * NH + (hl ^ ((lo ^ x) & (NH - 1)))] = v[x];
+    }
+    __syncthreads();
+    // block lo gets slots m = brev_MID(ph0 + hl) = m0 | brev_4(hl) << (MID - 4)
+    const uint32_t p0 = (uint32_t)(u % TG::NSEG) * TG::NT1;
+    const uint32_t m0 = brev_c<MID>(p0 >> L);
+    Cx<T>* rowbase = scratch + ((u / TG::NSEG) << S);
+#pragma unroll
+    for (int n = 0; n < EX; ++n) {
+      const int id = n * TG::NT1 + threadIdx.x;
+      const int xa = id & (EX - 1), hb = (id >> F) & (NH - 1), lo = id >> (F + 4);
+      const int hl = (int)brev_c<4>((uint32_t)hb), x = (int)brev_c<F>((uint32_t)xa);
+      const int m = (int)(m0 | ((uint32_t)hb << (MID - 4)));
+      rowbase[((int64_t)lo << SQ) + tri_pos<T, S, F>(m, xa)] = st[(lo * EX + x) * NH + (hl ^ ((lo ^ x) & (NH - 1)))];
+    }
+    __syncthreads();  // st is rewritten by the next unit
+  }
+}
+
+// Middle: persistent over units (row, b); the next unit's block is loaded into
+// registers (pass-0 layout) while this one runs.
+template <typename T, int S, int F>
+__global__ void __launch_bounds__(TriGeo<T, S, F>::NT2) k_tri_mid(const Cx<T>* __restrict__ scr1,
+                                                                  Cx<T>* __restrict__ scr2, int64_t nrows,
+                                                                  const Cx<T>* __restrict__ tw,
+                                                                  const int32_t* __restrict__ perm) {
+  using TG = TriGeo<T, S, F>;
+  constexpr int EX = TG::EX, MID = TG::MID, NQ = TG::NQ, SQ = TG::SQ, L = TG::L, E = TG::E2, LE = TG::LE2,
+                NT = TG::NT2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* sd = reinterpret_cast<Cx<T>*>(smem_raw);  // NQ, swizzled local slot l = (m << F) | x'
+  Cx<T>* stw = sd + NQ;                             // stage-major twiddles of stages F+1 .. S-L
+  int32_t* sperm = reinterpret_cast<int32_t*>(stw + TG::NTW2);
+  const int tid = threadIdx.x;
+  // tables staged asynchronously (cp.async) while the first unit's block loads
+  for (int i = tid; i < TG::NTW2; i += NT) cp_async_elem(stw + i, tw + EX - 1 + i);
+  for (int i = tid; i < NQ / 4; i += NT) cp_async16(sperm + 4 * i, perm + 4 * i);
+  cp_async_commit();
+  const int a = tid & (EX - 1), mr = tid >> F;
+  const int64_t units = nrows << L;
+  Cx<T> nx[E];
+  auto fetch = [&](int64_t u) {
+    const Cx<T>* src = scr1 + ((u >> L) << S) + ((int64_t)brev_c<L>((uint32_t)(u & (TG::EXL - 1))) << SQ) + tid;
+#pragma unroll
+    for (int x = 0; x < E; ++x) nx[x] = ld_cg(src + x * NT);
+  };
+  int64_t u = blockIdx.x;
+  pdl_wait();  // scratch1 written by this chunk's front pass
+  pdl_release();
+  if (u < units) fetch(u);
+  cp_async_wait<0>();
+  __syncthreads();  // staged tables
+  for (; u < units; u += gridDim.x) {
+    Cx<T> v[E];
+#pragma unroll
+    for (int x = 0; x < E; ++x) v[x] = nx[x];
+    if (u + gridDim.x < units) fetch(u + gridDim.x);
+#pragma unroll
+    for (int ps = 0; ps < TG::NPASS2; ++ps) {
+      const int w0 = pass_w0(ps, MID, LE);
+      if (ps > 0) {
+#pragma unroll
+        for (int x = 0; x < E; ++x) v[x] = sd[swz<T, SQ>((slot_of<MID, LE>(ps, mr, x) << F) | a)];
+      }
+      const int b0 = ps * LE, b1 = (b0 + LE < MID) ? b0 + LE : MID;
+#pragma unroll
+      for (int beta = b0; beta < b1; ++beta) {  // global stage F + beta + 1 pairs m bit beta
+        const int lb = beta - w0;
+#pragma unroll
+        for (int x = 0; x < E; ++x) {
+          if (x & (1 << lb)) continue;
+          const int m = slot_of<MID, LE>(ps, mr, x);
+          const int h = a | ((m & ((1 << beta) - 1)) << F);
+          bfly(v[x], v[x | (1 << lb)], stw[(1 << (F + beta)) - EX + h]);
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < E; ++x) sd[swz<T, SQ>((slot_of<MID, LE>(ps, mr, x) << F) | a)] = v[x];
+      __syncthreads();
+    }
+    Cx<T>* dst = scr2 + ((u >> L) << S) + ((u & (TG::EXL - 1)) << SQ);
+#pragma unroll
+    for (int n = 0; n < E; ++n) {
+      const int pi = tid + n * NT;
+      dst[pi] = sd[swz<T, SQ>(sperm[pi])];
+    }
+    __syncthreads();  // sd is rewritten by the next unit
+  }
+}
+
+// Final: a thread owns position pi for the rows of its CTA (twiddles and
+// output positions in registers); the next row is prefetched.
+template <typename T, int S, int F>
+__global__ void __launch_bounds__(TriGeo<T, S, F>::NT3, TriGeo<T, S, F>::MINB3) k_tri_final(const PlanArgs args, const Cx<T>* __restrict__ scr2,
+                                                                    int64_t row0, int64_t nrows, int nper,
+                                                                    const Cx<T>* __restrict__ twf,
+                                                                    const int32_t* __restrict__ invf,
+                                                                    const int32_t* __restrict__ perm) {
+  using TG = TriGeo<T, S, F>;
+  constexpr int NQ = TG::NQ, SQ = TG::SQ, EXL = TG::EXL, L = TG::L;
+  __shared__ Cx<T> sw[EXL - 1][TG::NT3];  // this CTA's pi block: twiddles of the last L stages
+  const int qb = blockIdx.x % TG::NQB;
+  const int64_t first = blockIdx.x / TG::NQB;
+  if (first >= nrows) return;
+  const int pi = qb * TG::NT3 + threadIdx.x;
+  Cx<T> nx[EXL];
+  auto fetch = [&](int64_t rr) {
+    const Cx<T>* src = scr2 + (rr << S) + pi;
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) nx[b] = ld_cs(src + ((int64_t)b << SQ));
+  };
+  const int q = perm[pi];
+#pragma unroll
+  for (int j = 0; j < EXL - 1; ++j) sw[j][threadIdx.x] = twf[(int64_t)j * NQ + pi];  // read by this thread only
+  int32_t e[EXL];
+#pragma unroll
+  for (int b = 0; b < EXL; ++b) e[b] = invf ? invf[(int64_t)b * NQ + pi] : ((b << SQ) | q);
+  pdl_wait();  // scratch2 written by this chunk's middle pass
+  pdl_release();
+  fetch(first);
+  const T scale = (T)args.scale1;
+  for (int64_t rr = first; rr < nrows; rr += nper) {
+    Cx<T> v[EXL];
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) v[b] = nx[b];
+    if (rr + nper < nrows) fetch(rr + nper);
+#pragma unroll
+    for (int t = 0; t < L; ++t) {  // global stage SQ + t + 1 pairs slot bit SQ + t = b bit t
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) {
+        if (b & (1 << t)) continue;
+        bfly(v[b], v[b | (1 << t)], sw[(1 << t) - 1 + (b & ((1 << t) - 1))][threadIdx.x]);
+      }
+    }
+    const int64_t r = row0 + rr;
+    Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + r * args.ld1;
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) st_cs_if(o1, e[b], cscale(v[b], scale));
+    if (args.out2) {
+      Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + r * args.ld2;
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) o2[(b << SQ) | q] = v[b];
+    }
+  }
+}
+
 // stream-ordered scratch from a library-owned pool that keeps its memory
 static int scratch_pool(int dev, cudaMemPool_t* pool) {
   static std::mutex mu;
@@ -317,7 +692,124 @@ static int run_split(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1,
   return SFFT_OK;
 }
 
+// cudaLaunchKernelEx, optionally as a programmatic dependent launch
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                            bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+// rows per chunk of the three-pass split: each of the two scratch buffers
+// up to SFFT_TRI_SCRATCH_MB (default 32 MiB) so both stay in L2
+static int64_t tri_chunk_rows(int64_t rows, size_t row_bytes) {
+  static const int64_t scr_mb = [] {
+    const char* e = getenv("SFFT_TRI_SCRATCH_MB");
+    return (int64_t)(e ? std::max(1, atoi(e)) : 32);
+  }();
+  return std::max<int64_t>(1, std::min<int64_t>(rows, (scr_mb << 20) / (int64_t)row_bytes));
+}
+
+template <typename T, int S, int F>
+static int tri_launches(int64_t rows, int64_t* n) {
+  const int64_t chunk = tri_chunk_rows(rows, sizeof(Cx<T>) << S);
+  *n = rows > 0 ? 3 * ((rows + chunk - 1) / chunk) : 0;
+  return SFFT_OK;
+}
+
+template <typename T, int S, int F>
+static int run_tri(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
+  using TG = TriGeo<T, S, F>;
+  if (!p->d_tri_perm) return fail(SFFT_ERR_INVALID, "plan has no three-pass tables");
+  const int32_t* invf = inv1 == p->d_inv_elem ? p->d_tri_inv_elem
+                        : inv1 == p->d_inv_node ? p->d_tri_inv_node
+                                                : nullptr;
+  if (inv1 && !invf) return fail(SFFT_ERR_INVALID, "no final-pass map for this output");
+  auto front = k_tri_front<T, S, F>;
+  auto mid = k_tri_mid<T, S, F>;
+  auto fin = k_tri_final<T, S, F>;
+  int occ1 = 0, occ2 = 0, occ3 = 0, rc;
+  if ((rc = kernel_occupancy(front, TG::NT1, TG::SMEM1, &occ1))) return rc;
+  if ((rc = kernel_occupancy(mid, TG::NT2, TG::SMEM2, &occ2))) return rc;
+  if ((rc = kernel_occupancy(fin, TG::NT3, 0, &occ3))) return rc;
+  const int64_t rows = a.B * a.nshift;
+  if (rows == 0) return SFFT_OK;
+  const size_t row_bytes = sizeof(Cx<T>) << S;
+  const int64_t chunk = tri_chunk_rows(rows, row_bytes);
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  if ((rc = scratch_pool(dev, &pool))) return rc;
+  void* scr = nullptr;
+  SFFT_CUDA(cudaMallocFromPoolAsync(&scr, 2 * (size_t)chunk * row_bytes, pool, st));
+  Cx<T>* s1 = (Cx<T>*)scr;
+  Cx<T>* s2 = s1 + ((size_t)chunk << S);
+  const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(p->d_twiddles);
+  const Cx<T>* twf = reinterpret_cast<const Cx<T>*>(p->d_tri_tw);
+  const int64_t sms = num_sms();
+  FrontTw<T> ftw;
+  std::memcpy(&ftw, p->tri_front_tw, sizeof(Cx<T>) * std::min<int64_t>(15, p->A - 1));
+  static const bool pdl = [] {
+    const char* e = getenv("SFFT_TRI_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  cudaError_t e = cudaSuccess;
+  for (int64_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += chunk) {
+    const int64_t n = std::min(chunk, rows - r0);
+    // the call's first kernel is stream-ordered (its pre-wait loads read the signals)
+    const int64_t g1 = std::min<int64_t>(n * TG::NSEG, sms * occ1);
+    e = launch_k(front, (unsigned)g1, TG::NT1, TG::SMEM1, st, pdl && r0 > 0, a, ftw, s1, r0, n);
+    const int64_t g2 = std::min<int64_t>(n << TG::L, sms * occ2);
+    if (e == cudaSuccess)
+      e = launch_k(mid, (unsigned)g2, TG::NT2, TG::SMEM2, st, pdl, (const Cx<T>*)s1, s2, n, tw,
+                   (const int32_t*)p->d_tri_perm);
+    const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / TG::NQB));
+    if (e == cudaSuccess)
+      e = launch_k(fin, (unsigned)(nper * TG::NQB), TG::NT3, 0, st, pdl, a, (const Cx<T>*)s2, r0, n, nper, twf,
+                   invf, (const int32_t*)p->d_tri_perm);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  cudaFreeAsync(scr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "three-pass transform launch");
+  return SFFT_OK;
+}
+
+// SFFT_SPLIT_PASSES=2 selects the two-pass split (A/B measurements)
+static bool use_tri() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_SPLIT_PASSES");
+    return !(e && atoi(e) == 2);
+  }();
+  return v;
+}
+
 int run_large(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
+  if (use_tri()) {
+    if (p->dtype == SFFT_C64) {
+      switch (p->s) {
+        case 15: return run_tri<float, 15, 3>(p, a, inv1, st);
+        case 16: return run_tri<float, 16, 4>(p, a, inv1, st);
+        case 17: return run_tri<float, 17, 4>(p, a, inv1, st);
+        default: break;
+      }
+    } else {
+      switch (p->s) {
+        case 14: return run_tri<double, 14, 2>(p, a, inv1, st);
+        case 15: return run_tri<double, 15, 3>(p, a, inv1, st);
+        case 16: return run_tri<double, 16, 4>(p, a, inv1, st);
+        default: break;
+      }
+    }
+  }
   if (p->dtype == SFFT_C64) {
     switch (p->s) {
       case 15: return run_split<float, 15, 3>(p, a, inv1, st);
@@ -337,6 +829,23 @@ int run_large(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaSt
 }
 
 int large_launch_count(const sfft_plan* p, int64_t rows, int64_t* launches) {
+  if (use_tri()) {
+    if (p->dtype == SFFT_C64) {
+      switch (p->s) {
+        case 15: return tri_launches<float, 15, 3>(rows, launches);
+        case 16: return tri_launches<float, 16, 4>(rows, launches);
+        case 17: return tri_launches<float, 17, 4>(rows, launches);
+        default: break;
+      }
+    } else {
+      switch (p->s) {
+        case 14: return tri_launches<double, 14, 2>(rows, launches);
+        case 15: return tri_launches<double, 15, 3>(rows, launches);
+        case 16: return tri_launches<double, 16, 4>(rows, launches);
+        default: break;
+      }
+    }
+  }
   if (p->dtype == SFFT_C64) {
     switch (p->s) {
       case 15: return split_launches<float, 15, 3>(rows, launches);
