@@ -50,8 +50,10 @@ k_hidft_plan(const PlanArgs args) {
                                         : ((args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u));
   Cx<T> v[G::E];
   if (live) {
-    const int64_t bs = b / args.nshift;
-    const uint32_t base = args.identity ? 0u : ((args.negshift - (uint32_t)(b % args.nshift)) & nmask);
+    // one row per signal (nshift == 1) skips the 64-bit division on the gather's critical path
+    const int64_t bs = args.nshift == 1 ? b : b / args.nshift;
+    const uint32_t rsh = args.nshift == 1 ? 0u : (uint32_t)(b % args.nshift);
+    const uint32_t base = args.identity ? 0u : ((args.negshift - rsh) & nmask);
     if (sizeof(T) == 8 && args.in_c64)
       gather<T, S, float>(v, t, reinterpret_cast<const Cx<float>*>(args.sig) + bs * args.ld, d, base, nmask);
     else
@@ -65,9 +67,17 @@ k_hidft_plan(const PlanArgs args) {
   if (live) {
     const T scale = (T)args.scale1;
     Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
-    for (int64_t i = t; i < args.n1; i += G::TPS) {
-      const int a = args.map1 ? __ldg(args.map1 + i) : (int)i;
-      o1[i] = cscale(sd[swz<T, S>(a)], scale);
+    if (args.n1 == G::A && args.map1) {  // one output per slot (homogeneous DFT order): unrolled, loads batched
+      int a[G::E];
+#pragma unroll
+      for (int j = 0; j < G::E; ++j) a[j] = __ldg(args.map1 + t + j * G::TPS);
+#pragma unroll
+      for (int j = 0; j < G::E; ++j) o1[t + j * G::TPS] = cscale(sd[swz<T, S>(a[j])], scale);
+    } else {
+      for (int64_t i = t; i < args.n1; i += G::TPS) {
+        const int a = args.map1 ? __ldg(args.map1 + i) : (int)i;
+        o1[i] = cscale(sd[swz<T, S>(a)], scale);
+      }
     }
     if (args.out2) {
       Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + b * args.ld2;

@@ -394,9 +394,10 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? SFFT_TRI_FRONT_MINB : 1)
 #ifdef SFFT_TRI_FOOTPRINT  // timing probe only: every row reads one of two signals
     base = (r & 1) * args.ld;
 #else
-    base = (r / args.nshift) * args.ld;
+    base = (args.nshift == 1 ? r : r / args.nshift) * args.ld;
 #endif
-    uint32_t off = off_t + (args.identity ? 0u : ((args.negshift - (uint32_t)(r % args.nshift)) & nmask));
+    const uint32_t rsh = args.nshift == 1 ? 0u : (uint32_t)(r % args.nshift);
+    uint32_t off = off_t + (args.identity ? 0u : ((args.negshift - rsh) & nmask));
     for (int j = TB; j < SP; ++j)
       if ((p0 >> j) & 1u) off += dstride(S - 1 - j);
     return off;
