@@ -307,8 +307,10 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* g) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-#ifndef SFFT_TRI_PF  // front: units prefetched into L2 beyond the one in registers
-#define SFFT_TRI_PF 1
+#ifndef SFFT_TRI_PF  // front: units prefetched into L2 beyond the one in registers (config 5: 0 -> 145 us, 1 -> 153 us;
+                     // loading the next unit after this one's stages instead of before, at
+                     // 2 / 3 / 4 CTAs per SM: 149 / 153 / 161 us)
+#define SFFT_TRI_PF 0
 #endif
 #ifndef SFFT_TRI_FRONT_MINB
 #define SFFT_TRI_FRONT_MINB 2

@@ -684,3 +684,43 @@ def test_plan_tables_at_config_size(S, cfg):
     tw = np.concatenate(o.twiddles)
     assert np.max(np.abs(t["twiddles"] - tw)) < 1e-15
     assert np.array_equal(S.pivoted_pattern(r, M).as_array(), O.pivoted_pattern(r, M))
+
+
+_ALT_SPLIT = r"""
+import sys
+import numpy as np
+import torch
+import structfft_oracle as O
+import paper_2211_15299_b200 as S
+ok = True
+for dt, s in [(np.complex64, 16), (np.complex64, 17), (np.complex128, 16), (np.complex128, 14)]:
+    rng = np.random.default_rng(3000 + s)
+    M, B = 22, 3
+    piv = sorted(rng.choice(M, size=s, replace=False).tolist())
+    J = O.gen_homogeneous(piv, M, int(rng.integers(0, 2 ** 62)))
+    coef = rng.normal(size=(B, J.size)) + 1j * rng.normal(size=(B, J.size))
+    f = np.stack([O.synthesize(J, coef[b], M) for b in range(B)]).astype(dt)
+    got = S.hidft_to_dft_batched(torch.from_numpy(f).cuda(), S.SupportSet(1 << M, J)).cpu().numpy()
+    tol = 1e-5 if dt == np.complex64 else 1e-11
+    for b in range(B):
+        want = O.hidft_to_dft(f[b], J, M)
+        err = np.linalg.norm(got[b] - want) / np.linalg.norm(want)
+        print(dt.__name__, s, b, err)
+        ok &= bool(err < tol)
+sys.exit(0 if ok else 1)
+"""
+
+
+@pytest.mark.parametrize("env", [{"SFFT_SPLIT_PASSES": "2"}, {"SFFT_TRI_SCRATCH_MB": "1"}])
+def test_alternate_split_configurations(S, env):
+    """The two-pass split (SFFT_SPLIT_PASSES=2, kept for A/B measurements)
+    and the three-pass split with many small row chunks (a 1 MiB scratch
+    budget: 1-4 rows per chunk, the PDL chain across chunks) against the
+    oracle.  Each runs in a fresh process: the settings are read once."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "oracle")]), **env)
+    out = subprocess.run([sys.executable, "-c", _ALT_SPLIT], env=e, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
