@@ -713,11 +713,12 @@ static cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, 
 }
 
 // rows per chunk of the three-pass split: each of the two scratch buffers
-// up to SFFT_TRI_SCRATCH_MB (default 32 MiB) so both stay in L2
+// up to SFFT_TRI_SCRATCH_MB (default 64 MiB: 2 chunks of 128 rows on config
+// 5; measured 16/24/32/48/64/96/128 MiB -> 166/153/144/141/140/144/146 us)
 static int64_t tri_chunk_rows(int64_t rows, size_t row_bytes) {
   static const int64_t scr_mb = [] {
     const char* e = getenv("SFFT_TRI_SCRATCH_MB");
-    return (int64_t)(e ? std::max(1, atoi(e)) : 32);
+    return (int64_t)(e ? std::max(1, atoi(e)) : 64);
   }();
   return std::max<int64_t>(1, std::min<int64_t>(rows, (scr_mb << 20) / (int64_t)row_bytes));
 }
