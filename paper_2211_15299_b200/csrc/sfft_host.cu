@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <condition_variable>
 #include <cstring>
@@ -81,6 +83,16 @@ class HostPool {
 };
 
 static std::mutex g_host_mu;  // one host job at a time through the shared pool and staging
+
+// SFFT_HOST_TRACE=1: per-call timeline of the host pipeline on stderr (probe only)
+static bool host_trace() {
+  static const bool v = [] { const char* e = getenv("SFFT_HOST_TRACE"); return e && atoi(e) != 0; }();
+  return v;
+}
+static double now_us() {
+  using namespace std::chrono;
+  return duration<double, std::micro>(steady_clock::now().time_since_epoch()).count();
+}
 static HostPool* g_pool = nullptr;
 
 // default: every core but the calling thread's (which gathers too), shared
@@ -188,6 +200,11 @@ struct Staging {
   void* d_J = nullptr;   size_t d_J_n = 0;
   void* d_stat = nullptr; size_t d_stat_n = 0;
   cudaEvent_t h_free = nullptr;
+  // device->host copies run on their own stream so chunk c's result copy
+  // overlaps chunk c+1's host->device copy (the two DMA directions); the
+  // caller's stream waits for it before the call returns
+  cudaStream_t d2h = nullptr;
+  cudaEvent_t ev_k = nullptr, ev_d2h = nullptr;
   int device = -1;
 };
 static Staging g_stage;
@@ -222,13 +239,32 @@ static int stage_begin(int dev) {
     if (S.d_J) cudaFree(S.d_J);
     if (S.d_stat) cudaFree(S.d_stat);
     if (S.h_free) cudaEventDestroy(S.h_free);
+    if (S.d2h) cudaStreamDestroy(S.d2h);
+    if (S.ev_k) cudaEventDestroy(S.ev_k);
+    if (S.ev_d2h) cudaEventDestroy(S.ev_d2h);
     S.d_in = S.d_out = S.d_slot = S.d_J = S.d_stat = nullptr;
     S.d_in_n = S.d_out_n = S.d_slot_n = S.d_J_n = S.d_stat_n = 0;
     S.h_free = nullptr;
+    S.d2h = nullptr;
+    S.ev_k = S.ev_d2h = nullptr;
     S.device = dev;
   }
   if (!S.h_free) SFFT_CUDA(cudaEventCreateWithFlags(&S.h_free, cudaEventDisableTiming));
+  if (!S.ev_k) SFFT_CUDA(cudaEventCreateWithFlags(&S.ev_k, cudaEventDisableTiming));
+  if (!S.ev_d2h) SFFT_CUDA(cudaEventCreateWithFlags(&S.ev_d2h, cudaEventDisableTiming));
+  if (!S.d2h) SFFT_CUDA(cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking));
   return SFFT_OK;
+}
+
+// the result copies of the chunk just enqueued on st go to the D2H stream
+static cudaError_t d2h_after(cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(g_stage.ev_k, st);
+  return e == cudaSuccess ? cudaStreamWaitEvent(g_stage.d2h, g_stage.ev_k, 0) : e;
+}
+// the caller's stream waits for every result copy
+static cudaError_t d2h_join(cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(g_stage.ev_d2h, g_stage.d2h);
+  return e == cudaSuccess ? cudaStreamWaitEvent(st, g_stage.ev_d2h, 0) : e;
 }
 
 static bool is_pinned_host(const void* p) {
@@ -245,15 +281,17 @@ static bool is_pinned_host(const void* p) {
 static std::vector<int64_t> plan_locations(const sfft_plan* p, int64_t shift0, bool pattern_order) {
   const int64_t N = 1ll << p->M, A = p->A;
   const int64_t sh = ((shift0 % N) + N) % N;
-  std::vector<int64_t> loc(A);
-  for (int64_t u = 0; u < A; ++u) {
-    int64_t v = 0;
-    for (int i = 0; i < p->s; ++i) {
-      const int bit = pattern_order ? (int)((u >> (p->s - 1 - i)) & 1) : (int)((u >> i) & 1);
-      v += (int64_t)bit << (p->M - 1 - p->used[i]);
-    }
-    loc[u] = (v - sh + N) & (N - 1);
+  // loc[u] = loc[u without its lowest set bit] + that bit's stride: O(A)
+  // (the per-bit sum was ~1 ms per call at A = 2^16)
+  int64_t d[64];
+  for (int j = 0; j < p->s; ++j) {
+    const int i = pattern_order ? p->s - 1 - j : j;  // index bit j <-> slot bit i
+    d[j] = 1ll << (p->M - 1 - p->used[i]);
   }
+  std::vector<int64_t> loc(A);
+  if (A > 0) loc[0] = 0;
+  for (int64_t u = 1; u < A; ++u) loc[u] = loc[u & (u - 1)] + d[__builtin_ctzll((unsigned long long)u)];
+  for (int64_t u = 0; u < A; ++u) loc[u] = (loc[u] - sh + N) & (N - 1);
   return loc;
 }
 
@@ -310,6 +348,7 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
   // the cluster transform reads pre-gathered rows in pattern order: stage
   // them that way there (coalesced on the device, ascending on the host)
   const bool sorted = gathered_sorted(plan);
+  const double t_call = host_trace() ? now_us() : 0.0;
   const std::vector<int64_t> loc = plan_locations(plan, shift, sorted);
 
   std::lock_guard<std::mutex> lk(g_host_mu);
@@ -369,31 +408,62 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
   HostPool& p = pool(nthreads);
   const std::function<void(int)> fn = [&job](int) { while (job.step()) {} };
   if (use_pool) p.start(&fn);
+  const bool tr = host_trace();
+  const double t0 = tr ? now_us() : 0.0;
+  std::vector<double> tw;
+  std::vector<cudaEvent_t> tev;  // per chunk: before H2D, after H2D, after transform, after D2H
   for (int64_t c = 0; c < job.nchunks() && job.B > 0 && rc == SFFT_OK; ++c) {
     job.await(c);
+    if (tr) tw.push_back(now_us() - t0);
     const int64_t rows = job.chunk_rows(c);
     const int64_t hb = c * job.chunk, b0 = g0 + hb;  // row in the staging / in the batch
     const size_t ib = (size_t)hb * A * esz;
     char* din = (char*)S.d_in + ib;
     char* dout = (char*)S.d_out + (size_t)b0 * n_out * esz;
     char* dslot = slot_out ? (char*)S.d_slot + (size_t)b0 * A * esz : nullptr;
+    if (tr) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), st); }
     cudaError_t e = cudaMemcpyAsync(din, (char*)S.h_in + ib, (size_t)rows * A * esz, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) { rc = cuda_fail(e, "host->device chunk copy"); break; }
+    if (tr) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), st); }
     rc = hidft_gathered(plan, din, rows, A, sorted, out_kind, dout, n_out, dslot, A, st);
     if (rc) break;
-    e = cudaMemcpy2DAsync(out_tgt + (size_t)b0 * ldo_tgt * esz, (size_t)ldo_tgt * esz, dout, (size_t)n_out * esz,
-                          (size_t)n_out * esz, rows, cudaMemcpyDeviceToHost, st);
+    if (tr) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), st); }
+    e = d2h_after(st);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(out_tgt + (size_t)b0 * ldo_tgt * esz, (size_t)ldo_tgt * esz, dout, (size_t)n_out * esz,
+                            (size_t)n_out * esz, rows, cudaMemcpyDeviceToHost, S.d2h);
     if (e == cudaSuccess && slot_out)
       e = cudaMemcpy2DAsync(slot_tgt + (size_t)b0 * lds_tgt * esz, (size_t)lds_tgt * esz, dslot, (size_t)A * esz,
-                            (size_t)A * esz, rows, cudaMemcpyDeviceToHost, st);
+                            (size_t)A * esz, rows, cudaMemcpyDeviceToHost, S.d2h);
+    if (tr) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), S.d2h); }
     if (e != cudaSuccess) rc = cuda_fail(e, "device->host chunk copy");
   }
+  const cudaError_t ej = d2h_join(st);
+  if (ej != cudaSuccess && rc == SFFT_OK) rc = cuda_fail(ej, "device->host stream join");
   if (use_pool) {
     while (job.step()) {}  // on error: drain so no worker still reads the caller's rows
     p.wait();
   }
+  const double t_enq = tr ? now_us() - t0 : 0.0;
   cudaEventRecord(S.h_free, st);
   const cudaError_t es = cudaStreamSynchronize(st);
+  if (tr) {
+    fprintf(stderr, "[sfft host] B=%lld A=%lld chunks=%lld chunk=%lld pool=%d out_pinned=%d: setup %.0f us, await(c) us:",
+            (long long)B, (long long)A, (long long)job.nchunks(), (long long)job.chunk, (int)use_pool,
+            (int)out_pinned, t0 - t_call);
+    for (double x : tw) fprintf(stderr, " %.0f", x);
+    fprintf(stderr, " | enqueued %.0f | synced %.0f\n", t_enq, now_us() - t0);
+    for (size_t i = 0; i + 3 < tev.size(); i += 4) {
+      float h2d = 0, k = 0, d2h = 0, from0 = 0;
+      cudaEventElapsedTime(&h2d, tev[i], tev[i + 1]);
+      cudaEventElapsedTime(&k, tev[i + 1], tev[i + 2]);
+      cudaEventElapsedTime(&d2h, tev[i + 2], tev[i + 3]);
+      cudaEventElapsedTime(&from0, tev[0], tev[i + 3]);
+      fprintf(stderr, "[sfft host]   chunk %zu: h2d %.0f us, transform %.0f us, d2h %.0f us, done at %.0f us\n", i / 4,
+              h2d * 1e3, k * 1e3, d2h * 1e3, from0 * 1e3);
+    }
+    for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
+  }
   if (rc) return rc;
   if (es != cudaSuccess) return cuda_fail(es, "host transform");
   // pageable outputs: copy out of the pinned result staging
@@ -576,10 +646,14 @@ extern "C" int sfft_hidft_to_dft_fused_host(const int64_t* J, int64_t k, int M, 
     if (e != cudaSuccess) { rc = cuda_fail(e, "host->device chunk copy"); break; }
     rc = fused_to_dft(dJ, k, rows, M, din, rows, A, dtype, dout, k, dstat + b0, st, 1);
     if (rc) break;
-    e = cudaMemcpy2DAsync(out_tgt + (size_t)b0 * ldo_tgt * esz, (size_t)ldo_tgt * esz, dout, (size_t)k * esz,
-                          (size_t)k * esz, rows, cudaMemcpyDeviceToHost, st);
+    e = d2h_after(st);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(out_tgt + (size_t)b0 * ldo_tgt * esz, (size_t)ldo_tgt * esz, dout, (size_t)k * esz,
+                            (size_t)k * esz, rows, cudaMemcpyDeviceToHost, Sg.d2h);
     if (e != cudaSuccess) rc = cuda_fail(e, "device->host chunk copy");
   }
+  const cudaError_t ej = d2h_join(st);
+  if (ej != cudaSuccess && rc == SFFT_OK) rc = cuda_fail(ej, "device->host stream join");
   if (use_pool) {
     while (job.step()) {}
     p.wait();
