@@ -178,7 +178,7 @@ def _signal_ptr(src: _Src) -> int:
 
 
 HOST_GATHER_THREADS = 0   # host gather workers besides the caller; 0: every other core
-HOST_CHUNK_ROWS = 0       # rows per pipelined chunk; 0: B/8 (at least 16)
+HOST_CHUNK_ROWS = 0       # rows per pipelined chunk; 0: B/16 (at least 32)
 
 
 def _host_threads() -> int:

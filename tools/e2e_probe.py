@@ -7,7 +7,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2211_15299_b200 as S  # noqa: E402
-import paper_2211_15299_b200.hidft as H  # noqa: E402
+H = sys.modules["paper_2211_15299_b200.hidft"]  # the package re-exports the function hidft under that name
 from paper_2211_15299_b200 import workloads as W  # noqa: E402
 
 wl = W.make_workload(2)
