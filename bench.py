@@ -338,6 +338,14 @@ def run_b200(args) -> None:
         except (OSError, ValueError):
             pass
 
+    # N > 1, untimed: one step with the result rows written straight into
+    # rank 0's device buffer over peer memory (dist.PeerRows),
+    # checked on rank 0 against the planted spectra of every rank's first and
+    # last row; the timed steps above leave the rows sharded
+    peer_info = None
+    if world > 1 and cfg != 3 and not args.no_peer_gather:
+        peer_info = run_peer_gather(S, W, torch, dist, sets[0], J, wl, cfg, B, B_total, status, cdt, rank, world)
+
     # end to end through the public API with host buffers (rank-local)
     e2e = None
     if not args.no_e2e:
@@ -374,11 +382,53 @@ def run_b200(args) -> None:
         }
         if e2e:
             line["e2e"] = e2e
+        if peer_info:
+            line["peer_gather"] = peer_info
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_peer_gather(S, W, torch, dist, signals, J, wl, cfg, B, B_total, status, cdt, rank, world) -> dict:
+    """One step per rank writing its rows into rank 0's buffer through CUDA
+    IPC peer memory (the transform's own epilogue stores); device time max
+    over ranks; rank 0 checks rows against the planted spectra.  Failures are
+    reported in the line, not raised (the timed numbers stand on their own)."""
+    from paper_2211_15299_b200.dist import PeerRows, shard_range
+    try:
+        peer = PeerRows(B_total, wl.k, cdt)
+        if peer.rows[1] - peer.rows[0] != B:
+            raise RuntimeError(f"peer rows {peer.rows} do not match this rank's {B} signals")
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        S.hidft_to_dft_batched(signals, J, out=peer.local, status=status, check=False)
+        e1.record()
+        full = peer.complete()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64)
+        if dist.get_backend() == "nccl":
+            ms = ms.cuda()
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        info = {"rows": B_total, "ms_step": round(float(ms.item()), 4), "status_max": int(status.max().item()),
+                "path": "dist.PeerRows: rank 0 exports a CUDA IPC handle of its B x k result buffer; every "
+                        "rank's transform stores its row shard there over NVLink/NVSwitch peer memory"}
+        if rank == 0:
+            errs = []
+            for r in range(world):
+                a, b = shard_range(B_total, r, world)
+                for row in sorted({a, b - 1}):
+                    want = W.make_workload(cfg, B=1, b0=row).coeffs[0]
+                    got = full[row].cpu().numpy()
+                    errs.append(float(np.linalg.norm(got - want) / np.linalg.norm(want)))
+            info["rows_checked"] = len(errs)
+            info["max_rel_l2"] = max(errs)
+        peer.close()
+        return info
+    except Exception as e:  # noqa: BLE001
+        return {"error": repr(e)[:300]}
 
 
 def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
@@ -431,7 +481,7 @@ def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
                      if wl.support.ndim == 2 else
                      "public API on a page-locked host tensor -> sfft_hidft_host: native host threads gather "
                      "the 2^s needed samples per signal into pinned staging while earlier row chunks are "
-                     "copied to the device, transformed and copied back (one stream)")}
+                     "copied to the device, transformed and copied back (downloads on a second stream)")}
 
 
 # ------------------------------------------------------- CPU reference ---
@@ -571,6 +621,7 @@ def main() -> None:
     ap.add_argument("--ref-seconds", type=float, default=150.0, help="whole --impl reference run budget")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-peer-gather", action="store_true", help="N > 1: skip the untimed peer-memory gather check")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: host-side collectives (multi-rank path test on fewer GPUs)")
     args = ap.parse_args()

@@ -260,6 +260,22 @@ SFFT_API int sfft_hidft_to_dft_fused_host(const int64_t* J, int64_t k, int M, co
                                           int64_t ld, int dtype, void* out, int64_t ld_out, int nthreads,
                                           sfft_stream_t stream);
 
+/* ---- result rows in another process's device memory ----
+ * The reference returns each signal's coefficients to its caller
+ * (hidft.py:188-207); with the batch sharded over the GPUs of a node the
+ * rows end up on one rank.  The owner allocates the B x k result buffer and
+ * exports a CUDA IPC handle (SFFT_IPC_HANDLE_BYTES opaque bytes, sent to the
+ * other ranks by the caller); each other rank maps it and passes its row
+ * shard of the mapped pointer as the `out` of sfft_hidft /
+ * sfft_hidft_to_dft_fused, so the transform's own stores write the rows
+ * over NVLink / NVSwitch peer memory (no separate gather collective).  The
+ * writer synchronises its stream before the owner reads (e.g. a barrier). */
+#define SFFT_IPC_HANDLE_BYTES 64
+SFFT_API int sfft_peer_alloc(int64_t bytes, void** dptr, unsigned char* handle);
+SFFT_API int sfft_peer_free(void* dptr);
+SFFT_API int sfft_peer_open(const unsigned char* handle, void** dptr);
+SFFT_API int sfft_peer_close(void* dptr);
+
 #ifdef __cplusplus
 }
 #endif
