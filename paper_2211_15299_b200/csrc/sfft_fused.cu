@@ -120,8 +120,18 @@ __device__ int fused_plan(const int64_t* __restrict__ Jrow, bool live, int M, in
   return __popc(mask) == S ? 0 : 3;
 }
 
+// Slots per thread of the fused kernel: with per-signal plans (config 4) the
+// on-chip plan derivation is spread over the signal's threads, so complex64
+// uses 8 slots per thread (twice the threads of the plan kernel's 16):
+// config 4 221 -> 198 us.  The shared-support variant keeps the default.
+#ifndef SFFT_FUSED_E
+#define SFFT_FUSED_E 8
+#endif
+template <typename T, int S, bool PS>
+constexpr int fused_e() { return (PS && sizeof(T) == 4 && S >= 7) ? SFFT_FUSED_E : 0; }
+
 template <typename T, int S, bool PS> constexpr size_t fused_smem() {
-  using G = Geo<T, S>;
+  using G = Geo<T, S, fused_e<T, S, PS>()>;
   constexpr size_t NP = PS ? G::SPC : 1;
   return (size_t)G::SPC * G::A * sizeof(Cx<T>) + NP * (G::A > 1 ? G::A - 1 : 1) * sizeof(Cx<T>) +
          NP * G::A * sizeof(int);
@@ -131,9 +141,11 @@ template <typename T, int S, bool PS> constexpr size_t fused_smem() {
 // plan on chip, then gathers, transforms and stores.  Shared support: CTAs
 // are persistent, build the one plan once and loop over signal groups.
 template <typename T, int S, bool PER_SIGNAL>
-__global__ void __launch_bounds__(Geo<T, S>::NT, Geo<T, S>::MINB)
+__global__ void __launch_bounds__(Geo<T, S, fused_e<T, S, PER_SIGNAL>()>::NT,
+                                  Geo<T, S, fused_e<T, S, PER_SIGNAL>()>::MINB)
 k_fused_to_dft(const FusedArgs args) {
-  using G = Geo<T, S>;
+  constexpr int EO = fused_e<T, S, PER_SIGNAL>();
+  using G = Geo<T, S, EO>;
   constexpr int A = G::A;
   constexpr int NP = PER_SIGNAL ? G::SPC : 1;  // plans held per CTA
   constexpr int TWN = A > 1 ? A - 1 : 1;
@@ -178,12 +190,12 @@ k_fused_to_dft(const FusedArgs args) {
 #pragma unroll
       for (int i = 0; i < S; ++i) d[i] = args.identity ? (1u << i) : (1u << (args.M - 1 - spiv[i]));
       const Cx<T>* row = reinterpret_cast<const Cx<T>*>(args.sig) + b * args.ld;
-      gather<T, S>(v, t, row, d, 0u, args.identity ? (uint32_t)(A - 1) : nmask);
+      gather<T, S, T, EO>(v, t, row, d, 0u, args.identity ? (uint32_t)(A - 1) : nmask);
     } else {
 #pragma unroll
       for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
     }
-    butterfly<T, S>(v, t, sd, tw);
+    butterfly<T, S, false, EO>(v, t, sd, tw);
     if (ok) {
       Cx<T>* o = reinterpret_cast<Cx<T>*>(args.out) + b * args.ld_out;
       for (int i = t; i < A; i += G::TPS) o[i] = cscale(sd[swz<T, S>(pats[i])], scale);
@@ -194,7 +206,7 @@ k_fused_to_dft(const FusedArgs args) {
 
 template <typename T, int S, bool PS>
 static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
-  using G = Geo<T, S>;
+  using G = Geo<T, S, fused_e<T, S, PS>()>;
   constexpr size_t smem = fused_smem<T, S, PS>();
   static_assert(smem <= 227 * 1024, "fused kernel smem");
   auto kern = k_fused_to_dft<T, S, PS>;

@@ -108,10 +108,10 @@ __device__ __forceinline__ void butterfly(Cx<T> (&v)[Geo<T, S, EOV>::E], int t, 
 // low LE bits of a come from the unrolled register index x, so their part
 // of the offset is a compile-time selection of d_0..d_{LE-1}.  All E loads
 // are issued back to back before any use.
-template <typename T, int S, typename In = T>
-__device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S>::E], int t, const Cx<In>* __restrict__ row,
+template <typename T, int S, typename In = T, int EOV = 0>
+__device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S, EOV>::E], int t, const Cx<In>* __restrict__ row,
                                        const uint32_t (&d)[S > 0 ? S : 1], uint32_t base, uint32_t nmask) {
-  using G = Geo<T, S>;
+  using G = Geo<T, S, EOV>;
   uint32_t hi = base;
 #pragma unroll
   for (int i = G::LE; i < S; ++i)
