@@ -236,10 +236,16 @@ def run_b200(args) -> None:
     if not (err < tol) or worst != 0:
         raise SystemExit(f"bench parity gate failed: rel L2 {err:.3e} status {worst}")
 
-    # CUDA graphs: one graph per rotation set, captured from the same step
-    # call, so a timed step is the step's kernels without host launch gaps
-    # (config 1 is launch-bound); --no-graph times the eager calls
-    run = step
+    # CUDA graphs captured from the same step calls, so a timed step is the
+    # step's kernels without host launch gaps (config 1 is launch-bound): one
+    # graph of GS >= --graph-steps consecutive steps (whole cycles over the R
+    # rotation sets; inside it the library's programmatic dependent launch
+    # lets step i+1 gather while step i drains, as it does for back-to-back
+    # eager calls) plus one graph per single step for counts that are not a
+    # multiple of GS.  --no-graph times the eager calls.
+    def run_steps(n, start=0):
+        for i in range(start, start + n):
+            step(i)
     if not args.no_graph:
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
@@ -253,10 +259,22 @@ def run_b200(args) -> None:
             with torch.cuda.graph(g):
                 step(i)
             graphs.append(g)
+        GS = R * max(1, math.ceil(args.graph_steps / R))  # steps per group graph, whole rotation cycles
+        group = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(group):
+            for i in range(GS):
+                step(i)
         torch.cuda.synchronize()
 
-        def run(i):
-            graphs[i % R].replay()
+        def run_steps(n, start=0):
+            i = start
+            while i < start + n:
+                if i % GS == 0 and start + n - i >= GS:
+                    group.replay()
+                    i += GS
+                else:
+                    graphs[i % R].replay()
+                    i += 1
 
     vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
     sampler = ClockSampler(vis[local] if local < len(vis) else local)
@@ -265,12 +283,10 @@ def run_b200(args) -> None:
     t_end = time.time() + args.soak
     i = 0
     while time.time() < t_end:
-        for _ in range(64):
-            run(i)
-            i += 1
+        run_steps(64, i)
+        i += 64
         torch.cuda.synchronize()
-    for w in range(args.warmup):
-        run(w)
+    run_steps(args.warmup)
     stream = torch.cuda.current_stream(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -278,8 +294,7 @@ def run_b200(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    for t in range(args.steps):
-        run(t)
+    run_steps(args.steps)
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -372,7 +387,9 @@ def run_b200(args) -> None:
                                    + f", {wl.dtype}, "
                                    + ("shared support" if wl.support.ndim == 1 else "per-signal supports"),
                        "global_batch": B_total, "N": N, "k": wl.k, "parallelism": f"batch shard x{world}",
-                       "launch": "eager calls" if args.no_graph else "CUDA graph replay of the step call",
+                       "launch": "eager calls" if args.no_graph else (
+                           f"CUDA graphs of {GS} consecutive step calls (rotating over the input sets), "
+                           "programmatic dependent launch between steps"),
                        "l2": f"rotating {R} input sets, gather footprint {R * footprint / 2**20:.0f} MiB "
                              f"vs 126 MB L2"},
             "gpu_launches": args.steps * launches_per_step,
@@ -611,6 +628,8 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=0,
                     help="signals per GPU (weak) or in total (strong); default: the config's B")
     ap.add_argument("--no-graph", action="store_true", help="time eager calls instead of CUDA-graph replays")
+    ap.add_argument("--graph-steps", type=int, default=32, help="steps captured per group graph (rounded up to "
+                    "whole rotation cycles)")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="weak: the config's B per GPU (default); strong: the config's B split over the GPUs")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])

@@ -36,6 +36,7 @@ k_hidft_plan(const PlanArgs args) {
   using G = Geo<T, S>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);
+  pdl_release();  // the next launch may start gathering (its inputs are checked on the host)
   const int tid = threadIdx.x;
   const int g = tid / G::TPS, t = tid % G::TPS;
   const int64_t b = (int64_t)blockIdx.x * G::SPC + g;  // output row
@@ -64,6 +65,7 @@ k_hidft_plan(const PlanArgs args) {
   }
   Cx<T>* sd = sdata + g * G::A;
   butterfly<T, S>(v, t, sd, reinterpret_cast<const Cx<T>*>(args.tw));
+  pdl_wait();  // earlier launches in the stream complete before the first store (see plan_pdl)
   if (live) {
     const T scale = (T)args.scale1;
     Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + b * args.ld1;
@@ -86,6 +88,50 @@ k_hidft_plan(const PlanArgs args) {
   }
 }
 
+// Consecutive plan-kernel launches on one stream overlap (programmatic
+// dependent launch): each kernel lets its successor launch at once
+// (pdl_release) and waits for its predecessor only before its first store
+// (pdl_wait), so launch N+1 gathers while launch N drains.  Completion stays
+// ordered (every CTA of N waits for N-1 before it can finish), so the
+// launches that may still be running when N+1 gathers are the PDL chain
+// since the last fully ordered launch.  N+1 joins the chain only if its
+// signals do not overlap any output of that chain (outputs recorded here);
+// otherwise, for pre-gathered rows, or when the chain is long, it launches
+// fully stream-ordered and the chain restarts.  A foreign kernel between two
+// launches is fully ordered itself, so the check is conservative.
+// SFFT_PDL=0 disables the overlap.
+namespace {
+struct PdlChain {
+  std::vector<std::pair<uintptr_t, uintptr_t>> outs;  // [lo, hi) written by the chain
+};
+std::mutex g_pdl_mu;
+std::map<cudaStream_t, PdlChain> g_pdl;
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+}  // namespace
+
+static bool plan_pdl(cudaStream_t st, uintptr_t in_lo, uintptr_t in_hi,
+                     const std::pair<uintptr_t, uintptr_t> (&outs)[2], bool eligible) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  PdlChain& c = g_pdl[st];
+  bool ok = eligible && pdl_enabled() && c.outs.size() < 16;
+  for (const auto& o : c.outs)
+    if (ok && in_lo < o.second && o.first < in_hi) ok = false;
+  if (!ok) c.outs.clear();  // fully ordered: the chain restarts here
+  for (const auto& o : outs) {
+    if (o.first >= o.second) continue;
+    bool seen = false;
+    for (const auto& x : c.outs) seen |= (x == o);
+    if (!seen) c.outs.push_back(o);
+  }
+  return ok;
+}
+
 template <typename T, int S>
 static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {
   using G = Geo<T, S>;
@@ -97,8 +143,26 @@ static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {
   if (rc) return rc;
   const int64_t ngroups = (a.B * a.nshift + G::SPC - 1) / G::SPC;
   if (ngroups > 0x7fffffff) return fail(SFFT_ERR_UNSUPPORTED, "batch too large for one launch");
-  kern<<<(unsigned)ngroups, G::NT, smem, st>>>(a);
-  SFFT_CUDA(cudaGetLastError());
+  if (ngroups == 0) return SFFT_OK;
+  const size_t esz_in = (sizeof(T) == 8 && a.in_c64) ? 8 : sizeof(Cx<T>);
+  const int64_t rows = a.B * a.nshift;
+  const uintptr_t in_lo = (uintptr_t)a.sig;
+  const uintptr_t in_hi = in_lo + (size_t)((a.B - 1) * a.ld + (a.identity ? G::A : (1ll << a.M))) * esz_in;
+  const std::pair<uintptr_t, uintptr_t> outs[2] = {
+      {(uintptr_t)a.out1, (uintptr_t)a.out1 + (size_t)((rows - 1) * a.ld1 + a.n1) * sizeof(Cx<T>)},
+      {(uintptr_t)a.out2, a.out2 ? (uintptr_t)a.out2 + (size_t)((rows - 1) * a.ld2 + G::A) * sizeof(Cx<T>) : 0}};
+  const bool pdl = plan_pdl(st, in_lo, in_hi, outs, a.identity == 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ngroups);
+  cfg.blockDim = dim3(G::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return SFFT_OK;
 }
 

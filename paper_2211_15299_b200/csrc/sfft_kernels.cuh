@@ -127,6 +127,13 @@ __device__ __forceinline__ void gather(Cx<T> (&v)[Geo<T, S, EOV>::E], int t, con
   }
 }
 
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; griddepcontrol.wait blocks until the predecessor has
+// completed and its writes are visible (a no-op without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct PlanArgs {
   const void* sig;
   int64_t B, ld;

@@ -297,15 +297,10 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(sdst)), "l"(g) : "memory");
 }
 
-// Programmatic dependent launch: a kernel launched with
-// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
-// predecessor drains; griddepcontrol.wait blocks until the predecessor has
-// completed and its writes are visible.  Each tri kernel reads only
-// read-only inputs (signals, plan tables) before the wait and releases its
-// dependents only after it, so by induction every earlier kernel in the
-// stream has completed once a kernel passes its wait.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Programmatic dependent launch (pdl_wait / pdl_release, sfft_kernels.cuh):
+// each tri kernel reads only read-only inputs (signals, plan tables) before
+// the wait and releases its dependents only after it, so by induction every
+// earlier kernel in the stream has completed once a kernel passes its wait.
 
 #ifndef SFFT_TRI_PF  // front: units prefetched into L2 beyond the one in registers (config 5: 0 -> 145 us, 1 -> 153 us;
                      // loading the next unit after this one's stages instead of before, at
