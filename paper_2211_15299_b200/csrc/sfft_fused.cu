@@ -155,6 +155,7 @@ k_fused_to_dft(const FusedArgs args) {
   int* spats_all = reinterpret_cast<int*>(stw_all + NP * TWN);  // NP * A
   __shared__ int sctl[NP][2 + (S > 0 ? S : 1)];
 
+  if (PER_SIGNAL) pdl_release();  // the next launch may start gathering (inputs checked on the host)
   const int tid = threadIdx.x;
   const int g = tid / G::TPS, t = tid % G::TPS;
   const uint32_t nmask = (args.M >= 32) ? 0xffffffffu : ((1u << args.M) - 1u);
@@ -181,7 +182,6 @@ k_fused_to_dft(const FusedArgs args) {
     if (PER_SIGNAL) {
       st = fused_plan<T, S>(args.J + (live ? b : 0) * (int64_t)A, live, args.M, t, G::TPS, pats, tw,
                             reinterpret_cast<int*>(sd), &sctl[g][0]);
-      if (live && t == 0 && args.status) args.status[b] = st;
     }
     const bool ok = live && st == 0;
     Cx<T> v[G::E];
@@ -196,6 +196,10 @@ k_fused_to_dft(const FusedArgs args) {
       for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
     }
     butterfly<T, S, false, EO>(v, t, sd, tw);
+    if (PER_SIGNAL) {
+      pdl_wait();  // earlier launches complete before the first store
+      if (live && t == 0 && args.status) args.status[b] = st;
+    }
     if (ok) {
       Cx<T>* o = reinterpret_cast<Cx<T>*>(args.out) + b * args.ld_out;
       for (int i = t; i < A; i += G::TPS) o[i] = cscale(sd[swz<T, S>(pats[i])], scale);
@@ -205,7 +209,7 @@ k_fused_to_dft(const FusedArgs args) {
 }
 
 template <typename T, int S, bool PS>
-static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
+static int run_fused_kernel(const FusedArgs& a, cudaStream_t st, bool pdl_ok) {
   using G = Geo<T, S, fused_e<T, S, PS>()>;
   constexpr size_t smem = fused_smem<T, S, PS>();
   static_assert(smem <= 227 * 1024, "fused kernel smem");
@@ -216,8 +220,27 @@ static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
   const int64_t ngroups = (a.B + G::SPC - 1) / G::SPC;
   int64_t grid = PS ? ngroups : std::min<int64_t>(ngroups, (int64_t)num_sms() * occ);
   if (grid > 0x7fffffff) return fail(SFFT_ERR_UNSUPPORTED, "batch too large for one launch");
-  kern<<<(unsigned)std::max<int64_t>(grid, 1), G::NT, smem, st>>>(a);
-  SFFT_CUDA(cudaGetLastError());
+  // per-signal plans join the stream's PDL chain like the plan kernel
+  // (sfft_hidft.cu, pdl_join): signals and supports are read before the wait
+  constexpr size_t esz = sizeof(Cx<T>);
+  const ByteRange in[2] = {
+      {(uintptr_t)a.sig, (uintptr_t)a.sig + (size_t)((a.B - 1) * a.ld + (a.identity ? G::A : (1ll << a.M))) * esz},
+      {(uintptr_t)a.J, (uintptr_t)a.J + (size_t)a.n_supports * G::A * sizeof(int64_t)}};
+  const ByteRange outs[2] = {
+      {(uintptr_t)a.out, (uintptr_t)a.out + (size_t)((a.B - 1) * a.ld_out + G::A) * esz},
+      {(uintptr_t)a.status, a.status ? (uintptr_t)(a.status + a.n_supports) : 0}};
+  const bool pdl = pdl_join(st, in, 2, outs, 2, PS && pdl_ok && !a.identity);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(grid, 1));
+  cfg.blockDim = dim3(G::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  SFFT_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return SFFT_OK;
 }
 
@@ -225,10 +248,10 @@ static int run_fused_kernel(const FusedArgs& a, cudaStream_t st) {
   M_(0, __VA_ARGS__) M_(1, __VA_ARGS__) M_(2, __VA_ARGS__) M_(3, __VA_ARGS__) M_(4, __VA_ARGS__) \
   M_(5, __VA_ARGS__) M_(6, __VA_ARGS__) M_(7, __VA_ARGS__) M_(8, __VA_ARGS__) M_(9, __VA_ARGS__) \
   M_(10, __VA_ARGS__) M_(11, __VA_ARGS__) M_(12, __VA_ARGS__)
-#define FUSED_CASE(S_, T_, PS_) case S_: return run_fused_kernel<T_, S_, PS_>(a, st);
+#define FUSED_CASE(S_, T_, PS_) case S_: return run_fused_kernel<T_, S_, PS_>(a, st, pdl_ok);
 
 template <bool PS>
-static int dispatch_fused(int dtype, int s, const FusedArgs& a, cudaStream_t st) {
+static int dispatch_fused(int dtype, int s, const FusedArgs& a, cudaStream_t st, bool pdl_ok) {
   if (dtype == SFFT_C64) {
     switch (s) {
       SFFT_CASES_12(FUSED_CASE, float, PS)
@@ -300,8 +323,10 @@ int sfft::fused_to_dft(const int64_t* J, int64_t k, int64_t n_supports, int M, c
   a.ld_out = ld_out;
   a.status = dstat;
   a.identity = identity;
-  int rc = (n_supports == 1 && B >= 1) ? dispatch_fused<false>(dtype, s, a, st)
-                                       : dispatch_fused<true>(dtype, s, a, st);
+  // no PDL after this call's own staging copies / memsets (only kernel-to-kernel overlap)
+  const bool pdl_ok = !tmpJ && !tmpStat;
+  int rc = (n_supports == 1 && B >= 1) ? dispatch_fused<false>(dtype, s, a, st, pdl_ok)
+                                       : dispatch_fused<true>(dtype, s, a, st, pdl_ok);
   if (rc == SFFT_OK && tmpStat) {
     std::vector<int32_t> h(n_supports);
     cudaError_t e = cudaMemcpyAsync(h.data(), tmpStat, sizeof(int32_t) * n_supports,

@@ -95,7 +95,7 @@ k_hidft_plan(const PlanArgs args) {
 // ordered (every CTA of N waits for N-1 before it can finish), so the
 // launches that may still be running when N+1 gathers are the PDL chain
 // since the last fully ordered launch.  N+1 joins the chain only if its
-// signals do not overlap any output of that chain (outputs recorded here);
+// signals do not overlap any output of that chain (pdl_join records them);
 // otherwise, for pre-gathered rows, or when the chain is long, it launches
 // fully stream-ordered and the chain restarts.  A foreign kernel between two
 // launches is fully ordered itself, so the check is conservative.
@@ -115,15 +115,16 @@ bool pdl_enabled() {
 }
 }  // namespace
 
-static bool plan_pdl(cudaStream_t st, uintptr_t in_lo, uintptr_t in_hi,
-                     const std::pair<uintptr_t, uintptr_t> (&outs)[2], bool eligible) {
+bool pdl_join(cudaStream_t st, const ByteRange* in, int nin, const ByteRange* out, int nout, bool eligible) {
   std::lock_guard<std::mutex> lk(g_pdl_mu);
   PdlChain& c = g_pdl[st];
   bool ok = eligible && pdl_enabled() && c.outs.size() < 16;
   for (const auto& o : c.outs)
-    if (ok && in_lo < o.second && o.first < in_hi) ok = false;
+    for (int i = 0; i < nin && ok; ++i)
+      if (in[i].first < o.second && o.first < in[i].second) ok = false;
   if (!ok) c.outs.clear();  // fully ordered: the chain restarts here
-  for (const auto& o : outs) {
+  for (int i = 0; i < nout; ++i) {
+    const ByteRange& o = out[i];
     if (o.first >= o.second) continue;
     bool seen = false;
     for (const auto& x : c.outs) seen |= (x == o);
@@ -146,12 +147,12 @@ static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {
   if (ngroups == 0) return SFFT_OK;
   const size_t esz_in = (sizeof(T) == 8 && a.in_c64) ? 8 : sizeof(Cx<T>);
   const int64_t rows = a.B * a.nshift;
-  const uintptr_t in_lo = (uintptr_t)a.sig;
-  const uintptr_t in_hi = in_lo + (size_t)((a.B - 1) * a.ld + (a.identity ? G::A : (1ll << a.M))) * esz_in;
-  const std::pair<uintptr_t, uintptr_t> outs[2] = {
+  const ByteRange in[1] = {{(uintptr_t)a.sig, (uintptr_t)a.sig + (size_t)((a.B - 1) * a.ld +
+                                                    (a.identity ? G::A : (1ll << a.M))) * esz_in}};
+  const ByteRange outs[2] = {
       {(uintptr_t)a.out1, (uintptr_t)a.out1 + (size_t)((rows - 1) * a.ld1 + a.n1) * sizeof(Cx<T>)},
       {(uintptr_t)a.out2, a.out2 ? (uintptr_t)a.out2 + (size_t)((rows - 1) * a.ld2 + G::A) * sizeof(Cx<T>) : 0}};
-  const bool pdl = plan_pdl(st, in_lo, in_hi, outs, a.identity == 0);
+  const bool pdl = pdl_join(st, in, 1, outs, 2, a.identity == 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ngroups);
   cfg.blockDim = dim3(G::NT);

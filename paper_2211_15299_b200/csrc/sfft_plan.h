@@ -3,6 +3,8 @@
 
 #include <stdint.h>
 
+#include <utility>
+
 struct sfft_plan {
   int device;
   int M, dtype, n_r, height, s, level, homogeneous;
@@ -62,6 +64,11 @@ int launch_hidft_plan(const sfft_plan* p, const void* sig, int64_t B, int64_t ld
                       int64_t ld1, void* out2, int64_t ld2, int identity, cudaStream_t st,
                       int64_t nshift = 1, int in_c64 = 0);
 int max_supported_s(int dtype);
+// programmatic-dependent-launch chain of one stream (sfft_hidft.cu): true if
+// a launch reading `in` may overlap the chain's running launches; records
+// its outputs (or restarts the chain when it must launch fully ordered)
+using ByteRange = std::pair<uintptr_t, uintptr_t>;
+bool pdl_join(cudaStream_t st, const ByteRange* in, int nin, const ByteRange* out, int nout, bool eligible);
 // per-signal plans only serve sfft_hidft(SFFT_OUT_DFT)
 int reject_per_signal(const sfft_plan* p, const char* entry);
 // hidft_to_dft for per-signal supports (sfft_hidft_to_dft_fused's body)

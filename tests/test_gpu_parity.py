@@ -760,3 +760,34 @@ def test_back_to_back_calls_chain(S, torch):
     # planted check of the first transform: the DFT of f
     want = np.fft.fft(f.cpu().numpy().astype(np.complex128), axis=1)
     assert rel_l2(ref[1].cpu().numpy(), want) < 1e-5
+
+
+def test_back_to_back_fused_chain(S, torch):
+    """The per-signal fused kernel joins the PDL chain too: chained calls
+    (signals = the previous call's output) and calls sharing one output and
+    status buffer stay ordered."""
+    M, B = 9, 48
+    N = 1 << M
+    Jt = torch.arange(N, dtype=torch.int64).repeat(B, 1).cuda()
+    rng = np.random.default_rng(6)
+    f = torch.from_numpy((rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(np.complex64)).cuda()
+    other = torch.from_numpy((rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(np.complex64)).cuda()
+    st = torch.zeros(B, dtype=torch.int32, device="cuda")
+    ref = [f]
+    for _ in range(3):
+        ref.append(S.hidft_to_dft_batched(ref[-1], Jt, status=st, check=False).clone())
+        torch.cuda.synchronize()
+    bufs = [torch.empty_like(f) for _ in range(3)]
+    for _ in range(20):
+        x = f
+        for i in range(3):
+            S.hidft_to_dft_batched(x, Jt, out=bufs[i], status=st, check=False)
+            x = bufs[i]
+        S.hidft_to_dft_batched(other, Jt, out=bufs[0], status=st, check=False)
+        S.hidft_to_dft_batched(f, Jt, out=bufs[0], status=st, check=False)
+        torch.cuda.synchronize()
+        for i in range(3):
+            assert torch.equal(bufs[i], ref[i + 1])
+        assert int(st.max()) == 0
+    want = np.fft.fft(f.cpu().numpy().astype(np.complex128), axis=1)
+    assert rel_l2(ref[1].cpu().numpy(), want) < 1e-5
