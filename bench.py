@@ -241,8 +241,8 @@ def run_b200(args) -> None:
     # graph of GS >= --graph-steps consecutive steps (whole cycles over the R
     # rotation sets; inside it the library's programmatic dependent launch
     # lets step i+1 gather while step i drains, as it does for back-to-back
-    # eager calls) plus one graph per single step for counts that are not a
-    # multiple of GS.  --no-graph times the eager calls.
+    # eager calls), one graph for each tail length this run needs, and one
+    # graph per single step as a fallback.  --no-graph times the eager calls.
     def run_steps(n, start=0):
         for i in range(start, start + n):
             step(i)
@@ -264,14 +264,26 @@ def run_b200(args) -> None:
         with torch.cuda.graph(group):
             for i in range(GS):
                 step(i)
+        # the tails this run needs (K, W and the soak's 64 modulo GS) as graphs of their own
+        tails = {}
+        for n in {args.steps % GS, args.warmup % GS, 64 % GS} - {0}:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for i in range(n):
+                    step(i)
+            tails[n] = g
         torch.cuda.synchronize()
 
         def run_steps(n, start=0):
             i = start
             while i < start + n:
-                if i % GS == 0 and start + n - i >= GS:
+                left = start + n - i
+                if i % GS == 0 and left >= GS:
                     group.replay()
                     i += GS
+                elif i % GS == 0 and left in tails:
+                    tails[left].replay()
+                    i += left
                 else:
                     graphs[i % R].replay()
                     i += 1
