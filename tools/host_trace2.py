@@ -17,11 +17,14 @@ host = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
 host.copy_(dev)
 del dev
 J = S.SupportSet(wl.N, wl.support)
-for chunks in [int(x) for x in os.environ.get("CHUNKS", "0").split()]:
+runs = [(c, t) for c in os.environ.get("CHUNKS", "0").split() for t in os.environ.get("THREADS", "0").split()]
+for chunks, thr in [(int(c), int(t)) for c, t in runs]:
     H.HOST_CHUNK_ROWS = chunks
+    H.HOST_GATHER_THREADS = thr
     per = []
     for i in range(8):
         t = time.perf_counter()
         S.hidft_to_dft_batched(host, J)
         per.append(time.perf_counter() - t)
-    print(f"chunk rows {chunks}: call ms", " ".join(f"{x * 1e3:.3f}" for x in per), file=sys.stderr, flush=True)
+    print(f"chunk rows {chunks} threads {thr}: call ms", " ".join(f"{x * 1e3:.3f}" for x in per), file=sys.stderr,
+          flush=True)
