@@ -427,9 +427,14 @@ def run_peer_gather(S, W, torch, dist, signals, J, wl, cfg, B, B_total, status, 
     reported in the line, not raised (the timed numbers stand on their own)."""
     from paper_2211_15299_b200.dist import PeerRows, shard_range
     try:
-        peer = PeerRows(B_total, wl.k, cdt)
-        if peer.rows[1] - peer.rows[0] != B:
-            raise RuntimeError(f"peer rows {peer.rows} do not match this rank's {B} signals")
+        peer = PeerRows(B_total, wl.k, cdt)  # collective; raises on every rank together
+        fits = torch.tensor([1 if peer.rows[1] - peer.rows[0] == B else 0], dtype=torch.int32)
+        if dist.get_backend() == "nccl":
+            fits = fits.cuda()
+        dist.all_reduce(fits, op=dist.ReduceOp.MIN)
+        if int(fits.item()) == 0:
+            peer.close()
+            return {"error": "peer rows do not match the ranks' signal shards"}
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -41,6 +41,12 @@ def gather_rows(local, B: int, group=None):
     return torch.cat([buf[r, : b - a] for r, (a, b) in enumerate(sizes)], dim=0)
 
 
+def _lib_error(_lib, what):
+    from .errors import DeviceError
+    detail = _lib.load().sfft_last_error().decode(errors="replace")
+    return DeviceError(f"{what}: {detail}" if detail else what)
+
+
 class _DeviceArray:
     """__cuda_array_interface__ view of raw device memory (zero-copy into torch)."""
 
@@ -76,17 +82,31 @@ class PeerRows:
         typestr = {torch.complex64: "<c8", torch.complex128: "<c16"}[dtype]
         lib = _lib.load()
         self._lib, self._ptr = lib, ctypes.c_void_p()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        # every rank takes the same path through the collectives, even when
+        # the allocation or a mapping fails (then all ranks raise together)
         msg = [None]
         if self.rank == owner:
             handle = (ctypes.c_ubyte * _lib.IPC_HANDLE_BYTES)()
-            _lib.check(lib.sfft_peer_alloc(max(1, B * width * esz), ctypes.byref(self._ptr), handle))
-            msg = [bytes(handle)]
+            if lib.sfft_peer_alloc(max(1, B * width * esz), ctypes.byref(self._ptr), handle) == _lib.OK:
+                msg = [bytes(handle)]
         dist.broadcast_object_list(msg, src=dist.get_global_rank(group, owner) if group is not None else owner,
                                    group=group)
+        if msg[0] is None:
+            raise _lib_error(_lib, "peer buffer allocation failed on the owner rank")
+        opened = True
         if self.rank != owner:
             handle = (ctypes.c_ubyte * _lib.IPC_HANDLE_BYTES).from_buffer_copy(msg[0])
-            _lib.check(lib.sfft_peer_open(handle, ctypes.byref(self._ptr)))
-        dev = torch.device("cuda", torch.cuda.current_device())
+            opened = lib.sfft_peer_open(handle, ctypes.byref(self._ptr)) == _lib.OK
+        flag = torch.tensor([1 if opened else 0], dtype=torch.int32,
+                            device=dev if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) == 0:
+            if not opened:
+                self._ptr = ctypes.c_void_p()
+            self.local = self.full = None
+            self.close()
+            raise _lib_error(_lib, "a rank could not map the owner's result buffer (CUDA IPC / peer access)")
         base = int(self._ptr.value)
         a, b = shard_range(B, self.rank, self.world)
         self.rows = (a, b)
@@ -102,13 +122,15 @@ class PeerRows:
         return self.full
 
     def close(self):
-        """Unmap (other ranks) before the owner frees the buffer."""
-        if self._ptr.value is None:
+        """Unmap (other ranks) before the owner frees the buffer.  Collective:
+        every rank calls it once."""
+        if getattr(self, "_closed", False):
             return
+        self._closed = True
         self.local = self.full = None
-        if self.rank != self.owner:
+        if self.rank != self.owner and self._ptr.value is not None:
             self._lib.sfft_peer_close(self._ptr)
         self._dist.barrier(group=self._group)
-        if self.rank == self.owner:
+        if self.rank == self.owner and self._ptr.value is not None:
             self._lib.sfft_peer_free(self._ptr)
         self._ptr = type(self._ptr)()
