@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <string>
 
@@ -625,6 +626,74 @@ static int scratch_pool(int dev, cudaMemPool_t* pool) {
   return SFFT_OK;
 }
 
+// Scratch of the three-pass split, kept per (device, stream) and reused by
+// every call on that stream: calls on one stream are ordered, and a pass
+// writes scratch only after its predecessor (hence the previous call) has
+// completed.  Allocating per call from a stream-ordered pool instead puts a
+// memory node into every captured graph, and alternating between graphs
+// that hold such nodes costs the driver a remap of the memory at each switch
+// (config 5 in bench.py: 137 us per step with one graph, 173-362 us when a
+// 32-step graph alternates with tail graphs).  A graph keeps the buffer of
+// the stream it was captured on: replay it on one stream at a time.  Up to
+// kStreamScratch streams per device keep a buffer; further streams fall back
+// to the pool (allocated and freed per call).
+constexpr int kStreamScratch = 8;
+struct StreamScratch {
+  cudaStream_t stream;
+  void* ptr;
+  size_t bytes;
+};
+static std::mutex g_ss_mu;
+static std::map<int, std::vector<StreamScratch>> g_ss;
+
+// *ptr: scratch of at least `bytes` for stream st; *pooled: the caller frees it (cudaFreeAsync)
+static int stream_scratch(int dev, cudaStream_t st, size_t bytes, void** ptr, bool* pooled) {
+  *pooled = false;
+  {
+    std::lock_guard<std::mutex> lk(g_ss_mu);
+    auto& v = g_ss[dev];
+    bool listed = false;
+    for (auto& e : v) {
+      if (e.stream != st) continue;
+      listed = true;
+      if (e.bytes < bytes) {
+        // grow: outside a capture, wait for work in flight on st that may
+        // read the old buffer; a capture (which cannot synchronise) takes
+        // the pool path instead
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        SFFT_CUDA(cudaStreamIsCapturing(st, &cs));
+        if (cs != cudaStreamCaptureStatusNone) break;
+        SFFT_CUDA(cudaStreamSynchronize(st));
+        SFFT_CUDA(cudaFree(e.ptr));
+        e.ptr = nullptr;
+        e.bytes = 0;
+        SFFT_CUDA(cudaMalloc(&e.ptr, bytes));
+        e.bytes = bytes;
+      }
+      *ptr = e.ptr;
+      return SFFT_OK;
+    }
+    if (!listed && (int)v.size() < kStreamScratch) {
+      // a plain allocation is legal while a stream captures once this
+      // thread's capture mode is relaxed (as PyTorch's allocator does)
+      cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+      SFFT_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+      void* p = nullptr;
+      const cudaError_t e = cudaMalloc(&p, bytes);
+      cudaThreadExchangeStreamCaptureMode(&mode);
+      if (e != cudaSuccess) return cuda_fail(e, "stream scratch allocation");
+      v.push_back({st, p, bytes});
+      *ptr = p;
+      return SFFT_OK;
+    }
+  }
+  cudaMemPool_t pool;
+  if (int rc = scratch_pool(dev, &pool)) return rc;
+  SFFT_CUDA(cudaMallocFromPoolAsync(ptr, bytes, pool, st));
+  *pooled = true;
+  return SFFT_OK;
+}
+
 // rows per chunk of the two-kernel split: scratch up to SFFT_SPLIT_SCRATCH_MB
 // (default 128 MiB, measured best for config 5, tools/cfg5_sweep.sh), rounded
 // to a multiple of the back pass's rows per wave so its persistent CTAs all
@@ -746,10 +815,9 @@ static int run_tri(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, c
   const int64_t chunk = tri_chunk_rows(rows, row_bytes);
   int dev = 0;
   SFFT_CUDA(cudaGetDevice(&dev));
-  cudaMemPool_t pool;
-  if ((rc = scratch_pool(dev, &pool))) return rc;
   void* scr = nullptr;
-  SFFT_CUDA(cudaMallocFromPoolAsync(&scr, 2 * (size_t)chunk * row_bytes, pool, st));
+  bool pooled = false;
+  if ((rc = stream_scratch(dev, st, 2 * (size_t)chunk * row_bytes, &scr, &pooled))) return rc;
   Cx<T>* s1 = (Cx<T>*)scr;
   Cx<T>* s2 = s1 + ((size_t)chunk << S);
   const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(p->d_twiddles);
@@ -777,7 +845,7 @@ static int run_tri(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, c
                    invf, (const int32_t*)p->d_tri_perm);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
-  cudaFreeAsync(scr, st);
+  if (pooled) cudaFreeAsync(scr, st);
   if (e != cudaSuccess) return cuda_fail(e, "three-pass transform launch");
   return SFFT_OK;
 }
