@@ -829,12 +829,23 @@ static int run_tri(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, c
     const char* e = getenv("SFFT_TRI_PDL");
     return !(e && atoi(e) == 0);
   }();
+  // the call's first front joins the stream's PDL chain (sfft_hidft.cu,
+  // pdl_join) when its signals do not overlap the chain's outputs: its
+  // pre-wait loads read only the signals, so it gathers while the previous
+  // call's final pass drains (scratch is written only after its wait)
+  const size_t esz_in = (sizeof(T) == 8 && a.in_c64) ? 8 : sizeof(Cx<T>);
+  const ByteRange in[1] = {{(uintptr_t)a.sig, (uintptr_t)a.sig + (size_t)((a.B - 1) * a.ld +
+                                                   (a.identity ? (1ll << S) : (1ll << a.M))) * esz_in}};
+  const ByteRange outs[2] = {
+      {(uintptr_t)a.out1, (uintptr_t)a.out1 + (size_t)((rows - 1) * a.ld1 + a.n1) * sizeof(Cx<T>)},
+      {(uintptr_t)a.out2, a.out2 ? (uintptr_t)a.out2 + (size_t)((rows - 1) * a.ld2 + (1ll << S)) * sizeof(Cx<T>)
+                                 : 0}};
+  const bool pdl_first = pdl_join(st, in, 1, outs, 2, pdl && !pooled && a.identity == 0);
   cudaError_t e = cudaSuccess;
   for (int64_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += chunk) {
     const int64_t n = std::min(chunk, rows - r0);
-    // the call's first kernel is stream-ordered (its pre-wait loads read the signals)
     const int64_t g1 = std::min<int64_t>(n * TG::NSEG, sms * occ1);
-    e = launch_k(front, (unsigned)g1, TG::NT1, TG::SMEM1, st, pdl && r0 > 0, a, ftw, s1, r0, n);
+    e = launch_k(front, (unsigned)g1, TG::NT1, TG::SMEM1, st, pdl && (r0 > 0 || pdl_first), a, ftw, s1, r0, n);
     const int64_t g2 = std::min<int64_t>(n << TG::L, sms * occ2);
     if (e == cudaSuccess)
       e = launch_k(mid, (unsigned)g2, TG::NT2, TG::SMEM2, st, pdl, (const Cx<T>*)s1, s2, n, tw,

@@ -729,8 +729,8 @@ def test_alternate_split_configurations(S, env):
 @pytest.mark.parametrize("M,B", [(10, 64), (15, 6)])
 def test_back_to_back_calls_chain(S, torch, M, B):
     """Consecutive launches overlap through programmatic dependent launch
-    (sfft_hidft.cu, pdl_join; M = 15 runs the three-pass split, which starts
-    fully ordered and chains its own passes).  A call whose signals are the previous call's
+    (sfft_hidft.cu, pdl_join; M = 15 runs the three-pass split, whose first
+    pass joins the chain).  A call whose signals are the previous call's
     output must still see that output (the host keeps it out of the PDL
     chain), and calls writing the same output buffer keep stream order.
     J = Z_N so a result row is a valid signal row."""
