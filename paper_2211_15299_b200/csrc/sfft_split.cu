@@ -311,6 +311,12 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* g) {
 #ifndef SFFT_TRI_FRONT_MINB
 #define SFFT_TRI_FRONT_MINB 2
 #endif
+#ifndef SFFT_TRI_FRONT_MINB_D  // complex128
+#define SFFT_TRI_FRONT_MINB_D 1
+#endif
+#ifndef SFFT_TRI_FINAL_MINB_D  // config 6: 2 / 3 / 4 CTAs per SM -> 37.7 / 39.8 / 41.0 us (front: 1 / 2 -> 39.8 / 45.5 us)
+#define SFFT_TRI_FINAL_MINB_D 2
+#endif
 template <typename T, int S, int F>
 struct TriGeo {
   static constexpr int L = 4, EXL = 1 << L;   // final: top L slot bits
@@ -331,7 +337,7 @@ struct TriGeo {
 #ifndef SFFT_TRI_FINAL_MINB
 #define SFFT_TRI_FINAL_MINB 5
 #endif
-  static constexpr int MINB3 = sizeof(T) == 4 ? SFFT_TRI_FINAL_MINB : 3;
+  static constexpr int MINB3 = sizeof(T) == 4 ? SFFT_TRI_FINAL_MINB : SFFT_TRI_FINAL_MINB_D;
   static_assert(MID >= LE2 && NT1 % EXL == 0 && NQ % NT3 == 0, "tri geometry");
 };
 
@@ -356,7 +362,7 @@ __device__ __forceinline__ int tri_pos(int m, int xa) {
 template <typename T> struct FrontTw { Cx<T> w[15]; };
 
 template <typename T, int S, int F>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? SFFT_TRI_FRONT_MINB : 1) k_tri_front(const PlanArgs args, const FrontTw<T> ftw,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? SFFT_TRI_FRONT_MINB : SFFT_TRI_FRONT_MINB_D) k_tri_front(const PlanArgs args, const FrontTw<T> ftw,
                                                                         Cx<T>* __restrict__ scratch, int64_t row0,
                                                                         int64_t nrows) {
   using TG = TriGeo<T, S, F>;
