@@ -30,10 +30,20 @@ namespace sfft {
 // One CTA per SPC signals, no per-CTA setup: the gather is the first thing
 // every thread does, the butterfly reads the plan's twiddles through L1,
 // and the block scheduler balances the grid over the 148 SMs.
+#ifndef SFFT_PLAN_E14
+#define SFFT_PLAN_E14 32
+#endif
+// slots per thread of the plan kernel (0: the type's default).  2^14-slot
+// complex64 rows (config 3) use 32 per thread: 512 threads, three register
+// passes (5 + 5 + 4 stages) instead of four, so the one CTA per SM spends
+// less time in the butterfly with its share of HBM idle (209 -> 197 us)
+template <typename T, int S> constexpr int plan_e() { return (sizeof(T) == 4 && S == 14) ? SFFT_PLAN_E14 : 0; }
+
 template <typename T, int S>
-__global__ void __launch_bounds__(Geo<T, S>::NT, Geo<T, S>::MINB)
+__global__ void __launch_bounds__(Geo<T, S, plan_e<T, S>()>::NT, Geo<T, S, plan_e<T, S>()>::MINB)
 k_hidft_plan(const PlanArgs args) {
-  using G = Geo<T, S>;
+  constexpr int EO = plan_e<T, S>();
+  using G = Geo<T, S, EO>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<T>* sdata = reinterpret_cast<Cx<T>*>(smem_raw);
   pdl_release();  // the next launch may start gathering (its inputs are checked on the host)
@@ -56,15 +66,15 @@ k_hidft_plan(const PlanArgs args) {
     const uint32_t rsh = args.nshift == 1 ? 0u : (uint32_t)(b % args.nshift);
     const uint32_t base = args.identity ? 0u : ((args.negshift - rsh) & nmask);
     if (sizeof(T) == 8 && args.in_c64)
-      gather<T, S, float>(v, t, reinterpret_cast<const Cx<float>*>(args.sig) + bs * args.ld, d, base, nmask);
+      gather<T, S, float, EO>(v, t, reinterpret_cast<const Cx<float>*>(args.sig) + bs * args.ld, d, base, nmask);
     else
-      gather<T, S>(v, t, reinterpret_cast<const Cx<T>*>(args.sig) + bs * args.ld, d, base, nmask);
+      gather<T, S, T, EO>(v, t, reinterpret_cast<const Cx<T>*>(args.sig) + bs * args.ld, d, base, nmask);
   } else {
 #pragma unroll
     for (int x = 0; x < G::E; ++x) v[x] = Cx<T>{T(0), T(0)};
   }
   Cx<T>* sd = sdata + g * G::A;
-  butterfly<T, S>(v, t, sd, reinterpret_cast<const Cx<T>*>(args.tw));
+  butterfly<T, S, false, EO>(v, t, sd, reinterpret_cast<const Cx<T>*>(args.tw));
   pdl_wait();  // earlier launches in the stream complete before the first store (see plan_pdl)
   if (live) {
     const T scale = (T)args.scale1;
@@ -135,7 +145,7 @@ bool pdl_join(cudaStream_t st, const ByteRange* in, int nin, const ByteRange* ou
 
 template <typename T, int S>
 static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {
-  using G = Geo<T, S>;
+  using G = Geo<T, S, plan_e<T, S>()>;
   constexpr size_t smem = plan_smem<T, S>();
   static_assert(smem <= 227 * 1024, "plan kernel smem");
   auto kern = k_hidft_plan<T, S>;
