@@ -556,6 +556,127 @@ __global__ void k_tri_tables(const Cx<T>* __restrict__ tw, const int32_t* __rest
       tw_fin[((1 << t) - 1 + c) * nq + pi] = tw[((int64_t)1 << (sq + t)) - 1 + (q | ((int64_t)c << sq))];
 }
 
+// Bank-conflict-free layout for the complex64 middle pass (sfft_split.cu,
+// k_tri_mid).  Its last register pass stores one value per lane per warp
+// instruction (group "store": a half-warp's 16 lanes for register x) and its
+// epilogue reads consecutive pi, i.e. q = perm[pi] (group "read": 16
+// consecutive pi).  8 B accesses are served per half-warp, conflict-free
+// when its 16 lanes hit the 16 word slots (position mod 16) once each.  The
+// q's form a 16-regular bipartite multigraph between store groups and read
+// groups (edge q); four Euler splits (alternate the edges of closed trails:
+// every vertex keeps half its edges on each side) cut it into 16 perfect
+// matchings, and matching c becomes word slot c: position = 16 * (rank of q
+// within class c) + c.  Host code, once per plan.
+static void euler_split(const std::vector<int>& edges, const std::vector<int>& eu, const std::vector<int>& ev,
+                        int nv, std::vector<int>& A, std::vector<int>& B) {
+  // vertices 0..nv-1 (stores) and nv..2nv-1 (reads)
+  std::vector<std::vector<int>> adj(2 * nv);
+  for (int e : edges) {
+    adj[eu[e]].push_back(e);
+    adj[nv + ev[e]].push_back(e);
+  }
+  std::vector<char> used(eu.size(), 0);
+  std::vector<size_t> ptr(2 * nv, 0);
+  for (int start = 0; start < 2 * nv; ++start) {
+    for (;;) {
+      while (ptr[start] < adj[start].size() && used[adj[start][ptr[start]]]) ++ptr[start];
+      if (ptr[start] == adj[start].size()) break;
+      // closed trail from start, labels alternate A, B, A, ...
+      int v = start, side = 0;
+      for (;;) {
+        while (ptr[v] < adj[v].size() && used[adj[v][ptr[v]]]) ++ptr[v];
+        if (ptr[v] == adj[v].size()) break;  // back at start with nothing left (degrees are even)
+        const int e = adj[v][ptr[v]];
+        used[e] = 1;
+        (side ? B : A).push_back(e);
+        side ^= 1;
+        v = (v < nv) ? nv + ev[e] : eu[e];
+      }
+    }
+  }
+}
+
+static int tri_conflict_free_tables(sfft_plan* p, cudaStream_t st) {
+  const int s = p->s;
+  const int F = s == 15 ? 3 : 4, L = 4, MID = s - F - L, SQ = s - L;
+  const int NQ = 1 << SQ, EX = 1 << F, LE = 4, E2 = std::min(16, 1 << MID), NT = NQ / E2;
+  const int NPASS = (MID + LE - 1) / LE, last = NPASS - 1;
+  if (MID < LE || NQ % 32 || NT % 32) return SFFT_OK;
+  std::vector<int32_t> perm(NQ), pinv(NQ);
+  SFFT_CUDA(cudaMemcpyAsync(perm.data(), p->d_tri_perm, 4 * (size_t)NQ, cudaMemcpyDeviceToHost, st));
+  SFFT_CUDA(cudaStreamSynchronize(st));
+  for (int pi = 0; pi < NQ; ++pi) pinv[perm[pi]] = pi;
+  // q stored by thread tid from register x in the last pass (k_tri_mid: a = tid & (EX-1), mr = tid >> F)
+  const int w0 = (last * LE < MID - LE) ? last * LE : MID - LE;
+  std::vector<int> eu(NQ), ev(NQ), qof(NQ);  // edge index = x * NT + tid
+  for (int x = 0; x < E2; ++x)
+    for (int tid = 0; tid < NT; ++tid) {
+      const int a = tid & (EX - 1), mr = tid >> F;
+      const int slot = (mr & ((1 << w0) - 1)) | ((mr >> w0) << (w0 + LE)) | (x << w0);
+      const int q = (slot << F) | a;
+      const int e = x * NT + tid;
+      qof[e] = q;
+      eu[e] = (tid >> 4) * E2 + x;  // store group: a half-warp's lanes for register x
+      ev[e] = pinv[q] >> 4;         // read group: 16 consecutive pi
+    }
+  const int nv = NQ / 16;
+  std::vector<std::vector<int>> cls(1);
+  cls[0].resize(NQ);
+  for (int e = 0; e < NQ; ++e) cls[0][e] = e;
+  for (int lvl = 0; lvl < 4; ++lvl) {
+    std::vector<std::vector<int>> next;
+    for (auto& c : cls) {
+      std::vector<int> A, B;
+      euler_split(c, eu, ev, nv, A, B);
+      next.push_back(std::move(A));
+      next.push_back(std::move(B));
+    }
+    cls.swap(next);
+  }
+  std::vector<int32_t> posq(NQ, -1), spos(NQ), ppos(NQ);
+  for (int c = 0; c < 16; ++c) {
+    if ((int)cls[c].size() != NQ / 16) return SFFT_OK;  // not balanced: keep the swizzled layout
+    for (int r = 0; r < (int)cls[c].size(); ++r) posq[qof[cls[c][r]]] = 16 * r + c;
+  }
+  for (int e = 0; e < NQ; ++e) spos[e] = posq[qof[e]];
+  for (int pi = 0; pi < NQ; ++pi) ppos[pi] = posq[perm[pi]];
+  // check: a bijection, and every store / read half-warp hits each word slot once
+  {
+    std::vector<char> seen(NQ, 0);
+    for (int q = 0; q < NQ; ++q) {
+      if (posq[q] < 0 || posq[q] >= NQ || seen[posq[q]]) return SFFT_OK;
+      seen[posq[q]] = 1;
+    }
+    for (int g = 0; g < NQ / 16; ++g) {
+      int cs[16] = {0}, cr[16] = {0};
+      for (int l = 0; l < 16; ++l) {
+        const int x = g % E2, h = g / E2;
+        ++cs[spos[x * NT + h * 16 + l] & 15];
+        ++cr[ppos[g * 16 + l] & 15];
+      }
+      for (int c = 0; c < 16; ++c)
+        if (cs[c] != 1 || cr[c] != 1) return SFFT_OK;
+    }
+  }
+  int32_t* ds = nullptr;
+  int32_t* dp = nullptr;
+  SFFT_CUDA(cudaMalloc((void**)&ds, 4 * (size_t)NQ));
+  if (cudaMalloc((void**)&dp, 4 * (size_t)NQ) != cudaSuccess) {
+    cudaFree(ds);
+    return cuda_fail(cudaGetLastError(), "conflict-free table allocation");
+  }
+  cudaError_t e1 = cudaMemcpy(ds, spos.data(), 4 * (size_t)NQ, cudaMemcpyHostToDevice);
+  cudaError_t e2 = cudaMemcpy(dp, ppos.data(), 4 * (size_t)NQ, cudaMemcpyHostToDevice);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaFree(ds);
+    cudaFree(dp);
+    return cuda_fail(e1 != cudaSuccess ? e1 : e2, "conflict-free table upload");
+  }
+  p->d_tri_spos = ds;
+  p->d_tri_ppos = dp;
+  return SFFT_OK;
+}
+
 static void plan_free(sfft_plan* p) {
   if (!p) return;
   cudaFree(p->d_element_slots);
@@ -578,6 +699,8 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_tri_tw);
   cudaFree(p->d_tri_inv_elem);
   cudaFree(p->d_tri_inv_node);
+  cudaFree(p->d_tri_spos);
+  cudaFree(p->d_tri_ppos);
   cudaFree(p->d_J);
   delete p;
 }
@@ -736,6 +859,11 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     return done(cuda_fail(cudaGetLastError(), "plan build"));
   p->n_nodes = (int64_t)h[0];
   p->mu_star = (int64_t)h[1];
+  static const bool cf = [] {
+    const char* e = getenv("SFFT_TRI_CF");
+    return !(e && atoi(e) == 0);
+  }();
+  if (p->d_tri_perm && dtype == SFFT_C64 && cf && (rc = tri_conflict_free_tables(p, st))) return done(rc);
   *out_plan = p;
   return SFFT_OK;
 }

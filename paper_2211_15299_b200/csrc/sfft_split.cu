@@ -331,7 +331,7 @@ struct TriGeo {
   static constexpr int LE2 = ilog2c(E2), NT2 = NQ / E2;
   static constexpr int NPASS2 = (MID + LE2 - 1) / LE2;
   static constexpr int NTW2 = NQ - EX;  // stage-major twiddles of stages F+1 .. S-L
-  static constexpr size_t SMEM2 = (size_t)NQ * sizeof(Cx<T>) + (size_t)NTW2 * sizeof(Cx<T>) + (size_t)NQ * 4;
+  static constexpr size_t SMEM2 = (size_t)NQ * sizeof(Cx<T>) + (size_t)NTW2 * sizeof(Cx<T>) + (size_t)NQ * 4 * 2;
   // final
   static constexpr int NT3 = 128, NQB = NQ / NT3;
 #ifndef SFFT_TRI_FINAL_MINB
@@ -488,18 +488,26 @@ template <typename T, int S, int F>
 __global__ void __launch_bounds__(TriGeo<T, S, F>::NT2) k_tri_mid(const Cx<T>* __restrict__ scr1,
                                                                   Cx<T>* __restrict__ scr2, int64_t nrows,
                                                                   const Cx<T>* __restrict__ tw,
-                                                                  const int32_t* __restrict__ perm) {
+                                                                  const int32_t* __restrict__ perm,
+                                                                  const int32_t* __restrict__ spos,
+                                                                  const int32_t* __restrict__ ppos) {
   using TG = TriGeo<T, S, F>;
   constexpr int EX = TG::EX, MID = TG::MID, NQ = TG::NQ, SQ = TG::SQ, L = TG::L, E = TG::E2, LE = TG::LE2,
                 NT = TG::NT2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<T>* sd = reinterpret_cast<Cx<T>*>(smem_raw);  // NQ, swizzled local slot l = (m << F) | x'
   Cx<T>* stw = sd + NQ;                             // stage-major twiddles of stages F+1 .. S-L
-  int32_t* sperm = reinterpret_cast<int32_t*>(stw + TG::NTW2);
+  int32_t* sperm = reinterpret_cast<int32_t*>(stw + TG::NTW2);  // perm, or ppos with the conflict-free layout
+  int32_t* sspos = sperm + NQ;                                  // spos (conflict-free layout only)
   const int tid = threadIdx.x;
+  // conflict-free layout (plan->d_tri_spos / d_tri_ppos, sfft_plan.cu): the
+  // last pass stores at spos and the epilogue reads pi at ppos[pi]
+  const bool cf = spos != nullptr;
   // tables staged asynchronously (cp.async) while the first unit's block loads
   for (int i = tid; i < TG::NTW2; i += NT) cp_async_elem(stw + i, tw + EX - 1 + i);
-  for (int i = tid; i < NQ / 4; i += NT) cp_async16(sperm + 4 * i, perm + 4 * i);
+  for (int i = tid; i < NQ / 4; i += NT) cp_async16(sperm + 4 * i, (cf ? ppos : perm) + 4 * i);
+  if (cf)
+    for (int i = tid; i < NQ / 4; i += NT) cp_async16(sspos + 4 * i, spos + 4 * i);
   cp_async_commit();
   const int a = tid & (EX - 1), mr = tid >> F;
   const int64_t units = nrows << L;
@@ -539,15 +547,21 @@ __global__ void __launch_bounds__(TriGeo<T, S, F>::NT2) k_tri_mid(const Cx<T>* _
           bfly(v[x], v[x | (1 << lb)], stw[(1 << (F + beta)) - EX + h]);
         }
       }
+      if (cf && ps == TG::NPASS2 - 1) {
+        if (ps > 0) __syncthreads();  // every thread has read this pass's inputs from sd
 #pragma unroll
-      for (int x = 0; x < E; ++x) sd[swz<T, SQ>((slot_of<MID, LE>(ps, mr, x) << F) | a)] = v[x];
+        for (int x = 0; x < E; ++x) sd[sspos[x * NT + tid]] = v[x];
+      } else {
+#pragma unroll
+        for (int x = 0; x < E; ++x) sd[swz<T, SQ>((slot_of<MID, LE>(ps, mr, x) << F) | a)] = v[x];
+      }
       __syncthreads();
     }
     Cx<T>* dst = scr2 + ((u >> L) << S) + ((u & (TG::EXL - 1)) << SQ);
 #pragma unroll
     for (int n = 0; n < E; ++n) {
       const int pi = tid + n * NT;
-      dst[pi] = sd[swz<T, SQ>(sperm[pi])];
+      dst[pi] = cf ? sd[sperm[pi]] : sd[swz<T, SQ>(sperm[pi])];
     }
     __syncthreads();  // sd is rewritten by the next unit
   }
@@ -855,7 +869,7 @@ static int run_tri(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, c
     const int64_t g2 = std::min<int64_t>(n << TG::L, sms * occ2);
     if (e == cudaSuccess)
       e = launch_k(mid, (unsigned)g2, TG::NT2, TG::SMEM2, st, pdl, (const Cx<T>*)s1, s2, n, tw,
-                   (const int32_t*)p->d_tri_perm);
+                   (const int32_t*)p->d_tri_perm, (const int32_t*)p->d_tri_spos, (const int32_t*)p->d_tri_ppos);
     const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / TG::NQB));
     if (e == cudaSuccess)
       e = launch_k(fin, (unsigned)(nper * TG::NQB), TG::NT3, 0, st, pdl, a, (const Cx<T>*)s2, r0, n, nper, twf,
