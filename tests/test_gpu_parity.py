@@ -792,3 +792,44 @@ def test_back_to_back_fused_chain(S, torch):
         assert int(st.max()) == 0
     want = np.fft.fft(f.cpu().numpy().astype(np.complex128), axis=1)
     assert rel_l2(ref[1].cpu().numpy(), want) < 1e-5
+
+
+_PDL_RUN = r"""
+import sys
+import numpy as np
+import torch
+import paper_2211_15299_b200 as S
+from paper_2211_15299_b200 import workloads as W
+outs = []
+for cfg, B in ((2, 64), (4, 48), (5, 3)):
+    wl = W.make_workload(cfg, B=B)
+    sig = torch.empty((wl.B, wl.N), dtype=torch.complex64, device="cuda")
+    W.synthesize_into(sig, wl.support, wl.coeffs)
+    J = S.SupportSet(wl.N, wl.support) if wl.support.ndim == 1 else torch.from_numpy(wl.support).cuda()
+    out = torch.empty((wl.B, wl.k), dtype=torch.complex64, device="cuda")
+    for _ in range(8):  # back-to-back calls into one output buffer
+        S.hidft_to_dft_batched(sig, J, out=out)
+    torch.cuda.synchronize()
+    outs.append(out.cpu().numpy())
+np.savez(sys.argv[1], *outs)
+"""
+
+
+def test_pdl_on_off_bitwise(S, tmp_path):
+    """The PDL overlap between consecutive calls changes timing only: the
+    results with SFFT_PDL=0 (every launch fully stream-ordered) are bitwise
+    identical (configs 2, 4, 5 shapes, back-to-back calls)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for pdl in ("1", "0"):
+        path = str(tmp_path / f"pdl{pdl}.npz")
+        env = dict(os.environ, PYTHONPATH=root, SFFT_PDL=pdl, SFFT_TRI_PDL=pdl)
+        out = subprocess.run([sys.executable, "-c", _PDL_RUN, path], env=env, capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, out.stderr
+        res[pdl] = np.load(path)
+    for key in res["1"].files:
+        assert np.array_equal(res["1"][key], res["0"][key]), key
