@@ -45,5 +45,12 @@ fb = fb.cpu().numpy() if hasattr(fb, "cpu") else np.asarray(fb)
 S.sas_transform(np.stack([fb, fb]), Jb, policy="random_subset", family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
 S.sas_transform(torch.from_numpy(np.stack([fb, fb])).cuda(), Jb, policy="random_subset",
                 family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
+# back-to-back calls (programmatic dependent launch chain), 2^14-slot plan kernel (32 slots per thread)
+for _ in range(3):
+    S.hidft_to_dft_batched(f, Js)
+    S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J3))
+J5 = O.gen_homogeneous(sorted(rng.choice(20, size=14, replace=False).tolist()), 20, 6)
+S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J5))
+S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J5))
 torch.cuda.synchronize()
 print("sanitize case ok")
