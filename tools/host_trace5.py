@@ -1,3 +1,4 @@
+"""SFFT_HOST_TRACE timeline of the config-5 public call on 64 page-locked host rows, plus Python-side costs."""
 import os, sys, time, torch
 sys.path.insert(0, os.getcwd())
 import paper_2211_15299_b200 as S
