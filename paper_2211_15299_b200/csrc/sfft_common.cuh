@@ -43,6 +43,36 @@ __device__ __forceinline__ void bfly(Cx<double>& u, Cx<double>& v, Cx<double> w)
   v = {px, py};
 }
 
+// Packed-fp32 butterfly (sm_100 FFMA2: two fp32 FMAs per instruction).  With
+// w v = v.x w + v.y (i w), i w = (-w.y, w.x):  p = u + v.x w + v.y iw,
+// u' = 2u - p: three FFMA2 instead of six FFMA (same roundings as bfly).
+// iw is passed in so that a twiddle shared by several butterflies is
+// rotated once.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ Cx<float> upk2(unsigned long long r) {
+  Cx<float> v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ Cx<float> rot_i(Cx<float> w) { return {-w.y, w.x}; }
+__device__ __forceinline__ void bfly2(Cx<float>& u, Cx<float>& v, Cx<float> w, Cx<float> iw) {
+  const unsigned long long U = pk2(u.x, u.y);
+  unsigned long long P = ffma2(pk2(v.x, v.x), pk2(w.x, w.y), U);
+  P = ffma2(pk2(v.y, v.y), pk2(iw.x, iw.y), P);
+  const Cx<float> p = upk2(P);
+  u = upk2(ffma2(pk2(2.f, 2.f), U, pk2(-p.x, -p.y)));
+  v = p;
+}
+
 // Streaming sample loads: one sector per sample in the sparse patterns, no
 // reuse through L1, so bypass L1 allocation.
 __device__ __forceinline__ Cx<float> load_sample(const Cx<float>* p) {

@@ -183,7 +183,15 @@ inline int kernel_occupancy(K kernel, int nt, size_t smem, int* occ) {
   SFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int o = 0;
   SFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, nt, smem));
-  if (o < 1) return fail(SFFT_ERR_UNSUPPORTED, "kernel does not fit on an SM");
+  if (o < 1) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kernel);
+    return fail(SFFT_ERR_UNSUPPORTED, "kernel does not fit on an SM (" + std::to_string(nt) + " threads x " +
+                                          std::to_string(fa.numRegs) + " registers, " + std::to_string(smem) +
+                                          " B dynamic + " + std::to_string(fa.sharedSizeBytes) +
+                                          " B static shared memory, max threads " +
+                                          std::to_string(fa.maxThreadsPerBlock) + ")");
+  }
   std::lock_guard<std::mutex> lk(g_kmu);
   g_occ[key] = o;
   *occ = o;

@@ -14,6 +14,9 @@
 #include <mutex>
 #include <string>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "sfft_kernels.cuh"
 
 namespace sfft {
@@ -881,6 +884,396 @@ static int run_tri(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, c
   return SFFT_OK;
 }
 
+// ------------------------------------------ TMA head + final (two-pass) ---
+//
+// The three-pass split reads whole 128 B lines in its front pass and needs a
+// middle pass (a second L2 round trip) because the first 12 stages run
+// across the lines of the pattern.  The head pass does the front's and the
+// middle's work in one kernel: slot a = (b << SQ) | q, and when the two
+// smallest sample strides are 1 and 2 (config 5: pivots M-1, M-2 present)
+// the 16 values of a q sit in one 128 B line, b's low-offset bits in the
+// line's low positions.  A CTA owns a unit (row, c): the P values of every
+// line at offset off_c (P = 2: 16 B, 8 units per row; P = 4: 32 B, 4 units),
+// i.e. P independent 2^SQ-slot transforms over q.  Its samples are fetched
+// by TMA: the q bits of the pattern form runs of consecutive strides, the
+// three longest runs become dims 1-3 of a rank-5 tensor map over the signal
+// batch (dim 0 = the P-element piece, dim 4 = the row) and the remaining q
+// bits are enumerated by one cp.async.bulk.tensor per combination, so the
+// LSU never issues a gather instruction.  The landing layout is a bit
+// permutation of q (HeadTma::qw); pass 0 reads it into registers, runs
+// stages 1-4 and continues with the swizzled single-CTA layout for stages
+// 5..SQ, and the epilogue writes scratch[row][b][pi] (pi: the final pass's
+// output order, coalesced).  The final pass (k_tri_final) is shared with
+// the three-pass split.  Reference: hidft.py:34-49 (gather), 160-167.
+struct HeadTma {
+  int nops, nleft, P;
+  uint32_t left_d[16];  // element offset of each enumerated (leftover) q bit
+  uint32_t k1, k2, k3;  // dim j covers element-offset bits [k_j, k_j+1) of the row (dim 0: [0, k1))
+  uint32_t qw[16];      // landing-layout weight of q bit i (in q units)
+  uint32_t dfix[4];     // element offset of b bit 0..3 (slot bits SQ..SQ+3)
+  int len[3];
+  uint8_t tq[16];       // pass-0 thread bit i -> q bit tq[i] (q bits LE.., ascending landing weight)
+};
+
+template <typename T, int S, int P>
+struct HeadGeo {
+  static constexpr int L = 4, SQ = S - L, NQ = 1 << SQ, NC = 16 / P;
+  static constexpr int E = 16, LE = 4;       // slots per thread, one b value per thread
+  static constexpr int TPB = NQ / E;         // threads per b value
+  static constexpr int NT = P * TPB;         // transform threads
+  static constexpr int NTT = NT + 32;        // + one warp that issues the tensor copies
+  static constexpr int NPASS = (SQ + LE - 1) / LE;
+  static constexpr int NTW = NQ - 16;        // stage-major twiddles 15 .. NQ-2 (stages 5 .. SQ)
+  // landing buffer (TMA) + working buffer (swizzled slots) + twiddles + 2 mbarriers
+  static constexpr size_t SMEM = 2 * (size_t)P * NQ * sizeof(Cx<T>) + (size_t)NTW * sizeof(Cx<T>) + 16;
+  static_assert(sizeof(T) == 4 && SQ >= 2 * LE && E <= TPB, "head pass: complex64, at least 2 register passes");
+};
+
+// twiddles of stages 1..4 and their rotations i*w (uniform over the grid)
+struct FrontTw2 { Cx<float> w[15], iw[15]; };
+
+__device__ __forceinline__ void mbar_init(uint32_t a, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(a) : "memory");
+}
+// barrier among the NT transform threads only (the copy warp runs its own loop)
+template <int NT>
+__device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
+
+// Persistent: CTA i serves units i, i + grid, ...; a copy warp fills the
+// landing buffer with unit u+1 (tensor copies; it alone stalls when the TMA
+// queue is full) as soon as the transform threads have read unit u from it,
+// so the copies run while unit u is transformed in the working buffer.
+template <typename T, int S, int P>
+__global__ void __launch_bounds__(HeadGeo<T, S, P>::NTT, 1)
+k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 ftw, const Cx<T>* __restrict__ tw,
+       const int32_t* __restrict__ perm, Cx<T>* __restrict__ scratch, int64_t row0, int64_t units) {
+  using HG = HeadGeo<T, S, P>;
+  constexpr int SQ = HG::SQ, NQ = HG::NQ, E = HG::E, LE = HG::LE, TPB = HG::TPB, NT = HG::NT, NC = HG::NC;
+  constexpr int LP = P == 4 ? 2 : 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Cx<T>* land = reinterpret_cast<Cx<T>*>(smem_raw);  // P x NQ, TMA box order
+  Cx<T>* work = land + P * NQ;                       // P x NQ, swizzled slots per b value
+  Cx<T>* stw = work + P * NQ;                        // twiddles of stages 5 .. SQ
+  const uint32_t full = smem_addr(stw + HG::NTW), empty = full + 8;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(full, 1);
+    mbar_init(empty, NT / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= NT) {  // copy warp (signals are read-only: the first copies may overlap the previous kernel)
+    const int lane = tid - NT;
+    const int box = (NQ / ht.nops) * P;
+    uint32_t it = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+      if (it > 0) mbar_wait(empty, (it - 1) & 1);  // the transform threads have read the landing buffer
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(full), "r"((uint32_t)(P * NQ * sizeof(Cx<T>))) : "memory");
+      }
+      __syncwarp();
+      const int64_t rr = u / NC;
+      const int c = (int)(u % NC);
+      uint32_t offc = 0;
+#pragma unroll
+      for (int j = 0; j < 4 - LP; ++j)
+        if ((c >> j) & 1) offc += ht.dfix[j];
+      for (int o = lane; o < ht.nops; o += 32) {
+        uint32_t e = offc;
+        for (int j = 0; j < ht.nleft; ++j)
+          if ((o >> j) & 1) e += ht.left_d[j];
+        const int c0 = (int)(e & ((1u << ht.k1) - 1u));
+        const int c1 = (int)((e >> ht.k1) & ((1u << (ht.k2 - ht.k1)) - 1u));
+        const int c2 = (int)((e >> ht.k2) & ((1u << (ht.k3 - ht.k2)) - 1u));
+        const int c3 = (int)(e >> ht.k3);
+        const int c4 = (int)(row0 + rr);
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+            :: "r"(smem_addr(land + (size_t)o * box)), "l"(&tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+               "r"(full) : "memory");
+      }
+    }
+    return;
+  }
+  // Thread bits 4..4+LP-1 pick the b value inside the piece, so each
+  // half-warp works on one b value: its 16 lanes hit 16 distinct 8 B word
+  // slots in the swizzled passes (conflict-free); pass-0 thread bit i holds
+  // q bit tq[i] (host order: ascending landing weight).
+  for (int i = tid; i < HG::NTW; i += NT) cp_async_elem(stw + i, tw + 15 + i);
+  cp_async_commit();
+  const int bl = (tid >> 4) & (P - 1), tt = (tid & 15) | ((tid >> (4 + LP)) << 4);
+  uint32_t qt = 0, base = 0;
+#pragma unroll
+  for (int i = 0; i < SQ - LE; ++i)
+    if ((tt >> i) & 1) {
+      qt |= 1u << ht.tq[i];
+      base += ht.qw[ht.tq[i]];
+    }
+  const int tb0 = swz<T, SQ>((int)qt);
+  Cx<T>* sb = work + bl * NQ;
+  cp_async_wait<0>();
+  bool waited = false;
+  uint32_t it = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    Cx<T> v[E];
+    mbar_wait(full, it & 1);
+#pragma unroll
+    for (int x = 0; x < E; ++x) {
+      uint32_t q = base;
+#pragma unroll
+      for (int i = 0; i < LE; ++i)
+        if ((x >> i) & 1) q += ht.qw[i];
+      v[x] = land[q * P + bl];
+    }
+    work_sync<NT>();  // landing reads done; the previous unit's epilogue reads of work done
+    if ((tid & 31) == 0) mbar_arrive(empty);
+    // stages 1..LE: twiddle index a mod 2^beta = x mod 2^beta, uniform over the grid
+#pragma unroll
+    for (int beta = 0; beta < LE; ++beta) {
+#pragma unroll
+      for (int x = 0; x < E; ++x) {
+        if (x & (1 << beta)) continue;
+        const int j = (1 << beta) - 1 + (x & ((1 << beta) - 1));
+        bfly2(v[x], v[x | (1 << beta)], ftw.w[j], ftw.iw[j]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < E; ++x) sb[tb0 ^ swz<T, SQ>(x)] = v[x];
+    work_sync<NT>();
+#pragma unroll
+    for (int p = 1; p < HG::NPASS; ++p) {
+      const int tb = swz<T, SQ>(slot_t<SQ, LE>(p, tt));
+#pragma unroll
+      for (int x = 0; x < E; ++x) v[x] = sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))];
+      const int b0 = p * LE, b1 = (b0 + LE < SQ) ? b0 + LE : SQ, w0 = pass_w0(p, SQ, LE);
+#pragma unroll
+      for (int beta = b0; beta < b1; ++beta) {
+        const int lb = beta - w0;
+        // butterflies of this stage share twiddle h = a mod 2^beta: one per value of x's bits below lb
+#pragma unroll
+        for (int xl = 0; xl < (1 << lb); ++xl) {
+          const int a0 = slot_of<SQ, LE>(p, tt, xl);
+          const Cx<T> w = stw[(1 << beta) - 16 + (a0 & ((1 << beta) - 1))];
+          const Cx<T> iw = rot_i(w);
+#pragma unroll
+          for (int x = xl; x < E; x += (1 << lb)) {
+            if (x & (1 << lb)) continue;
+            bfly2(v[x], v[x | (1 << lb)], w, iw);
+          }
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < E; ++x) sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))] = v[x];  // in place: same positions
+      work_sync<NT>();
+    }
+    if (!waited) {
+      pdl_wait();  // scratch is free (the previous chunk's final pass completed)
+      pdl_release();
+      waited = true;
+    }
+    const int64_t rr = u / NC;
+    const int c = (int)(u % NC);
+    const int b = c | (LP == 1 ? (bl << 3) : (((bl & 1) << 3) | ((bl >> 1) << 2)));
+    Cx<T>* dst = scratch + ((int64_t)rr << S) + ((int64_t)b << SQ) + tt;
+#pragma unroll
+    for (int n = 0; n < E; ++n) dst[n * TPB] = sb[swz<T, SQ>(__ldg(perm + tt + n * TPB))];
+  }
+}
+
+// host: the tensor-map decomposition of a plan's pattern (false: not eligible)
+static bool head_plan(const sfft_plan* p, int P, HeadTma* ht) {
+  const int S = p->s, M = p->M, SQ = S - 4;
+  if (S < 12 || S > 20) return false;
+  std::memset(ht, 0, sizeof(*ht));
+  ht->P = P;
+  auto d = [&](int i) { return M - 1 - p->used[i]; };  // log2 of slot bit i's sample stride
+  if (d(S - 1) != 0 || (P == 4 && d(S - 2) != 1)) return false;
+  const int LP = P == 4 ? 2 : 1;
+  for (int j = 0; j < 4 - LP; ++j) ht->dfix[j] = 1u << d(SQ + j);
+  // runs of q bits with consecutive strides: q bit i has log-stride d(i), decreasing in i
+  struct Run { int lo, len; };  // element-offset bits [lo, lo+len)
+  std::vector<Run> runs;
+  for (int i = SQ - 1; i >= 0;) {
+    int j = i;
+    while (j - 1 >= 0 && d(j - 1) == d(j) + 1 && (i - j + 1) < 8) --j;
+    runs.push_back({d(i), i - j + 1});
+    i = j - 1;
+  }
+  std::vector<int> idx(runs.size());
+  for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return runs[a].len > runs[b].len; });
+  std::vector<Run> pick;
+  for (size_t i = 0; i < idx.size() && pick.size() < 3; ++i) pick.push_back(runs[idx[i]]);
+  std::sort(pick.begin(), pick.end(), [](const Run& a, const Run& b) { return a.lo < b.lo; });
+  while (pick.size() < 3) pick.push_back({M, 0});
+  ht->k1 = pick[0].lo;
+  ht->k2 = pick[1].lo;
+  ht->k3 = pick[2].lo;
+  if (ht->k1 < (uint32_t)LP) return false;
+  int boxq = 0;
+  for (int j = 0; j < 3; ++j) {
+    ht->len[j] = pick[j].len;
+    boxq += pick[j].len;
+  }
+  if (boxq < 3) return false;  // landing boxes of >= 128 B
+  // landing weights: run bits in box order, then the enumerated bits
+  int wpos = 0;
+  for (int j = 0; j < 3; ++j)
+    for (int t = 0; t < pick[j].len; ++t) {
+      const int e = pick[j].lo + t;
+      for (int i = 0; i < SQ; ++i)
+        if (d(i) == e) ht->qw[i] = 1u << (wpos + t);
+    }
+  for (int j = 0, w = 0; j < 3; ++j) {  // box order: run 0 lowest
+    for (int t = 0; t < pick[j].len; ++t)
+      for (int i = 0; i < SQ; ++i)
+        if (d(i) == pick[j].lo + t) ht->qw[i] = 1u << (w + t);
+    w += pick[j].len;
+  }
+  wpos = boxq;
+  for (int i = 0; i < SQ; ++i) {
+    bool in_run = false;
+    for (int j = 0; j < 3; ++j) in_run |= d(i) >= pick[j].lo && d(i) < pick[j].lo + pick[j].len;
+    if (in_run) continue;
+    ht->left_d[ht->nleft] = 1u << d(i);
+    ht->qw[i] = 1u << (wpos + ht->nleft);
+    ++ht->nleft;
+  }
+  ht->nops = 1 << ht->nleft;
+  std::vector<int> qb;
+  for (int i = 4; i < SQ; ++i) qb.push_back(i);
+  std::stable_sort(qb.begin(), qb.end(), [&](int a, int b) { return ht->qw[a] < ht->qw[b]; });
+  for (size_t i = 0; i < qb.size(); ++i) ht->tq[i] = (uint8_t)qb[i];
+  return ht->nleft <= 10;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+template <typename T, int S, int P>
+static int head_launches(int64_t rows, int64_t* n) {
+  const int64_t chunk = tri_chunk_rows(rows, sizeof(Cx<T>) << S);
+  *n = rows > 0 ? 2 * ((rows + chunk - 1) / chunk) : 0;
+  return SFFT_OK;
+}
+
+// 1: launched; 0: not eligible (caller falls back); <0 never; >1 error code
+template <typename T, int S, int P>
+static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st, bool* ran) {
+  using HG = HeadGeo<T, S, P>;
+  using TG = TriGeo<T, S, 4>;
+  *ran = false;
+  HeadTma ht;
+  if (!p->d_tri_perm || a.identity != 0 || a.nshift != 1 || a.negshift != 0 || a.in_c64 || a.debug_skip ||
+      (reinterpret_cast<uintptr_t>(a.sig) & 15) || ((a.ld * (int64_t)sizeof(Cx<T>)) & 15) || a.B > 0x7fffffff ||
+      !head_plan(p, P, &ht))
+    return SFFT_OK;
+  const int32_t* invf = inv1 == p->d_inv_elem ? p->d_tri_inv_elem
+                        : inv1 == p->d_inv_node ? p->d_tri_inv_node
+                                                : nullptr;
+  if (inv1 && !invf) return SFFT_OK;
+  auto enc = tensor_map_encoder();
+  if (!enc) return SFFT_OK;
+  CUtensorMap tm;
+  const cuuint64_t dims[5] = {(cuuint64_t)1 << ht.k1, (cuuint64_t)1 << (ht.k2 - ht.k1),
+                              (cuuint64_t)1 << (ht.k3 - ht.k2), (cuuint64_t)1 << (a.M - ht.k3), (cuuint64_t)a.B};
+  const cuuint64_t strides[4] = {(cuuint64_t)sizeof(Cx<T>) << ht.k1, (cuuint64_t)sizeof(Cx<T>) << ht.k2,
+                                 (cuuint64_t)sizeof(Cx<T>) << ht.k3, (cuuint64_t)(a.ld * (int64_t)sizeof(Cx<T>))};
+  const cuuint32_t box[5] = {(cuuint32_t)P, 1u << ht.len[0], 1u << ht.len[1], 1u << ht.len[2], 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_INT64, 5, const_cast<void*>(a.sig), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return SFFT_OK;
+  auto head = k_head<T, S, P>;
+  auto fin = k_tri_final<T, S, 4>;
+  int occ1 = 0, occ3 = 0, rc;
+  if ((rc = kernel_occupancy(head, HG::NTT, HG::SMEM, &occ1))) return rc;
+  if ((rc = kernel_occupancy(fin, TG::NT3, 0, &occ3))) return rc;
+  *ran = true;
+  const int64_t rows = a.B;
+  if (rows == 0) return SFFT_OK;
+  const size_t row_bytes = sizeof(Cx<T>) << S;
+  const int64_t chunk = tri_chunk_rows(rows, row_bytes);
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  void* scr = nullptr;
+  bool pooled = false;
+  if ((rc = stream_scratch(dev, st, (size_t)chunk * row_bytes, &scr, &pooled))) return rc;
+  const Cx<T>* tw = reinterpret_cast<const Cx<T>*>(p->d_twiddles);
+  const Cx<T>* twf = reinterpret_cast<const Cx<T>*>(p->d_tri_tw);
+  const int64_t sms = num_sms();
+  FrontTw2 ftw;
+  std::memcpy(ftw.w, p->tri_front_tw, sizeof(Cx<float>) * 15);
+  for (int j = 0; j < 15; ++j) ftw.iw[j] = Cx<float>{-ftw.w[j].y, ftw.w[j].x};
+  static const bool pdl = [] {
+    const char* e = getenv("SFFT_TRI_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  const ByteRange in[1] = {{(uintptr_t)a.sig, (uintptr_t)a.sig + (size_t)((a.B - 1) * a.ld + (1ll << a.M)) * sizeof(Cx<T>)}};
+  const ByteRange outs[2] = {
+      {(uintptr_t)a.out1, (uintptr_t)a.out1 + (size_t)((rows - 1) * a.ld1 + a.n1) * sizeof(Cx<T>)},
+      {(uintptr_t)a.out2, a.out2 ? (uintptr_t)a.out2 + (size_t)((rows - 1) * a.ld2 + (1ll << S)) * sizeof(Cx<T>) : 0}};
+  const bool pdl_first = pdl_join(st, in, 1, outs, 2, pdl && !pooled);
+  cudaError_t e = cudaSuccess;
+  for (int64_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += chunk) {
+    const int64_t n = std::min(chunk, rows - r0);
+    const int64_t units = n * HG::NC;
+    e = launch_k(head, (unsigned)std::min<int64_t>(units, sms * occ1), HG::NTT, HG::SMEM, st,
+                 pdl && (r0 > 0 || pdl_first), tm, ht, ftw, tw, (const int32_t*)p->d_tri_perm, (Cx<T>*)scr, r0,
+                 units);
+    const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / TG::NQB));
+    if (e == cudaSuccess)
+      e = launch_k(fin, (unsigned)(nper * TG::NQB), TG::NT3, 0, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
+                   invf, (const int32_t*)p->d_tri_perm);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (pooled) cudaFreeAsync(scr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "head transform launch");
+  return SFFT_OK;
+}
+
+// SFFT_HEAD=0 keeps the three-pass split; SFFT_HEAD_P selects the piece (2 or 4)
+static int head_mode() {
+  static const int v = [] {
+    const char* e = getenv("SFFT_HEAD");
+    if (e && atoi(e) == 0) return 0;
+    const char* q = getenv("SFFT_HEAD_P");
+    return (q && atoi(q) == 4) ? 4 : 2;
+  }();
+  return v;
+}
+
+static int try_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st, bool* ran) {
+  *ran = false;
+  const int P = head_mode();
+  if (P == 0 || p->dtype != SFFT_C64) return SFFT_OK;
+  switch (p->s) {
+    case 16: return P == 4 ? run_head<float, 16, 4>(p, a, inv1, st, ran) : run_head<float, 16, 2>(p, a, inv1, st, ran);
+    default: return SFFT_OK;
+  }
+}
+
 // SFFT_SPLIT_PASSES=2 selects the two-pass split (A/B measurements)
 static bool use_tri() {
   static const bool v = [] {
@@ -892,6 +1285,9 @@ static bool use_tri() {
 
 int run_large(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
   if (use_tri()) {
+    bool ran = false;
+    const int rc = try_head(p, a, inv1, st, &ran);
+    if (rc || ran) return rc;
     if (p->dtype == SFFT_C64) {
       switch (p->s) {
         case 15: return run_tri<float, 15, 3>(p, a, inv1, st);
@@ -928,6 +1324,9 @@ int run_large(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaSt
 
 int large_launch_count(const sfft_plan* p, int64_t rows, int64_t* launches) {
   if (use_tri()) {
+    HeadTma ht;
+    if (head_mode() && p->dtype == SFFT_C64 && p->s == 16 && p->d_tri_perm && head_plan(p, head_mode(), &ht))
+      return head_launches<float, 16, 2>(rows, launches);
     if (p->dtype == SFFT_C64) {
       switch (p->s) {
         case 15: return tri_launches<float, 15, 3>(rows, launches);
