@@ -864,6 +864,17 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     return !(e && atoi(e) == 0);
   }();
   if (p->d_tri_perm && dtype == SFFT_C64 && cf && (rc = tri_conflict_free_tables(p, st))) return done(rc);
+  if (p->d_tri_perm) {  // blocked output maps (k_fin2)
+    const int64_t nq = A >> 4;
+    std::vector<int32_t> inv(A);
+    for (int which = 0; which < 2; ++which) {
+      SFFT_CUDA(cudaMemcpy(inv.data(), which ? p->d_tri_inv_node : p->d_tri_inv_elem, 4 * (size_t)A,
+                           cudaMemcpyDeviceToHost));
+      bool ok = true;
+      for (int64_t i = 0; i < A && ok; ++i) ok = inv[i] >= 0 && (inv[i] & (nq - 1)) == (i & (nq - 1));
+      (which ? p->tri_blocked_node : p->tri_blocked_elem) = ok ? 1 : 0;
+    }
+  }
   *out_plan = p;
   return SFFT_OK;
 }

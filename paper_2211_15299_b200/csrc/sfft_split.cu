@@ -1091,6 +1091,233 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
   }
 }
 
+// In-place variant (SFFT_HEAD_IP=1): the landing buffer is also the working
+// buffer (64 KB + 32 KB of twiddles), so two CTAs share an SM and overlap
+// each other's phases; the next unit's copies are issued (by lane 0 of every
+// warp, NW-th share each) once the epilogue has read the buffer.
+template <typename T, int S, int P>
+struct HeadIpGeo {
+  using HG = HeadGeo<T, S, P>;
+  static constexpr size_t SMEM = (size_t)P * HG::NQ * sizeof(Cx<T>) + (size_t)HG::NTW * sizeof(Cx<T>) + 16;
+};
+
+template <typename T, int S, int P>
+__global__ void __launch_bounds__(HeadGeo<T, S, P>::NT, 2)
+k_head_ip(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 ftw, const Cx<T>* __restrict__ tw,
+          const int32_t* __restrict__ perm, Cx<T>* __restrict__ scratch, int64_t row0, int64_t units) {
+  using HG = HeadGeo<T, S, P>;
+  constexpr int SQ = HG::SQ, NQ = HG::NQ, E = HG::E, LE = HG::LE, TPB = HG::TPB, NT = HG::NT, NC = HG::NC;
+  constexpr int LP = P == 4 ? 2 : 1, NW = NT / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Cx<T>* land = reinterpret_cast<Cx<T>*>(smem_raw);  // P x NQ: TMA box order, then swizzled slots per b value
+  Cx<T>* stw = land + P * NQ;                        // twiddles of stages 5 .. SQ
+  const uint32_t full = smem_addr(stw + HG::NTW);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(full, NW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t u) {  // lane 0 of warp w: copies o = w, w + NW, ... of unit u
+    const int w = tid >> 5;
+    const int box = (NQ / ht.nops) * P;
+    const int mine = ht.nops > w ? (ht.nops - w + NW - 1) / NW : 0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(full), "r"((uint32_t)(mine * box * sizeof(Cx<T>))) : "memory");
+    const int64_t rr = u / NC;
+    const int c = (int)(u % NC);
+    uint32_t offc = 0;
+#pragma unroll
+    for (int j = 0; j < 4 - LP; ++j)
+      if ((c >> j) & 1) offc += ht.dfix[j];
+    for (int o = w; o < ht.nops; o += NW) {
+      uint32_t e = offc;
+      for (int j = 0; j < ht.nleft; ++j)
+        if ((o >> j) & 1) e += ht.left_d[j];
+      const int c0 = (int)(e & ((1u << ht.k1) - 1u));
+      const int c1 = (int)((e >> ht.k1) & ((1u << (ht.k2 - ht.k1)) - 1u));
+      const int c2 = (int)((e >> ht.k2) & ((1u << (ht.k3 - ht.k2)) - 1u));
+      const int c3 = (int)(e >> ht.k3);
+      const int c4 = (int)(row0 + rr);
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+          :: "r"(smem_addr(land + (size_t)o * box)), "l"(&tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+             "r"(full) : "memory");
+    }
+  };
+  if ((tid & 31) == 0 && blockIdx.x < units) issue(blockIdx.x);  // signals are read-only
+  for (int i = tid; i < HG::NTW; i += NT) cp_async_elem(stw + i, tw + 15 + i);
+  cp_async_commit();
+  const int bl = (tid >> 4) & (P - 1), tt = (tid & 15) | ((tid >> (4 + LP)) << 4);
+  uint32_t qt = 0, base = 0;
+#pragma unroll
+  for (int i = 0; i < SQ - LE; ++i)
+    if ((tt >> i) & 1) {
+      qt |= 1u << ht.tq[i];
+      base += ht.qw[ht.tq[i]];
+    }
+  const int tb0 = swz<T, SQ>((int)qt);
+  Cx<T>* sb = land + bl * NQ;
+  cp_async_wait<0>();
+  bool waited = false;
+  uint32_t it = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    Cx<T> v[E];
+    mbar_wait(full, it & 1);
+#pragma unroll
+    for (int x = 0; x < E; ++x) {
+      uint32_t q = base;
+#pragma unroll
+      for (int i = 0; i < LE; ++i)
+        if ((x >> i) & 1) q += ht.qw[i];
+      v[x] = land[q * P + bl];
+    }
+    __syncthreads();  // landing reads done (and, the first time, the tables staged)
+#pragma unroll
+    for (int beta = 0; beta < LE; ++beta) {
+#pragma unroll
+      for (int x = 0; x < E; ++x) {
+        if (x & (1 << beta)) continue;
+        const int j = (1 << beta) - 1 + (x & ((1 << beta) - 1));
+        bfly2(v[x], v[x | (1 << beta)], ftw.w[j], ftw.iw[j]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < E; ++x) sb[tb0 ^ swz<T, SQ>(x)] = v[x];
+    __syncthreads();
+#pragma unroll
+    for (int p = 1; p < HG::NPASS; ++p) {
+      const int tb = swz<T, SQ>(slot_t<SQ, LE>(p, tt));
+#pragma unroll
+      for (int x = 0; x < E; ++x) v[x] = sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))];
+      const int b0 = p * LE, b1 = (b0 + LE < SQ) ? b0 + LE : SQ, w0 = pass_w0(p, SQ, LE);
+#pragma unroll
+      for (int beta = b0; beta < b1; ++beta) {
+        const int lb = beta - w0;
+#pragma unroll
+        for (int xl = 0; xl < (1 << lb); ++xl) {
+          const int a0 = slot_of<SQ, LE>(p, tt, xl);
+          const Cx<T> w = stw[(1 << beta) - 16 + (a0 & ((1 << beta) - 1))];
+          const Cx<T> iw = rot_i(w);
+#pragma unroll
+          for (int x = xl; x < E; x += (1 << lb)) {
+            if (x & (1 << lb)) continue;
+            bfly2(v[x], v[x | (1 << lb)], w, iw);
+          }
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < E; ++x) sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))] = v[x];
+      __syncthreads();
+    }
+#pragma unroll
+    for (int n = 0; n < E; ++n) v[n] = sb[swz<T, SQ>(__ldg(perm + tt + n * TPB))];
+    __syncthreads();  // the buffer is free: the next unit's copies may land
+    if ((tid & 31) == 0 && u + gridDim.x < units) issue(u + gridDim.x);
+    if (!waited) {
+      pdl_wait();  // scratch is free (the previous chunk's final pass completed)
+      pdl_release();
+      waited = true;
+    }
+    const int64_t rr = u / NC;
+    const int c = (int)(u % NC);
+    const int b = c | (LP == 1 ? (bl << 3) : (((bl & 1) << 3) | ((bl >> 1) << 2)));
+    Cx<T>* dst = scratch + ((int64_t)rr << S) + ((int64_t)b << SQ) + tt;
+#pragma unroll
+    for (int n = 0; n < E; ++n) dst[n * TPB] = v[n];
+  }
+}
+
+// Final pass of the head path: as k_tri_final (a thread owns position pi for
+// the rows of its CTA; 15 twiddles per pi, last 4 stages in registers) with
+// FFMA2 butterflies and, when the plan's output map is blocked (output of
+// slot (b, q) at T * 2^(S-4) + pi(q) for a per-q bijection b -> T: config 5,
+// whose top four pivots are the top bits of j), stores staged per warp in
+// shared memory so that each store instruction writes 32 consecutive
+// outputs of one block T instead of 32 scattered ones.
+template <typename T, int S>
+struct Fin2Geo {
+  static constexpr int L = 4, EXL = 16, SQ = S - L, NQ = 1 << SQ, NT = 128, NW = NT / 32, NQB = NQ / NT;
+  static constexpr size_t SMEM = (size_t)2 * (EXL - 1) * NT * sizeof(Cx<T>) + (size_t)NW * EXL * 32 * sizeof(Cx<T>);
+};
+
+template <typename T, int S>
+__global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T>* __restrict__ scr2, int64_t row0,
+                                                 int64_t nrows, int nper, const Cx<T>* __restrict__ twf,
+                                                 const int32_t* __restrict__ invf, const int32_t* __restrict__ perm,
+                                                 int blocked) {
+  using FG = Fin2Geo<T, S>;
+  constexpr int NQ = FG::NQ, SQ = FG::SQ, EXL = FG::EXL, L = FG::L, NT = FG::NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<T>* sw = reinterpret_cast<Cx<T>*>(smem_raw);  // [j][tid] twiddles of this CTA's pi block
+  Cx<T>* siw = sw + (EXL - 1) * NT;                   // [j][tid] i * twiddle
+  Cx<T>* stg = siw + (EXL - 1) * NT;                  // [warp][T][lane] output staging
+  const int qb = blockIdx.x % FG::NQB;
+  const int64_t first = blockIdx.x / FG::NQB;
+  if (first >= nrows) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pi = qb * NT + threadIdx.x;
+  Cx<T>* st = stg + wid * EXL * 32;
+  Cx<T> nx[EXL];
+  auto fetch = [&](int64_t rr) {
+    const Cx<T>* src = scr2 + (rr << S) + pi;
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) nx[b] = ld_cs(src + ((int64_t)b << SQ));
+  };
+#pragma unroll
+  for (int j = 0; j < EXL - 1; ++j) {  // read by this thread only
+    const Cx<T> w = twf[(int64_t)j * NQ + pi];
+    sw[j * NT + threadIdx.x] = w;
+    siw[j * NT + threadIdx.x] = Cx<T>{-w.y, w.x};
+  }
+  int32_t e[EXL];
+  const int q = perm[pi];
+#pragma unroll
+  for (int b = 0; b < EXL; ++b) {
+    e[b] = invf ? invf[(int64_t)b * NQ + pi] : ((b << SQ) | q);
+    if (blocked) e[b] >>= SQ;  // block T of value b
+  }
+  pdl_wait();  // scratch written by this chunk's head pass
+  pdl_release();
+  fetch(first);
+  const T scale = (T)args.scale1;
+  const int pib = qb * NT + wid * 32;  // this warp's first pi
+  for (int64_t rr = first; rr < nrows; rr += nper) {
+    Cx<T> v[EXL];
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) v[b] = nx[b];
+    if (rr + nper < nrows) fetch(rr + nper);
+#pragma unroll
+    for (int t = 0; t < L; ++t) {  // global stage SQ + t + 1 pairs slot bit SQ + t = b bit t
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) {
+        if (b & (1 << t)) continue;
+        const int j = (1 << t) - 1 + (b & ((1 << t) - 1));
+        bfly2(v[b], v[b | (1 << t)], sw[j * NT + threadIdx.x], siw[j * NT + threadIdx.x]);
+      }
+    }
+    const int64_t r = row0 + rr;
+    Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + r * args.ld1;
+    if (blocked) {
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) st[e[b] * 32 + lane] = cscale(v[b], scale);
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < EXL; ++t) st_cs(o1 + ((int64_t)t << SQ) + pib + lane, st[t * 32 + lane]);
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) st_cs_if(o1, e[b], cscale(v[b], scale));
+    }
+    if (args.out2) {
+      Cx<T>* o2 = reinterpret_cast<Cx<T>*>(args.out2) + r * args.ld2;
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) o2[(b << SQ) | q] = v[b];
+    }
+  }
+}
+
 // host: the tensor-map decomposition of a plan's pattern (false: not eligible)
 static bool head_plan(const sfft_plan* p, int P, HeadTma* ht) {
   const int S = p->s, M = p->M, SQ = S - 4;
@@ -1181,7 +1408,6 @@ static int head_launches(int64_t rows, int64_t* n) {
 template <typename T, int S, int P>
 static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st, bool* ran) {
   using HG = HeadGeo<T, S, P>;
-  using TG = TriGeo<T, S, 4>;
   *ran = false;
   HeadTma ht;
   if (!p->d_tri_perm || a.identity != 0 || a.nshift != 1 || a.negshift != 0 || a.in_c64 || a.debug_skip ||
@@ -1206,10 +1432,19 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return SFFT_OK;
   auto head = k_head<T, S, P>;
-  auto fin = k_tri_final<T, S, 4>;
+  auto fin = k_fin2<T, S>;
+  using FG = Fin2Geo<T, S>;
   int occ1 = 0, occ3 = 0, rc;
   if ((rc = kernel_occupancy(head, HG::NTT, HG::SMEM, &occ1))) return rc;
-  if ((rc = kernel_occupancy(fin, TG::NT3, 0, &occ3))) return rc;
+  static const bool ip = [] {
+    const char* e = getenv("SFFT_HEAD_IP");
+    return e && atoi(e) == 1;
+  }();
+  auto head_ip = k_head_ip<T, S, P>;
+  int occ_ip = 0;
+  if (ip && (rc = kernel_occupancy(head_ip, HG::NT, HeadIpGeo<T, S, P>::SMEM, &occ_ip))) return rc;
+  if ((rc = kernel_occupancy(fin, FG::NT, FG::SMEM, &occ3))) return rc;
+  const int blocked = inv1 == p->d_inv_elem ? p->tri_blocked_elem : inv1 == p->d_inv_node ? p->tri_blocked_node : 0;
   *ran = true;
   const int64_t rows = a.B;
   if (rows == 0) return SFFT_OK;
@@ -1239,13 +1474,18 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
   for (int64_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += chunk) {
     const int64_t n = std::min(chunk, rows - r0);
     const int64_t units = n * HG::NC;
-    e = launch_k(head, (unsigned)std::min<int64_t>(units, sms * occ1), HG::NTT, HG::SMEM, st,
-                 pdl && (r0 > 0 || pdl_first), tm, ht, ftw, tw, (const int32_t*)p->d_tri_perm, (Cx<T>*)scr, r0,
-                 units);
-    const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / TG::NQB));
+    if (ip)
+      e = launch_k(head_ip, (unsigned)std::min<int64_t>(units, sms * occ_ip), HG::NT, HeadIpGeo<T, S, P>::SMEM, st,
+                   pdl && (r0 > 0 || pdl_first), tm, ht, ftw, tw, (const int32_t*)p->d_tri_perm, (Cx<T>*)scr, r0,
+                   units);
+    else
+      e = launch_k(head, (unsigned)std::min<int64_t>(units, sms * occ1), HG::NTT, HG::SMEM, st,
+                   pdl && (r0 > 0 || pdl_first), tm, ht, ftw, tw, (const int32_t*)p->d_tri_perm, (Cx<T>*)scr, r0,
+                   units);
+    const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / FG::NQB));
     if (e == cudaSuccess)
-      e = launch_k(fin, (unsigned)(nper * TG::NQB), TG::NT3, 0, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
-                   invf, (const int32_t*)p->d_tri_perm);
+      e = launch_k(fin, (unsigned)(nper * FG::NQB), FG::NT, FG::SMEM, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
+                   invf, (const int32_t*)p->d_tri_perm, blocked);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (pooled) cudaFreeAsync(scr, st);
