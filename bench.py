@@ -6,19 +6,24 @@ coeffs/s = B*k/s, and the fraction of the HBM-gather roofline).
 
 A step is one pass of the hot path -- hidft(f_b, J, pivots(J)) +
 hidft_to_dft for every signal of the batch -- over one batch of synthetic
-signals resident in HBM.  The default workload is BASELINE config 2
-(N=2^20, k=1024, B=1024 signals per GPU sharing one support, complex64).
-Under torchrun each rank owns its own B-signal batch (weak scaling, no
-data-path collective); the timed region is bracketed by a barrier and a
-device synchronise and the max over ranks is reported.
+signals resident in HBM.  The headline workload is BASELINE config 2
+(N=2^20, k=1024, B=1024 signals per GPU sharing one support, complex64); at
+N=1 the same run also measures configs 1, 3, 4, 5 and 5's complex128 pass
+(`per_config`).  --gpus N > 1 without torchrun re-launches this script under
+torch.distributed.run with N ranks (127.0.0.1); each rank owns its own
+batch (weak scaling, no data-path collective; --scaling strong shards the
+config's batch), the timed region is bracketed by a barrier and a device
+synchronise and the max over ranks is reported.
 
 L2: the gather footprint of one batch (~32-40 MiB) fits in the 126 MB L2,
 so the timed steps rotate over R input sets whose combined footprint is
 several times L2 (each set is the same signals at different addresses).
 
---impl reference times the reference algorithm's CPU implementation (the
-numpy port in oracle/, pinned to the reference by golden vectors) on the
-host cores with a process pool, on a bounded sample of the same workload.
+--impl reference times the UNMODIFIED reference package (structfft,
+installed into baseline/_ref by `pip install --target baseline/_ref`) on
+the host cores with a process pool, on a bounded sample of the same
+workload; without that install it falls back to the numpy port in oracle/
+(kind "port", pinned to the reference by golden vectors).
 """
 
 from __future__ import annotations
@@ -131,81 +136,85 @@ def measured_peaks() -> dict:
 
 # ------------------------------------------------------------ b200 arm ---
 
-def run_b200(args) -> None:
-    import torch
-    import torch.distributed as dist
-
-    import paper_2211_15299_b200 as S
+def config_dict(cfg: int, B_total: int, B_rank: int, world: int, scaling: str) -> dict:
+    """The workload of a line; byte-identical in both arms (b200 and reference)."""
     from paper_2211_15299_b200 import workloads as W
+    spec = W.CONFIGS[cfg]
+    k = spec.get("k", 1 << spec["p"])
+    return {"workload": f"config {cfg}: N=2^{spec['M']}, k={k}, "
+                        + (f"B={B_total} total" if scaling == "strong" else f"B={B_rank} per GPU")
+                        + f", {spec['dtype']}, " + ("per-signal supports" if cfg == 4 else "shared support"),
+            "global_batch": B_total, "N": 1 << spec["M"], "k": k, "parallelism": f"batch shard x{world}"}
 
-    world = env_int("WORLD_SIZE", 1)
-    rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
-    ndev = torch.cuda.device_count()
-    torch.cuda.set_device(local % ndev)
-    dev = torch.device("cuda", local % ndev)
-    if world > 1:
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:  # host-side collectives only (CPU tests of the multi-rank path)
-            dist.init_process_group("gloo")
 
-    cfg = args.config
+def measure_config(args, cfg: int, S, W, torch, dev, rank: int, world: int, dist, steps: int, headline: bool):
+    """Device-timed steps of one config on this rank; returns (result dict,
+    state for the e2e / peer legs).  The caller holds the barrier discipline."""
     spec = W.CONFIGS[cfg]
     if args.scaling == "strong":  # fixed total batch, sharded over the ranks
         from paper_2211_15299_b200.dist import shard_range
-        B_total = args.batch or spec["B"]
+        B_total = (args.batch if headline and args.batch else spec["B"])
         b0, b1 = shard_range(B_total, rank, world)
         B = b1 - b0
         if B < 1:
             raise SystemExit(f"strong scaling: {B_total} signals cannot feed {world} ranks")
     else:  # fixed batch per rank
-        B = args.batch or spec["B"]
+        B = args.batch if headline and args.batch else spec["B"]
         b0, B_total = rank * B, B * world
     wl = W.make_workload(cfg, B, b0=b0)
     cdt = torch.complex64 if wl.dtype == "complex64" else torch.complex128
     esz = 8 if cdt == torch.complex64 else 16
     N = wl.N
 
-    # rotation sets so that the timed steps read cold HBM, not L2
+    # byte accounting of one step (SURVEY 8(d)): 32 B sectors and 128 B lines of the gather
     L2 = 126 * 2 ** 20
-    pattern_bytes = None
-    per_sig_sector = []
-    lines = 0
+    per_sig_sector, lines, ub_sum = [], 0, 0
     if wl.support.ndim == 1:
         piv = S.pivots(S.SupportSet(N, wl.support))
         pat = S.pivoted_pattern(piv, wl.M).as_array()
         gb, ub = gather_bytes(pat, esz)
         per_sig_sector = [gb] * B
-        pattern_bytes = (gb, ub)
+        ub_sum = ub * B
         lines = B * line_bytes(pat, esz)
     else:
-        ub_sum = 0
         for b in range(B):
             pat = W.pattern_of(W.config_pivots(cfg, b0 + b), wl.M)
             gb, ub = gather_bytes(pat, esz)
             per_sig_sector.append(gb)
             ub_sum += ub
             lines += line_bytes(pat, esz)
-        pattern_bytes = (None, ub_sum / B)
     footprint = sum(per_sig_sector)
     R = max(2, math.ceil(4 * L2 / max(footprint, 1)))
     R = min(R, args.max_sets)
     sig_bytes = B * N * esz
     free = torch.cuda.mem_get_info(dev)[0]
-    R = max(1, min(R, int((free * 0.85) // sig_bytes)))
+    R = max(1, min(R, int((free * 0.85 - 2 * (1 << 30)) // sig_bytes)))
     sets = [torch.empty((B, N), dtype=cdt, device=dev) for _ in range(R)]
     W.synthesize_into(sets[0], wl.support, wl.coeffs)
-    for s in sets[1:]:
-        s.copy_(sets[0])
-    if wl.support.ndim == 1:
-        J = S.SupportSet(N, wl.support)
-    else:
-        J = torch.from_numpy(wl.support).to(dev)
+    for st_ in sets[1:]:
+        st_.copy_(sets[0])
     out = torch.empty((B, wl.k), dtype=cdt, device=dev)
     status = torch.zeros(wl.support.shape[0] if wl.support.ndim == 2 else 1, dtype=torch.int32, device=dev)
 
-    # kernels one step launches (2 per row chunk for the split transform of large A)
+    # cold call: a fresh SupportSet pays the whole device plan build (pivots,
+    # pattern, tables, twiddles) before its first transform (the reference
+    # rebuilds its plan on every call, hidft.py:154)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if wl.support.ndim == 1:
+        J = S.SupportSet(N, wl.support)
+        if cfg == 3:
+            from paper_2211_15299_b200.hidft import get_plan
+            get_plan(J, S.pivots(J), 0, 0 if cdt == torch.complex64 else 1, dev)
+        else:
+            S.hidft_to_dft_batched(sets[0][:1], J, check=False)
+    else:
+        J = torch.from_numpy(wl.support).to(dev)
+        S.hidft_to_dft_batched(sets[0][:1], J[:1], check=False)
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - t0) * 1e3
+
+    # kernels one step launches (the split transforms launch 2-3 per row chunk)
     launches_per_step = 1
     if wl.support.ndim == 1:
         import ctypes
@@ -234,18 +243,21 @@ def run_b200(args) -> None:
     tol = 1e-5 if esz == 8 else 1e-11
     worst = int(status.max().item())
     if not (err < tol) or worst != 0:
-        raise SystemExit(f"bench parity gate failed: rel L2 {err:.3e} status {worst}")
+        raise SystemExit(f"bench parity gate failed on config {cfg}: rel L2 {err:.3e} status {worst}")
 
-    # CUDA graphs captured from the same step calls, so a timed step is the
-    # step's kernels without host launch gaps (config 1 is launch-bound): one
-    # graph of GS >= --graph-steps consecutive steps (whole cycles over the R
-    # rotation sets; inside it the library's programmatic dependent launch
-    # lets step i+1 gather while step i drains, as it does for back-to-back
-    # eager calls), one graph for each tail length this run needs, and one
-    # graph per single step as a fallback.  --no-graph times the eager calls.
+    # CUDA graphs captured from the same step calls inside a PDL chain scope
+    # (S.stream_chain: consecutive library calls on the capture stream may
+    # overlap through programmatic dependent launch, as back-to-back eager
+    # calls in a scope do): one graph of GS >= --graph-steps consecutive
+    # steps (whole cycles over the R rotation sets), one graph for each tail
+    # length this run needs, and one graph per single step as a fallback.
+    # --no-graph times eager calls (in a scope as well).
+    GS = 0
+
     def run_steps(n, start=0):
-        for i in range(start, start + n):
-            step(i)
+        with S.stream_chain():
+            for i in range(start, start + n):
+                step(i)
     if not args.no_graph:
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
@@ -253,25 +265,18 @@ def run_b200(args) -> None:
             for i in range(R):
                 step(i)
         torch.cuda.current_stream(dev).wait_stream(side)
-        graphs = []
-        for i in range(R):
+
+        def capture(idx):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                step(i)
-            graphs.append(g)
+                with S.stream_chain():
+                    for i in idx:
+                        step(i)
+            return g
+        graphs = [capture([i]) for i in range(R)]
         GS = R * max(1, math.ceil(args.graph_steps / R))  # steps per group graph, whole rotation cycles
-        group = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(group):
-            for i in range(GS):
-                step(i)
-        # the tails this run needs (K, W and the soak's 64 modulo GS) as graphs of their own
-        tails = {}
-        for n in {args.steps % GS, args.warmup % GS, 64 % GS} - {0}:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                for i in range(n):
-                    step(i)
-            tails[n] = g
+        group = capture(range(GS))
+        tails = {n: capture(range(n)) for n in {steps % GS, args.warmup % GS, 64 % GS} - {0}}
         torch.cuda.synchronize()
 
         def run_steps(n, start=0):
@@ -288,11 +293,12 @@ def run_b200(args) -> None:
                     graphs[i % R].replay()
                     i += 1
 
+    local = env_int("LOCAL_RANK", 0)
     vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
     sampler = ClockSampler(vis[local] if local < len(vis) else local)
     sampler.start()
-    # ~1 s soak so that clock samples exist under load, then W warm-up steps
-    t_end = time.time() + args.soak
+    # soak so that clock samples exist under load, then W warm-up steps
+    t_end = time.time() + (args.soak if headline else min(args.soak, 0.5))
     i = 0
     while time.time() < t_end:
         run_steps(64, i)
@@ -306,7 +312,7 @@ def run_b200(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    run_steps(args.steps)
+    run_steps(steps)
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -318,96 +324,170 @@ def run_b200(args) -> None:
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    ms_per_step = ms / args.steps
+    ms_per_step = ms / steps
     coeffs_per_step = B_total * wl.k
     value = coeffs_per_step / (ms_per_step / 1e3)
 
-    # roofline of the step: one kernel (configs 1-4), or the split transform's
-    # front + back pair (config 5), whose bytes are counted once per step
+    # roofline of the step (HBM-bound): G = gather sectors +
+    # coefficient writes + support reads (shared: once; per-signal: B*k int64)
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
-    # gather sectors + coefficient writes + support reads (shared: once; per-signal: B*k int64)
     G = footprint + B * wl.k * esz + wl.support.size * 8
     achieved = G / (ms_per_step / 1e3) / 1e9
     A_sl = 1 << (len(S.pivots(J)) if wl.support.ndim == 1 else int(math.log2(wl.k)))
     flops_step = int(B * 5 * A_sl * max(1, int(math.log2(A_sl))))
+    fp = fma_peaks()
+    fpk = fp["fp32_tflops"] if esz == 8 else fp["fp64_tflops"]
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
             "kernels_per_step": launches_per_step,
-            # secondary: flops 5 A log2 A per signal against the measured
-            # non-tensor FMA peak (tools/fma_peak.cu: 66.4 TF/s fp32, 32.7 TF/s fp64)
             "flops": {"per_step": flops_step, "achieved_tflops": round(flops_step / (ms_per_step / 1e3) / 1e12, 3),
-                      "peak_tflops": 66.4 if esz == 8 else 32.7,
-                      "frac": round(flops_step / (ms_per_step / 1e3) / 1e12 / (66.4 if esz == 8 else 32.7), 4)},
+                      "peak_tflops": fpk, "peak_source": fp["source"],
+                      "frac": round(flops_step / (ms_per_step / 1e3) / 1e12 / fpk, 4)},
             "algorithmic_bytes_per_launch": int(G),
-            "element_bytes_per_launch": int(B * (pattern_bytes[1] if pattern_bytes else 0) + B * wl.k * esz)}
-    # the same kernel against HBM bytes at the measured 128 B access granularity
+            "element_bytes_per_launch": int(ub_sum + B * wl.k * esz),
+            "sector_efficiency": round(ub_sum / max(footprint, 1), 4)}
+    # the same step against HBM bytes at the measured 128 B access granularity
     G_line = lines + B * wl.k * esz + wl.support.size * 8
     roof["at_measured_granularity"] = {
         "bytes_per_launch": int(G_line), "achieved": round(G_line / (ms_per_step / 1e3) / 1e9, 1),
         "frac": round(G_line / (ms_per_step / 1e3) / 1e9 / hbm, 4),
         "note": "every isolated HBM read moves a 128 B line on this B200 (profiles/r01_gather_granularity.md)"}
-    # practical floor: the measured best rate of isolated line reads (3.94e10 lines/s,
-    # tools/gather_probe*.cu, profiles/r01_gather_granularity.md) for this launch's lines
-    n_samples = B * (pattern_bytes[1] / esz if pattern_bytes and pattern_bytes[1] else wl.k)
+    n_samples = ub_sum / esz
     if lines / 128 >= 0.99 * n_samples:  # every sample in its own line (configs 2-4)
         floor_us = (lines / 128) / 3.94e10 * 1e6
         roof["isolated_line_floor"] = {"us_per_launch": round(floor_us, 2),
                                        "frac": round(floor_us / (ms_per_step * 1e3), 4)}
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as fh:
-                tr = json.load(fh).get(f"cfg{cfg}")
-            if tr:
-                roof["traffic"] = tr
-        except (OSError, ValueError):
-            pass
+    tr = profile_traffic(cfg)
+    if tr:
+        roof["traffic"] = tr.get("traffic")
+        roof["traffic_source"] = tr.get("source")
+        if tr.get("sector_efficiency_ncu") is not None:
+            roof["sector_efficiency_ncu"] = tr["sector_efficiency_ncu"]
+    res = {"config": config_dict(cfg, B_total, B, world, args.scaling), "value": value, "ms_per_step": ms_per_step,
+           "steps": steps, "gpu_launches": steps * launches_per_step, "roofline": roof, "clocks": clocks,
+           "plan_ms": round(plan_ms, 3),
+           "parity": {"rel_l2_vs_planted_max": err, "tol": tol, "status_max": worst, "rows": B},
+           "method": {"launch": "eager calls in a stream_chain scope" if args.no_graph else (
+                          f"CUDA graphs of {GS} consecutive step calls (rotating over the input sets), "
+                          "programmatic dependent launch between steps inside S.stream_chain"),
+                      "l2": f"rotating {R} input sets, gather footprint {R * footprint / 2**20:.0f} MiB "
+                            f"vs 126 MB L2"}}
+    state = {"sets": sets, "J": J, "wl": wl, "esz": esz, "B": B, "B_total": B_total, "status": status,
+             "cdt": cdt, "out": out, "coeffs_per_step": coeffs_per_step, "cdev": cdev}
+    return res, state
 
-    # N > 1, untimed: one step with the result rows written straight into
+
+def fma_peaks() -> dict:
+    """Non-tensor FMA peaks: profiles/fma_peak.json (tools/fma_peak.cu on the
+    GPU box, committed) or the round-1 measurement."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fma_peak.json")) as fh:
+            d = json.load(fh)
+        return {"fp32_tflops": float(d["fp32_tflops"]), "fp64_tflops": float(d["fp64_tflops"]),
+                "source": "profiles/fma_peak.json (tools/fma_peak.cu, measured on the B200 box)"}
+    except (OSError, ValueError, KeyError):
+        return {"fp32_tflops": 66.4, "fp64_tflops": 32.7, "source": "round-1 tools/fma_peak.cu measurement"}
+
+
+def profile_traffic(cfg: int) -> dict | None:
+    """ncu-measured DRAM traffic per step and sector efficiency (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            d = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    e = d.get(f"cfg{cfg}")
+    if e is None:
+        return None
+    if not isinstance(e, dict):
+        return {"traffic": e, "source": "profiles/traffic.json (ncu dram__bytes_read+write)"}
+    return {"traffic": e.get("traffic"), "source": e.get("source", "profiles/traffic.json"),
+            "sector_efficiency_ncu": e.get("sector_efficiency_ncu")}
+
+
+def run_b200(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_15299_b200 as S
+    from paper_2211_15299_b200 import workloads as W
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    ndev = torch.cuda.device_count()
+    local_world = env_int("LOCAL_WORLD_SIZE", world)
+    if ndev < 1:
+        raise SystemExit("bench.py: no CUDA device")
+    if args.dist_backend == "nccl" and local_world > ndev:
+        raise SystemExit(f"bench.py: --gpus {world} needs {local_world} devices on this node, found {ndev}")
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # host-side collectives only (CPU tests of the multi-rank path)
+            dist.init_process_group("gloo")
+
+    head, st = measure_config(args, args.config, S, W, torch, dev, rank, world, dist, args.steps, True)
+
+    # N > 1, timed: one step with the result rows written straight into
     # rank 0's device buffer over peer memory (dist.PeerRows, SURVEY 8(e)),
     # checked on rank 0 against the planted spectra of every rank's first and
     # last row; the timed steps above leave the rows sharded
     peer_info = None
-    if world > 1 and cfg != 3 and not args.no_peer_gather:
-        peer_info = run_peer_gather(S, W, torch, dist, sets[0], J, wl, cfg, B, B_total, status, cdt, rank, world)
+    if world > 1 and args.config != 3 and not args.no_peer_gather:
+        peer_info = run_peer_gather(S, W, torch, dist, st["sets"][0], st["J"], st["wl"], args.config, st["B"],
+                                    st["B_total"], st["status"], st["cdt"], rank, world)
 
     # end to end through the public API with host buffers (rank-local)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, S, torch, sets[0], J, wl, esz, dev)
+        e2e = run_e2e(args, S, torch, st["sets"][0], st["J"], st["wl"], st["esz"], dev)
         if world > 1:
-            t = torch.tensor([e2e["seconds_per_step"]], dtype=torch.float64, device=cdev)
+            t = torch.tensor([e2e["seconds_per_step"]], dtype=torch.float64, device=st["cdev"])
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e["value"] = coeffs_per_step / float(t.item())
+            e2e["value"] = st["coeffs_per_step"] / float(t.item())
         del e2e["seconds_per_step"]
+    del st
+    torch.cuda.empty_cache()
+
+    # every other config on the record (N = 1): same discipline, same run
+    per_config = {}
+    if world == 1 and not args.no_per_config:
+        for c in [c for c in (1, 2, 3, 4, 5, 6) if c != args.config]:
+            steps_c = max(20, min(args.steps, args.per_config_steps))
+            try:
+                r, stc = measure_config(args, c, S, W, torch, dev, rank, world, dist, steps_c, False)
+                del stc
+                if not args.no_cpu:
+                    r["reference_single_call"] = reference_single_call(c)
+                per_config[f"cfg{c}"] = r
+            except SystemExit as e:  # a failed parity gate is reported, not hidden
+                per_config[f"cfg{c}"] = {"error": str(e)}
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = run_cpu_reference(cfg, args.cpu_seconds)
+        cpu = run_cpu_reference(args.config, args.cpu_seconds)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "c64 (f32)" if esz == 8 else "c128 (f64)",
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "c64 (f32)" if W.CONFIGS[args.config]["dtype"] == "complex64" else "c128 (f64)",
             "data": "synthetic: seeded supports (reference generators) and complex-Gaussian spectra, "
                     "signals = inverse DFT synthesised on device",
-            "config": {"workload": f"config {cfg}: N=2^{wl.M}, k={wl.k}, "
-                                   + (f"B={B_total} total" if args.scaling == "strong" else f"B={B} per GPU")
-                                   + f", {wl.dtype}, "
-                                   + ("shared support" if wl.support.ndim == 1 else "per-signal supports"),
-                       "global_batch": B_total, "N": N, "k": wl.k, "parallelism": f"batch shard x{world}",
-                       "launch": "eager calls" if args.no_graph else (
-                           f"CUDA graphs of {GS} consecutive step calls (rotating over the input sets), "
-                           "programmatic dependent launch between steps"),
-                       "l2": f"rotating {R} input sets, gather footprint {R * footprint / 2**20:.0f} MiB "
-                             f"vs 126 MB L2"},
-            "gpu_launches": args.steps * launches_per_step,
-            "roofline": roof,
-            "clocks": clocks,
-            "parity": {"rel_l2_vs_planted_max": err, "tol": tol},
+            "config": head["config"],
+            "method": head["method"],
+            "gpu_launches": head["gpu_launches"],
+            "roofline": head["roofline"],
+            "clocks": head["clocks"],
+            "plan_ms": head["plan_ms"],
+            "parity": head["parity"],
         }
         if e2e:
             line["e2e"] = e2e
@@ -415,6 +495,8 @@ def run_b200(args) -> None:
             line["peer_gather"] = peer_info
         if cpu:
             line["cpu_baseline"] = cpu
+        if per_config:
+            line["per_config"] = per_config
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -520,50 +602,126 @@ def run_e2e(args, S, torch, dev_signals, J, wl, esz, dev) -> dict:
 
 # ------------------------------------------------------- CPU reference ---
 
+def _reference_module():
+    """The unmodified reference package from baseline/_ref (pip install
+    --target baseline/_ref /root/reference/pkg), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "structfft")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import structfft  # noqa: F401
+        return structfft
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def _reference_callables(cfg: int):
+    """(kind, prepare(J, M) -> support object, call(f, Jobj)) of the CPU leg:
+    the reference's public path (hidft.py:135-207, sas.py:313-409) when
+    installed, else the oracle port of it."""
+    sf = _reference_module()
+    if sf is not None:
+        def prep(J, M):
+            return sf.SupportSet.make(1 << M, J.tolist())
+        if cfg == 3:
+            def call(f, Js):
+                return sf.sas_transform(f, Js, r=sf.pivots(Js)).coeffs
+        else:
+            def call(f, Js):
+                return sf.hidft_to_dft(sf.hidft(f, Js, sf.pivots(Js)))
+        return "reference", prep, call
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import structfft_oracle as O
+
+    def prep(J, M):
+        return (J, M)
+    if cfg == 3:
+        def call(f, Js):
+            return O.reference_sas_call(f, Js[0], Js[1])
+    else:
+        def call(f, Js):
+            return O.reference_call(f, Js[0], Js[1])
+    return "port", prep, call
+
+
+def _host_signal(cfg: int, b: int):
+    """Signal b of config cfg as a dense host array of the config dtype
+    (harness: the oracle's synthesis, the inverse DFT of the spectrum)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import structfft_oracle as O
+    from paper_2211_15299_b200 import workloads as W
+    spec = W.CONFIGS[cfg]
+    J, M = W.config_support(cfg, b)
+    coef = W.coefficients(cfg, b, J.size)
+    f = O.synthesize(J, coef, M).astype(np.complex64 if spec["dtype"] == "complex64" else np.complex128)
+    return J, M, f, coef
+
+
+def reference_single_call(cfg: int) -> dict:
+    """One core, one signal: the reference call's wall time (after one
+    warm-up call) and, when the reference is installed, the port's time on
+    the same signal (their ratio shows how faithful the port is in cost)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    kind, prep, call = _reference_callables(cfg)
+    J, M, f, coef = _host_signal(cfg, 0)
+    Js = prep(J, M)
+    call(f, Js)
+    t0 = time.perf_counter()
+    got = call(f, Js)
+    dt = time.perf_counter() - t0
+    err = float(np.linalg.norm(np.asarray(got) - coef) / np.linalg.norm(coef))
+    info = {"kind": kind, "ms_per_signal": round(dt * 1e3, 3), "coeffs_per_s_per_core": J.size / dt,
+            "rel_l2_vs_planted": err}
+    if kind == "reference":
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import structfft_oracle as O
+        port = O.reference_sas_call if cfg == 3 else O.reference_call
+        port(f, J, M)
+        t0 = time.perf_counter()
+        port(f, J, M)
+        info["port_ms_per_signal"] = round((time.perf_counter() - t0) * 1e3, 3)
+        info["port_over_reference_time"] = round(info["port_ms_per_signal"] / info["ms_per_signal"], 3)
+    return info
+
+
 def _cpu_worker(cfg, rows, steps, barrier, queue):
     """One host process: synthesise its rows (untimed), then time `steps`
     passes of the reference call over them, each pass starting on a barrier."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import structfft_oracle as O
-    from paper_2211_15299_b200 import workloads as W
-    spec = W.CONFIGS[cfg]
-    dt = np.complex64 if spec["dtype"] == "complex64" else np.complex128
+    kind, prep, call = _reference_callables(cfg)
     sigs = []
     for b in rows:
-        J, M = W.config_support(cfg, b)
-        coef = W.coefficients(cfg, b, J.size)
-        sigs.append((J, M, O.synthesize(J, coef, M).astype(dt)))
-    fn = O.reference_sas_call if cfg == 3 else O.reference_call
-    ncoef = sum(J.size for J, _, _ in sigs)
+        J, M, f, _ = _host_signal(cfg, b)
+        sigs.append((prep(J, M), f, J.size))
+    ncoef = sum(k for _, _, k in sigs)
     for step in range(steps):
         barrier.wait()
         t0 = time.perf_counter()
-        for J, M, f in sigs:
-            fn(f, J, M)
+        for Js, f, _ in sigs:
+            call(f, Js)
         queue.put((step, time.perf_counter() - t0, ncoef))
 
 
 def cpu_reference_steps(cfg: int, steps: int, seconds: float) -> tuple[list, dict]:
-    """The reference algorithm (oracle port, cost-faithful to the reference
-    call) on every host core, one process per core (the reference's own
-    process-pool mechanism, bench.py:261-263).  Each step is a bounded
-    sample: every worker runs its rows once; step value = coefficients /
-    slowest worker's time."""
+    """The reference call on every host core, one process per core (the
+    reference's own process-pool mechanism, bench.py:261-263).  Each step is
+    a bounded sample: every worker runs its rows once; step value =
+    coefficients / slowest worker's time."""
     import multiprocessing as mp
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import structfft_oracle as O
     from paper_2211_15299_b200 import workloads as W
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     P = os.cpu_count() or 1
     spec = W.CONFIGS[cfg]
-    J, M = W.config_support(cfg, 0)
-    esz = 8 if spec["dtype"] == "complex64" else 16
-    f0 = O.synthesize(J, W.coefficients(cfg, 0, J.size), M).astype(
-        np.complex64 if esz == 8 else np.complex128)
-    fn = O.reference_sas_call if cfg == 3 else O.reference_call
-    fn(f0, J, M)
+    kind, prep, call = _reference_callables(cfg)
+    J, M, f0, _ = _host_signal(cfg, 0)
+    esz = f0.itemsize
+    Js = prep(J, M)
+    call(f0, Js)
     t0 = time.perf_counter()
-    fn(f0, J, M)
+    call(f0, Js)
     per_sig = time.perf_counter() - t0
     del f0
     mem_rows = max(1, (1 << 30) // ((1 << M) * esz))          # <= 1 GiB of signals per worker
@@ -597,12 +755,14 @@ def cpu_reference_steps(cfg: int, steps: int, seconds: float) -> tuple[list, dic
                     break
     except OSError:
         pass
-    info = {"unit": UNIT, "cores": P, "kind": "port",
+    what = ("unmodified reference structfft (baseline/_ref)" if kind == "reference"
+            else "oracle port of the reference call (baseline/_ref absent)")
+    info = {"unit": UNIT, "cores": P, "kind": kind,
             "sample": f"{P * per_worker} signals of config {cfg} per step ({per_worker} per worker process, "
-                      f"{P} processes on {model or 'host CPU'}); oracle port of "
+                      f"{P} processes on {model or 'host CPU'}); {what}: "
                       f"{'sas_transform(f, J, r=pivots(J))' if cfg == 3 else 'hidft(f, J, pivots(J)) + hidft_to_dft'}"
-                      f" on dense host arrays, per-call plan and c64->c128 upcast as the reference; "
-                      f"single-call probe {per_sig * 1e3:.2f} ms/signal; total wall {time.perf_counter() - t_wall:.1f} s"}
+                      f" on dense host arrays of the config dtype; single-call probe {per_sig * 1e3:.2f} ms/signal; "
+                      f"total wall {time.perf_counter() - t_wall:.1f} s"}
     return vals, info
 
 
@@ -622,23 +782,40 @@ def run_reference(args) -> None:
     timed = vals[args.warmup:]
     value = statistics.median(timed)
     spec = W.CONFIGS[cfg]
-    k = 4096 if cfg == 3 else (1 << spec["p"])
-    B = spec["B"]
+    k = spec.get("k", 1 << spec["p"])
+    B = args.batch or spec["B"]
+    B_total = B if args.scaling == "strong" else B * world
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": B * k / value * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": B_total * k / value * 1e3,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "c64 input, f64 compute (reference upcasts)" if spec["dtype"] == "complex64" else "c128 (f64)",
             "data": "synthetic, same seeds as the b200 arm",
-            "config": {"workload": f"config {cfg}: N=2^{spec['M']}, k={k}, B={B}", "global_batch": B,
-                       "parallelism": "host process pool"},
+            "config": config_dict(cfg, B_total, B, world, args.scaling),
             "cpu_baseline": {"value": value, **info},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if info["kind"] == "reference":
+        try:
+            line["port_check"] = reference_single_call(cfg)
+        except Exception as e:  # noqa: BLE001
+            line["port_check"] = {"error": repr(e)[:200]}
     print(json.dumps(line), flush=True)
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script with N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None, help="GPUs (ranks); > 1 outside torchrun re-launches under it")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6])
@@ -653,16 +830,25 @@ def main() -> None:
     ap.add_argument("--max-sets", type=int, default=8)
     ap.add_argument("--soak", type=float, default=1.0)
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--per-config-steps", type=int, default=100, help="timed steps of each per_config entry")
+    ap.add_argument("--no-per-config", action="store_true", help="headline config only")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU-baseline budget (b200 arm)")
     ap.add_argument("--ref-seconds", type=float, default=150.0, help="whole --impl reference run budget")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-peer-gather", action="store_true", help="N > 1: skip the untimed peer-memory gather check")
+    ap.add_argument("--no-peer-gather", action="store_true", help="N > 1: skip the peer-memory gather step")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: host-side collectives (multi-rank path test on fewer GPUs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = env_int("WORLD_SIZE", 0)
+    if args.gpus is not None and args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if world == 0 and args.gpus and args.gpus > 1:
+        raise SystemExit(relaunch(args))
+    if world and args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

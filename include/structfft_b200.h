@@ -145,6 +145,18 @@ SFFT_API int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B, i
  * transform for 2^s beyond one CTA). */
 SFFT_API int sfft_launch_count(const sfft_plan* plan, int64_t rows, int64_t* launches);
 
+/* Programmatic dependent launch across calls, opt-in per stream.  With
+ * enable = 1 the caller declares that, until the scope is closed, the
+ * library's calls on `stream` are consecutive and no other kernel on the
+ * stream writes their inputs: each call's first kernel may then start while
+ * the previous call's last kernel drains (its loads run before
+ * griddepcontrol.wait; a call whose inputs overlap an output of the chain
+ * still launches fully ordered).  Default (no scope): every call's first
+ * kernel is fully stream-ordered, so a foreign producer kernel that triggers
+ * its dependents early can never race the library's loads.  The reference
+ * has no counterpart (pure Python, no streams). */
+SFFT_API int sfft_stream_chain(sfft_stream_t stream, int enable);
+
 /* Same transform on samples already gathered in slot order (B rows of A
  * complex, row stride ld >= A): the path for callable / synthesised sources
  * (hidft.py:41-45, where the caller evaluates the signal at the offsets). */

@@ -98,20 +98,27 @@ k_hidft_plan(const PlanArgs args) {
   }
 }
 
-// Consecutive plan-kernel launches on one stream overlap (programmatic
-// dependent launch): each kernel lets its successor launch at once
-// (pdl_release) and waits for its predecessor only before its first store
-// (pdl_wait), so launch N+1 gathers while launch N drains.  Completion stays
-// ordered (every CTA of N waits for N-1 before it can finish), so the
-// launches that may still be running when N+1 gathers are the PDL chain
-// since the last fully ordered launch.  N+1 joins the chain only if its
-// signals do not overlap any output of that chain (pdl_join records them);
-// otherwise, for pre-gathered rows, or when the chain is long, it launches
-// fully stream-ordered and the chain restarts.  A foreign kernel between two
-// launches is fully ordered itself, so the check is conservative.
-// SFFT_PDL=0 disables the overlap.
+// Programmatic dependent launch across calls (opt-in).  A kernel launched
+// with the PDL attribute may start while its predecessor on the stream
+// drains; the library's kernels read only their inputs (signals, supports,
+// plan tables) before griddepcontrol.wait and store only after it.  That is
+// safe when the predecessor is one of the library's own launches whose
+// outputs the new launch does not read, but NOT when the predecessor is a
+// foreign kernel that produced the inputs and triggered its dependents early
+// (CUTLASS-style producers call launch_dependents before their last stores).
+// The library cannot see foreign launches, so overlap across calls happens
+// only inside a chain scope the caller opens on a stream
+// (sfft_stream_chain(stream, 1): "consecutive library calls on this stream;
+// no other kernel on it writes their inputs while the scope is open").  In a
+// scope, launch N+1 joins the chain only if its inputs do not overlap any
+// output of the chain since the last fully ordered launch (checked here),
+// and the first launch after opening the scope is fully ordered.  Outside a
+// scope (the default) the first kernel of every call is fully stream-ordered;
+// kernels inside one call still chain among themselves.  SFFT_PDL=0
+// disables PDL everywhere.
 namespace {
 struct PdlChain {
+  bool scope = false;                                  // sfft_stream_chain(st, 1) in effect
   std::vector<std::pair<uintptr_t, uintptr_t>> outs;  // [lo, hi) written by the chain
 };
 std::mutex g_pdl_mu;
@@ -128,20 +135,36 @@ bool pdl_enabled() {
 bool pdl_join(cudaStream_t st, const ByteRange* in, int nin, const ByteRange* out, int nout, bool eligible) {
   std::lock_guard<std::mutex> lk(g_pdl_mu);
   PdlChain& c = g_pdl[st];
-  bool ok = eligible && pdl_enabled() && c.outs.size() < 16;
+  // outside a scope the chain is always empty: the call's first launch is ordered
+  bool ok = eligible && c.scope && pdl_enabled() && !c.outs.empty() && c.outs.size() < 16;
   for (const auto& o : c.outs)
     for (int i = 0; i < nin && ok; ++i)
       if (in[i].first < o.second && o.first < in[i].second) ok = false;
   if (!ok) c.outs.clear();  // fully ordered: the chain restarts here
-  for (int i = 0; i < nout; ++i) {
-    const ByteRange& o = out[i];
-    if (o.first >= o.second) continue;
-    bool seen = false;
-    for (const auto& x : c.outs) seen |= (x == o);
-    if (!seen) c.outs.push_back(o);
+  if (c.scope) {
+    for (int i = 0; i < nout; ++i) {
+      const ByteRange& o = out[i];
+      if (o.first >= o.second) continue;
+      bool seen = false;
+      for (const auto& x : c.outs) seen |= (x == o);
+      if (!seen) c.outs.push_back(o);
+    }
   }
   return ok;
 }
+
+}  // namespace sfft
+
+// Open (enable = 1) or close (0) a PDL chain scope on a stream (see pdl_join).
+extern "C" int sfft_stream_chain(sfft_stream_t stream, int enable) {
+  std::lock_guard<std::mutex> lk(sfft::g_pdl_mu);
+  sfft::PdlChain& c = sfft::g_pdl[(cudaStream_t)stream];
+  c.scope = enable != 0;
+  c.outs.clear();  // the first launch after opening (or closing) is fully ordered
+  return SFFT_OK;
+}
+
+namespace sfft {
 
 template <typename T, int S>
 static int run_plan_kernel(const PlanArgs& a, cudaStream_t st) {

@@ -616,6 +616,7 @@ extern "C" int sfft_hidft_to_dft_fused_host(const int64_t* J, int64_t k, int M, 
     uint64_t mask = 0;
     for (int64_t e = 1; e < k && ok; ++e) {
       ok = Jr[e] > Jr[e - 1] && Jr[e] < N;
+      if (!ok) break;  // strictly increasing: Jr[e] != Jr[0], so the ctz below is defined
       mask |= 1ull << __builtin_ctzll((unsigned long long)(Jr[e] ^ Jr[0]));
     }
     if (!ok || __builtin_popcountll(mask) != s) {  // the device reports it

@@ -668,6 +668,7 @@ struct StreamScratch {
 };
 static std::mutex g_ss_mu;
 static std::map<int, std::vector<StreamScratch>> g_ss;
+static std::vector<void*> g_ss_retired;  // outgrown buffers, kept until process exit
 
 // *ptr: scratch of at least `bytes` for stream st; *pooled: the caller frees it (cudaFreeAsync)
 static int stream_scratch(int dev, cudaStream_t st, size_t bytes, void** ptr, bool* pooled) {
@@ -680,17 +681,16 @@ static int stream_scratch(int dev, cudaStream_t st, size_t bytes, void** ptr, bo
       if (e.stream != st) continue;
       listed = true;
       if (e.bytes < bytes) {
-        // grow: outside a capture, wait for work in flight on st that may
-        // read the old buffer; a capture (which cannot synchronise) takes
-        // the pool path instead
+        // grow outside a capture (a capture takes the pool path instead)
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         SFFT_CUDA(cudaStreamIsCapturing(st, &cs));
         if (cs != cudaStreamCaptureStatusNone) break;
-        SFFT_CUDA(cudaStreamSynchronize(st));
-        SFFT_CUDA(cudaFree(e.ptr));
-        e.ptr = nullptr;
-        e.bytes = 0;
-        SFFT_CUDA(cudaMalloc(&e.ptr, bytes));
+        // the old buffer is retired, not freed: a CUDA graph captured
+        // earlier on this stream may still reference it
+        void* np = nullptr;
+        SFFT_CUDA(cudaMalloc(&np, bytes));
+        g_ss_retired.push_back(e.ptr);
+        e.ptr = np;
         e.bytes = bytes;
       }
       *ptr = e.ptr;

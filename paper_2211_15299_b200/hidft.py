@@ -366,6 +366,22 @@ def hidft_to_dft(res: HiDftResult, counter=None):
     return out.cpu().numpy() if host else out
 
 
+def _check_out(out, shape, dtype, device, name):
+    """A caller-supplied output buffer must match exactly: the C-ABI writes
+    through its data pointer and row stride only."""
+    torch = _torch()
+    if not torch.is_tensor(out):
+        raise InvalidInputError(f"{name} must be a tensor")
+    if out.dtype != dtype:
+        raise InvalidInputError(f"{name} has dtype {out.dtype}, expected {dtype}")
+    if out.device != device:
+        raise InvalidInputError(f"{name} is on {out.device}, expected {device}")
+    if tuple(out.shape) != tuple(shape):
+        raise InvalidInputError(f"{name} has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if out.stride(-1) != 1 or (len(shape) == 2 and shape[0] > 1 and out.stride(0) < shape[1]):
+        raise InvalidInputError(f"{name} rows must be contiguous and must not overlap")
+
+
 def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
     """Fused hidft(f_b, J_b, pivots(J_b)) + hidft_to_dft for a batch.
 
@@ -414,6 +430,14 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
         nsup, k = B, jt.shape[1]
         Js = None
     code = _DT[sig.dtype]
+    if out is not None:
+        if single and torch.is_tensor(out) and out.dim() == 1:
+            out = out.unsqueeze(0)
+        _check_out(out, (B, k), sig.dtype, run_dev, "out")
+    if status is not None:
+        if not torch.is_tensor(status) or status.dtype != torch.int32 or status.device != run_dev \
+                or status.dim() != 1 or status.numel() < nsup or status.stride(0) != 1:
+            raise InvalidInputError(f"status must be a contiguous int32 tensor of >= {nsup} elements on {run_dev}")
     if out is None and not (host_out and Js is not None):
         out = torch.empty((B, k), dtype=sig.dtype, device=run_dev)
     lib = _lib.load()
@@ -445,3 +469,26 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
             raise ContractViolationError(
                 f"hidft_to_dft requires a homogeneous support (row {int(np.argmax(bad == 3))})")
     return out[0] if single else out
+
+
+class stream_chain:
+    """Context manager: consecutive library calls on `stream` (default: the
+    current stream of the current device) may overlap through programmatic
+    dependent launch (include/structfft_b200.h, sfft_stream_chain).  Inside
+    the scope, no other kernel on that stream may write the inputs of a
+    library call; outside any scope every call starts fully stream-ordered.
+    Used by bench.py around its timed steps and captured graphs."""
+
+    def __init__(self, stream=None):
+        self._stream = stream
+
+    def __enter__(self):
+        torch = _torch()
+        st = self._stream if self._stream is not None else torch.cuda.current_stream()
+        self._ptr = st.cuda_stream if hasattr(st, "cuda_stream") else int(st)
+        _lib.check(_lib.load().sfft_stream_chain(self._ptr, 1))
+        return self
+
+    def __exit__(self, *exc):
+        _lib.load().sfft_stream_chain(self._ptr, 0)
+        return False

@@ -747,13 +747,14 @@ def test_back_to_back_calls_chain(S, torch, M, B):
     bufs = [torch.empty_like(f) for _ in range(3)]
     other = torch.from_numpy((rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(np.complex64)).cuda()
     for _ in range(20):
-        x = f
-        for i in range(3):  # each call reads the previous call's output: fully ordered launches
-            S.hidft_to_dft_batched(x, Js, out=bufs[i])
-            x = bufs[i]
-        # independent calls into one output buffer (PDL chain, write-after-write)
-        S.hidft_to_dft_batched(other, Js, out=bufs[0])
-        S.hidft_to_dft_batched(f, Js, out=bufs[0])
+        with S.stream_chain():  # consecutive library calls may overlap (PDL chain scope)
+            x = f
+            for i in range(3):  # each call reads the previous call's output: fully ordered launches
+                S.hidft_to_dft_batched(x, Js, out=bufs[i])
+                x = bufs[i]
+            # independent calls into one output buffer (PDL chain, write-after-write)
+            S.hidft_to_dft_batched(other, Js, out=bufs[0])
+            S.hidft_to_dft_batched(f, Js, out=bufs[0])
         torch.cuda.synchronize()
         assert torch.equal(bufs[0], ref[1])
         assert torch.equal(bufs[1], ref[2])
@@ -780,12 +781,13 @@ def test_back_to_back_fused_chain(S, torch):
         torch.cuda.synchronize()
     bufs = [torch.empty_like(f) for _ in range(3)]
     for _ in range(20):
-        x = f
-        for i in range(3):
-            S.hidft_to_dft_batched(x, Jt, out=bufs[i], status=st, check=False)
-            x = bufs[i]
-        S.hidft_to_dft_batched(other, Jt, out=bufs[0], status=st, check=False)
-        S.hidft_to_dft_batched(f, Jt, out=bufs[0], status=st, check=False)
+        with S.stream_chain():
+            x = f
+            for i in range(3):
+                S.hidft_to_dft_batched(x, Jt, out=bufs[i], status=st, check=False)
+                x = bufs[i]
+            S.hidft_to_dft_batched(other, Jt, out=bufs[0], status=st, check=False)
+            S.hidft_to_dft_batched(f, Jt, out=bufs[0], status=st, check=False)
         torch.cuda.synchronize()
         for i in range(3):
             assert torch.equal(bufs[i], ref[i + 1])
@@ -807,8 +809,9 @@ for cfg, B in ((2, 64), (4, 48), (5, 3)):
     W.synthesize_into(sig, wl.support, wl.coeffs)
     J = S.SupportSet(wl.N, wl.support) if wl.support.ndim == 1 else torch.from_numpy(wl.support).cuda()
     out = torch.empty((wl.B, wl.k), dtype=torch.complex64, device="cuda")
-    for _ in range(8):  # back-to-back calls into one output buffer
-        S.hidft_to_dft_batched(sig, J, out=out)
+    with S.stream_chain():
+        for _ in range(8):  # back-to-back calls into one output buffer
+            S.hidft_to_dft_batched(sig, J, out=out)
     torch.cuda.synchronize()
     outs.append(out.cpu().numpy())
 np.savez(sys.argv[1], *outs)
@@ -833,3 +836,57 @@ def test_pdl_on_off_bitwise(S, tmp_path):
         res[pdl] = np.load(path)
     for key in res["1"].files:
         assert np.array_equal(res["1"][key], res["0"][key]), key
+
+
+@pytest.mark.parametrize("cfg,B", [(2, 64), (4, 32), (5, 3)])
+def test_foreign_producer_early_trigger(S, torch, cfg, B):
+    """A foreign kernel that produces the signals and lets its dependents
+    launch early (griddepcontrol.launch_dependents at entry, then a spin, then
+    the stores; tests/csrc/early_producer.cu) must never race the library's
+    loads: outside a stream_chain scope every call's first kernel is fully
+    stream-ordered (pdl_join)."""
+    import ctypes
+    import os
+    from paper_2211_15299_b200 import workloads as W
+    lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsfft_test_producer.so"))
+    lib.sfft_test_early_producer.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_void_p]
+    wl = W.make_workload(cfg, B=B)
+    src = torch.empty((wl.B, wl.N), dtype=torch.complex64, device="cuda")
+    W.synthesize_into(src, wl.support, wl.coeffs)
+    J = S.SupportSet(wl.N, wl.support) if wl.support.ndim == 1 else torch.from_numpy(wl.support).cuda()
+    want = S.hidft_to_dft_batched(src, J).clone()
+    dst = torch.empty_like(src)
+    out = torch.empty_like(want)
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(5):
+        dst.zero_()
+        S.hidft_to_dft_batched(src, J, out=out)  # a library launch right before the producer
+        assert lib.sfft_test_early_producer(dst.data_ptr(), src.data_ptr(), dst.numel(), 2_000_000, stream) == 0
+        S.hidft_to_dft_batched(dst, J, out=out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
+
+
+def test_out_buffer_validation(S, torch):
+    """A caller-supplied out / status buffer is checked before any device
+    write (hidft.py passed only data_ptr and stride(0))."""
+    from paper_2211_15299_b200 import workloads as W
+    wl = W.make_workload(2, B=4)
+    sig = torch.empty((wl.B, wl.N), dtype=torch.complex64, device="cuda")
+    W.synthesize_into(sig, wl.support, wl.coeffs)
+    J = S.SupportSet(wl.N, wl.support)
+    bad = [torch.empty((wl.B, wl.k), dtype=torch.complex128, device="cuda"),   # dtype
+           torch.empty((wl.B - 1, wl.k), dtype=torch.complex64, device="cuda"),  # rows
+           torch.empty((wl.B, wl.k), dtype=torch.complex64),                   # device
+           torch.empty((wl.B, 2 * wl.k), dtype=torch.complex64, device="cuda")[:, ::2]]  # inner stride
+    for o in bad:
+        with pytest.raises(S.InvalidInputError):
+            S.hidft_to_dft_batched(sig, J, out=o)
+    Jt = torch.from_numpy(np.stack([wl.support] * wl.B)).cuda()
+    for st in (torch.zeros(wl.B - 1, dtype=torch.int32, device="cuda"), torch.zeros(wl.B, dtype=torch.int64,
+                                                                                     device="cuda")):
+        with pytest.raises(S.InvalidInputError):
+            S.hidft_to_dft_batched(sig, Jt, status=st)
+    ok = torch.empty((wl.B, wl.k), dtype=torch.complex64, device="cuda")
+    assert S.hidft_to_dft_batched(sig, J, out=ok) is not None

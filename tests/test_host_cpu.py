@@ -196,8 +196,44 @@ def test_bench_reference_arm_contract():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    want_kind = "reference" if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "structfft")) else "port"
+    assert line["cpu_baseline"]["kind"] == want_kind and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
     other = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert other.returncode == 0 and other.stdout.strip() == ""
+
+
+def test_bench_gpus_flag_relaunches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks
+    (torch.distributed.run on 127.0.0.1): exactly one JSON line, from rank 0,
+    reporting n_gpus = 2.  Run on the reference arm, which needs no GPU."""
+    import json
+    import subprocess
+    import sys
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--config", "1",
+           "--steps", "1", "--warmup", "3", "--ref-seconds", "5"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "batch shard x2"
+    assert line["config"]["global_batch"] == 2 * 16
+
+
+def test_bench_gpus_mismatch_and_no_device_fail_loudly():
+    """--gpus that disagrees with WORLD_SIZE is refused; the b200 arm without
+    a CUDA device exits non-zero instead of falling back to the CPU."""
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4"], capture_output=True,
+                         text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in (out.stderr + out.stdout)
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "1", "--no-per-config"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode != 0
