@@ -45,10 +45,17 @@ fb = fb.cpu().numpy() if hasattr(fb, "cpu") else np.asarray(fb)
 S.sas_transform(np.stack([fb, fb]), Jb, policy="random_subset", family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
 S.sas_transform(torch.from_numpy(np.stack([fb, fb])).cuda(), Jb, policy="random_subset",
                 family_meta={"base_pivots": (0, 2, 3, 5, 7, 9, 10)})
-# back-to-back calls (programmatic dependent launch chain), 2^14-slot plan kernel (32 slots per thread)
-for _ in range(3):
-    S.hidft_to_dft_batched(f, Js)
-    S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J3))
+# TMA head + final (s = 16 c64 with pivots M-2, M-1: two row chunks via a small scratch budget is
+# not settable here, so three rows), and the three-pass fallback for a shifted call
+J6 = O.gen_homogeneous(sorted(rng.choice(18, size=14, replace=False).tolist()) + [18, 19], 20, 7)
+S.hidft_to_dft_batched(torch.randn(3, 1 << 20, dtype=torch.complex64, device="cuda"), S.SupportSet(1 << 20, J6))
+S.hidft(f2, S.SupportSet(1 << 20, J6), S.pivots(S.SupportSet(1 << 20, J6)), shift=5)
+# back-to-back calls in a PDL chain scope, 2^14-slot plan kernel (32 slots per thread)
+with S.stream_chain():
+    for _ in range(3):
+        S.hidft_to_dft_batched(f, Js)
+        S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J3))
+        S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J6))
 J5 = O.gen_homogeneous(sorted(rng.choice(20, size=14, replace=False).tolist()), 20, 6)
 S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J5))
 S.hidft_to_dft_batched(f2, S.SupportSet(1 << 20, J5))
