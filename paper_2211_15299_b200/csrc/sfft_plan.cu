@@ -13,6 +13,9 @@
 // set bits, prefix-popcount the words, rank = prefix + popc(low bits).
 
 #include <algorithm>
+#include <chrono>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -189,11 +192,59 @@ struct DevBuf {
   }
 };
 
-static int alloc(DevBuf& b, size_t bytes, cudaStream_t st) {
-  b.st = st;
-  SFFT_CUDA(cudaMallocAsync(&b.p, std::max<size_t>(bytes, 16), st));
+// plan-build temporaries come from a library-owned stream-ordered pool that
+// keeps its memory (the default pool returns it at every synchronisation, so
+// each plan build would re-map its bitmaps and tables from the driver)
+static int temp_pool(cudaMemPool_t* pool) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) {
+    *pool = it->second;
+    return SFFT_OK;
+  }
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t p;
+  SFFT_CUDA(cudaMemPoolCreate(&p, &props));
+  uint64_t keep = 256ull << 20;  // keep up to 256 MiB between builds
+  SFFT_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep));
+  pools[dev] = p;
+  *pool = p;
   return SFFT_OK;
 }
+
+static int alloc(DevBuf& b, size_t bytes, cudaStream_t st) {
+  b.st = st;
+  cudaMemPool_t pool;
+  if (int rc = temp_pool(&pool)) return rc;
+  SFFT_CUDA(cudaMallocFromPoolAsync(&b.p, std::max<size_t>(bytes, 16), pool, st));
+  return SFFT_OK;
+}
+
+// SFFT_PLAN_TRACE=1: synchronise and print the wall time of each plan-build phase (stderr)
+struct PlanTrace {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit PlanTrace(cudaStream_t s) : on(getenv("SFFT_PLAN_TRACE") != nullptr), st(s) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[sfft plan] %-28s %8.3f ms (total %8.3f ms)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 
 static int grid_1d(int64_t n, int threads = 256) {
   const int64_t g = (n + threads - 1) / threads;
@@ -240,7 +291,83 @@ static int to_device_J(const int64_t* J, int64_t k, cudaStream_t st, DevBuf& tmp
 }
 
 // pivots(J) on the device; *mask valid after the call (synchronises)
+// O(k) pivots of a homogeneous support (no sort): for homogeneous J every
+// pivot is v2(j - j_0), so P0 = OR_e 1 << ctz(J[e] ^ J[0]); J is homogeneous
+// with pivots P0 iff |J| = 2^|P0|, j -> pext(j, P0) is a bijection onto the
+// 2^|P0| slots, and for every slot x != 0 the elements at x and at x minus
+// its top bit first differ exactly at that bit's pivot (then every pairwise
+// valuation lies in P0).  Same check as the fused per-signal kernel
+// (sfft_fused.cu); a support that fails it takes the general bit-reversed
+// rank below.
+__global__ void k_homog_mask(const int64_t* __restrict__ J, int64_t k, int M, unsigned long long* __restrict__ w) {
+  const int64_t N = 1ll << M;
+  unsigned long long m = 0;
+  int bad = 0;
+  const int64_t j0 = J[0];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = J[e];
+    if (j < 0 || j >= N || (e > 0 && J[e - 1] >= j)) bad = 1;
+    else if (e > 0) m |= 1ull << __ffsll((unsigned long long)(j ^ j0)) - 1;
+  }
+  if (m) atomicOr(&w[0], m);
+  if (bad) atomicOr(&w[1], 1ull);
+}
+__global__ void k_homog_slots(const int64_t* __restrict__ J, int64_t k, const unsigned long long* __restrict__ w,
+                              int32_t* __restrict__ inv, unsigned long long* __restrict__ fail) {
+  const unsigned long long P0 = w[0];
+  if (w[1] || (1ll << __popcll(P0)) != k) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long j = (unsigned long long)J[e];
+    unsigned long long x = 0, m = P0;
+    for (int i = 0; m; ++i, m &= m - 1) x |= ((j >> (__ffsll(m) - 1)) & 1ull) << i;
+    if (atomicCAS(&inv[x], -1, (int32_t)e) != -1) atomicOr(fail, 1ull);  // two elements, one slot
+  }
+}
+__global__ void k_homog_pairs(const int64_t* __restrict__ J, int64_t k, const unsigned long long* __restrict__ w,
+                              const int32_t* __restrict__ inv, unsigned long long* __restrict__ fail) {
+  const unsigned long long P0 = w[0];
+  if (w[1] || (1ll << __popcll(P0)) != k) return;
+  for (int64_t x = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < k; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = 63 - __clzll((unsigned long long)x);
+    unsigned long long m = P0;
+    for (int i = 0; i < t; ++i) m &= m - 1;
+    const int piv = __ffsll(m) - 1;  // pivot of slot bit t
+    const int32_t e1 = inv[x], e2 = inv[x ^ (1ll << t)];
+    if (e1 < 0 || e2 < 0 || __ffsll((unsigned long long)(J[e1] ^ J[e2])) - 1 != piv) atomicOr(fail, 1ull);
+  }
+}
+
 static int analyze_device(const int64_t* dJ, int64_t k, int M, uint64_t* mask_out, cudaStream_t st) {
+  {  // homogeneous fast path
+    DevBuf w, inv;
+    int rc;
+    if ((rc = alloc(w, 32, st))) return rc;
+    SFFT_CUDA(cudaMemsetAsync(w.p, 0, 32, st));
+    unsigned long long* dw = (unsigned long long*)w.p;
+    const bool pow2 = k > 0 && (k & (k - 1)) == 0 && k <= (1ll << 26);
+    if (pow2) {
+      if ((rc = alloc(inv, 4 * k, st))) return rc;
+      SFFT_CUDA(cudaMemsetAsync(inv.p, 0xff, 4 * k, st));
+    }
+    k_homog_mask<<<grid_1d(k), 256, 0, st>>>(dJ, k, M, dw);
+    if (pow2) {
+      k_homog_slots<<<grid_1d(k), 256, 0, st>>>(dJ, k, dw, (int32_t*)inv.p, dw + 2);
+      k_homog_pairs<<<grid_1d(k), 256, 0, st>>>(dJ, k, dw, (const int32_t*)inv.p, dw + 2);
+    }
+    SFFT_CUDA(cudaGetLastError());
+    unsigned long long h[3] = {0, 0, 0};
+    SFFT_CUDA(cudaMemcpyAsync(h, w.p, 24, cudaMemcpyDeviceToHost, st));
+    SFFT_CUDA(cudaStreamSynchronize(st));
+    if (h[1]) return fail(SFFT_ERR_INVALID, "support indices must be strictly increasing and lie in [0, N)");
+    if (pow2 && h[2] == 0 && (1ll << __builtin_popcountll(h[0])) == k) {
+      *mask_out = h[0];
+      return SFFT_OK;
+    }
+    if (k == 1) {
+      *mask_out = 0;
+      return SFFT_OK;
+    }
+  }
   DevBuf keys, sorted, small;
   RankCtx R;
   int rc;
@@ -306,6 +433,29 @@ __global__ void k_fill_level(uint32_t* __restrict__ reps, int kk, int r) {
   }
 }
 
+// levels kk = top .. 0 of k_min_level in one CTA (2^top <= 4096 entries)
+__global__ void __launch_bounds__(1024) k_min_levels_cta(uint32_t* __restrict__ reps, int top) {
+  for (int kk = top; kk >= 0; --kk) {
+    const int n = 1 << kk;
+    for (int x = threadIdx.x; x < n; x += blockDim.x) reps[n - 1 + x] = min(reps[2 * n - 1 + x], reps[3 * n - 1 + x]);
+    __syncthreads();
+  }
+}
+// levels kk = 1 .. top of k_fill_level in one CTA
+__global__ void __launch_bounds__(1024) k_fill_levels_cta(uint32_t* __restrict__ reps, int top,
+                                                          const int32_t* __restrict__ used) {
+  for (int kk = 1; kk <= top; ++kk) {
+    const int n = 1 << kk, r = used[kk - 1];
+    for (int x = threadIdx.x; x < n; x += blockDim.x) {
+      uint32_t* cur = reps + (n - 1);
+      if (cur[x] != 0xffffffffu) continue;
+      const uint32_t shared = reps[n / 2 - 1 + (x & (n / 2 - 1))] & ((1u << r) - 1u);
+      cur[x] = shared + ((uint32_t)((x >> (kk - 1)) & 1) << r);
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void k_plan_twiddles(const uint32_t* __restrict__ reps, const int32_t* __restrict__ used,
                                 int64_t A, Cx<T>* __restrict__ tw) {
@@ -358,6 +508,16 @@ __global__ void k_node_order(const int32_t* __restrict__ slot_res, const uint8_t
     node_slots[rk] = (int32_t)x;
     node_res[rk] = (int32_t)res;
     inv_node[x] = (int32_t)rk;
+  }
+}
+
+__global__ void k_node_identity(const int64_t* __restrict__ J, int64_t k, const int32_t* __restrict__ pats,
+                                int32_t* __restrict__ node_slots, int32_t* __restrict__ node_res,
+                                int32_t* __restrict__ inv_node) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x) {
+    node_slots[e] = pats[e];
+    node_res[e] = (int32_t)J[e];
+    inv_node[pats[e]] = (int32_t)e;
   }
 }
 
@@ -521,17 +681,50 @@ __global__ void k_tri_key(const int32_t* __restrict__ inv, int s, int64_t n_out,
   key[q] = cnt ? sum / cnt : 1e18 + (double)q;
 }
 
-// perm[rank(q)] = q, rank by (key, q): O(nq^2) compares, nq <= 8192
-__global__ void k_tri_rank(const double* __restrict__ key, int64_t nq, int32_t* __restrict__ perm) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= nq) return;
-  const double kq = key[q];
-  int64_t rank = 0;
-  for (int64_t i = 0; i < nq; ++i) {
-    const double ki = __ldg(key + i);
-    rank += (ki < kq) || (ki == kq && i < q);
+// perm[rank(q)] = q, rank by (key, q): one CTA bitonic-sorts the (key, q)
+// pairs in shared memory (nq <= 8192: 96 KB), O(nq log^2 nq) compares
+// instead of the O(nq^2) all-pairs rank.
+__global__ void __launch_bounds__(1024) k_tri_sort(const double* __restrict__ key, int nq,
+                                                   int32_t* __restrict__ perm) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sk = reinterpret_cast<double*>(smem_raw);
+  int32_t* sq = reinterpret_cast<int32_t*>(sk + nq);
+  for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+    sk[i] = key[i];
+    sq[i] = i;
   }
-  perm[rank] = (int32_t)q;
+  __syncthreads();
+  for (int size = 2; size <= nq; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          const double ki = sk[i], kj = sk[j];
+          const int32_t qi = sq[i], qj = sq[j];
+          const bool gt = ki > kj || (ki == kj && qi > qj);
+          if (gt == up) {
+            sk[i] = kj;
+            sk[j] = ki;
+            sq[i] = qj;
+            sq[j] = qi;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < nq; i += blockDim.x) perm[i] = sq[i];
+}
+
+// blocked output map of the final pass (k_fin2): inv[b][pi] = T * nq + pi
+// for every b, pi; flag stays 1 only if all entries comply
+__global__ void k_blocked_check(const int32_t* __restrict__ inv, int64_t A, int64_t nq,
+                                unsigned long long* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = inv[i];
+    if (v < 0 || (v & (nq - 1)) != (i & (nq - 1))) atomicAnd(flag, 0ull);
+  }
 }
 
 // Final-pass tables in pi order: stage s-4+t (t < 4) pairs slot bit s-4+t
@@ -715,11 +908,14 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
   int rc = validate_r(r, n_r, M);  // congruence.py:272-278
   if (rc) return rc;
+  PlanTrace trace(st);
   DevBuf tmpJ;
   const int64_t* dJ = nullptr;
   if ((rc = to_device_J(J, k, st, tmpJ, &dJ))) return rc;
   uint64_t mask = 0;
+  trace.mark("support upload");
   if ((rc = analyze_device(dJ, k, M, &mask, st))) return rc;
+  trace.mark("analyze (pivots)");
   if (n_r > 0) {  // assert_part_homogeneous, congruence.py:259-269
     const int rmax = r[n_r - 1];
     uint64_t rmask = 0;
@@ -777,11 +973,12 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   if ((rc = alloc(dused, 4 * 32, st))) return done(rc);
   if ((rc = alloc(count, 4 * A, st))) return done(rc);
   if ((rc = alloc(reps, 4 * (2 * A - 1), st))) return done(rc);
-  if ((rc = alloc(stats, 16, st))) return done(rc);
+  if ((rc = alloc(stats, 32, st))) return done(rc);
   if (cudaMemcpyAsync(dused.p, p->used, 4 * 32, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemsetAsync(count.p, 0, 4 * A, st) != cudaSuccess ||
       cudaMemsetAsync(reps.p, 0xff, 4 * (2 * A - 1), st) != cudaSuccess ||
       cudaMemsetAsync(stats.p, 0, 16, st) != cudaSuccess ||
+      cudaMemsetAsync((char*)stats.p + 16, 0xff, 16, st) != cudaSuccess ||
       cudaMemsetAsync(p->d_inv_elem, 0xff, 4 * A, st) != cudaSuccess ||
       cudaMemsetAsync(p->d_inv_node, 0xff, 4 * A, st) != cudaSuccess)
     return done(cuda_fail(cudaGetLastError(), "plan init"));
@@ -789,8 +986,12 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   const int32_t* du = (const int32_t*)dused.p;
   k_plan_elements<<<grid_1d(k), 256, 0, st>>>(dJ, k, du, s, p->d_element_slots, (uint32_t*)count.p,
                                               dreps + (A - 1), p->d_inv_elem);
-  for (int kk = s - 1; kk >= 0; --kk) k_min_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk);
-  for (int kk = 1; kk <= s; ++kk) k_fill_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk, p->used[kk - 1]);
+  constexpr int kCtaLevels = 12;  // levels of <= 4096 entries run in one CTA launch
+  for (int kk = s - 1; kk >= kCtaLevels; --kk) k_min_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk);
+  if (s > 0) k_min_levels_cta<<<1, 1024, 0, st>>>(dreps, std::min(s - 1, kCtaLevels - 1));
+  if (s > 0) k_fill_levels_cta<<<1, 1024, 0, st>>>(dreps, std::min(s, kCtaLevels), du);
+  for (int kk = kCtaLevels + 1; kk <= s; ++kk)
+    k_fill_level<<<grid_1d(1ll << kk), 256, 0, st>>>(dreps, kk, p->used[kk - 1]);
   if (A > 1) {
     if (dtype == SFFT_C64)
       k_plan_twiddles<float><<<grid_1d(A), 256, 0, st>>>(dreps, du, A, (Cx<float>*)p->d_twiddles);
@@ -800,7 +1001,12 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   k_plan_slots<<<grid_1d(A), 256, 0, st>>>(dreps + (A - 1), (const uint32_t*)count.p, A, level,
                                            p->d_slot_residues, p->d_slot_real,
                                            (unsigned long long*)stats.p);
-  {
+  if (p->homogeneous && height == 0 && level == M && k == A) {
+    // every slot is real and its residue mod 2^M is its element: ascending
+    // residue is J's own (sorted) order, no rank over 2^M bits needed
+    k_node_identity<<<grid_1d(k), 256, 0, st>>>(dJ, k, p->d_element_slots, p->d_node_slots, p->d_node_residues,
+                                                p->d_inv_node);
+  } else {
     RankCtx R;
     if ((rc = rank_prepare(R, nullptr, nullptr, A, level, st))) return done(rc);
     // residues of real slots are distinct: set their bits, then rank
@@ -812,21 +1018,24 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
                                              (const uint32_t*)R.bsum.p, p->d_node_slots, p->d_node_residues,
                                              p->d_inv_node);
   }
+  trace.mark("slots, twiddles, node order");
   p->split_lc = split_lc(dtype, s);
-  if (p->split_lc) {  // block-major tables of the two-pass transform (sfft_hidft.cu, k_split_*)
-    const int lc = p->split_lc, sl = s - lc;
-    M_(&p->d_tw_blk, csz * ((size_t)1 << lc) * (((size_t)1 << sl) - 1));
-    M_((void**)&p->d_inv_elem_blk, 4 * A);
-    M_((void**)&p->d_inv_node_blk, 4 * A);
-    if (e != cudaSuccess) return done(cuda_fail(e, "split table allocation"));
-    if (dtype == SFFT_C64)
-      k_split_tables<float><<<grid_1d(A), 256, 0, st>>>((const Cx<float>*)p->d_twiddles, p->d_inv_elem, p->d_inv_node,
-                                                        s, lc, (Cx<float>*)p->d_tw_blk, p->d_inv_elem_blk,
-                                                        p->d_inv_node_blk);
-    else
-      k_split_tables<double><<<grid_1d(A), 256, 0, st>>>((const Cx<double>*)p->d_twiddles, p->d_inv_elem,
-                                                         p->d_inv_node, s, lc, (Cx<double>*)p->d_tw_blk,
-                                                         p->d_inv_elem_blk, p->d_inv_node_blk);
+  if (p->split_lc) {
+    if (split_two_pass()) {  // block-major tables of the two-pass transform (k_split_*, SFFT_SPLIT_PASSES=2)
+      const int lc = p->split_lc, sl = s - lc;
+      M_(&p->d_tw_blk, csz * ((size_t)1 << lc) * (((size_t)1 << sl) - 1));
+      M_((void**)&p->d_inv_elem_blk, 4 * A);
+      M_((void**)&p->d_inv_node_blk, 4 * A);
+      if (e != cudaSuccess) return done(cuda_fail(e, "split table allocation"));
+      if (dtype == SFFT_C64)
+        k_split_tables<float><<<grid_1d(A), 256, 0, st>>>((const Cx<float>*)p->d_twiddles, p->d_inv_elem,
+                                                          p->d_inv_node, s, lc, (Cx<float>*)p->d_tw_blk,
+                                                          p->d_inv_elem_blk, p->d_inv_node_blk);
+      else
+        k_split_tables<double><<<grid_1d(A), 256, 0, st>>>((const Cx<double>*)p->d_twiddles, p->d_inv_elem,
+                                                           p->d_inv_node, s, lc, (Cx<double>*)p->d_tw_blk,
+                                                           p->d_inv_elem_blk, p->d_inv_node_blk);
+    }
     // three-pass tables (k_tri_*)
     const int64_t nq = A >> 4;
     M_((void**)&p->d_tri_perm, 4 * nq);
@@ -838,7 +1047,12 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     if ((rc = alloc(key, 8 * nq, st))) return done(rc);
     k_tri_key<<<grid_1d(nq), 256, 0, st>>>(p->homogeneous ? p->d_inv_elem : p->d_inv_node, s,
                                             p->homogeneous ? k : std::min<int64_t>(A, k), (double*)key.p);
-    k_tri_rank<<<grid_1d(nq), 256, 0, st>>>((const double*)key.p, nq, p->d_tri_perm);
+    {
+      const size_t sm = (size_t)nq * (sizeof(double) + sizeof(int32_t));
+      if (cudaFuncSetAttribute(k_tri_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+        return done(cuda_fail(cudaGetLastError(), "plan sort"));
+      k_tri_sort<<<1, 1024, sm, st>>>((const double*)key.p, (int)nq, p->d_tri_perm);
+    }
     if (dtype == SFFT_C64)
       k_tri_tables<float><<<grid_1d(nq), 256, 0, st>>>((const Cx<float>*)p->d_twiddles, p->d_inv_elem,
                                                         p->d_inv_node, p->d_tri_perm, s, (Cx<float>*)p->d_tri_tw,
@@ -849,32 +1063,32 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
                                                          (Cx<double>*)p->d_tri_tw, p->d_tri_inv_elem,
                                                          p->d_tri_inv_node);
   }
-  unsigned long long h[2];
+  trace.mark("split / three-pass tables");
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (p->d_tri_perm) {  // blocked output maps of the final pass (k_fin2)
+    unsigned long long* fl = (unsigned long long*)stats.p + 2;
+    k_blocked_check<<<grid_1d(A), 256, 0, st>>>(p->d_tri_inv_elem, A, A >> 4, fl);
+    k_blocked_check<<<grid_1d(A), 256, 0, st>>>(p->d_tri_inv_node, A, A >> 4, fl + 1);
+  }
   if (p->d_tri_perm && cudaMemcpyAsync(p->tri_front_tw, p->d_twiddles, csz * std::min<int64_t>(15, A - 1),
                                        cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return done(cuda_fail(cudaGetLastError(), "plan build"));
   if (cudaGetLastError() != cudaSuccess ||
-      cudaMemcpyAsync(h, stats.p, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(h, stats.p, 32, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return done(cuda_fail(cudaGetLastError(), "plan build"));
   p->n_nodes = (int64_t)h[0];
   p->mu_star = (int64_t)h[1];
+  p->tri_blocked_elem = p->d_tri_perm && h[2] != 0;
+  p->tri_blocked_node = p->d_tri_perm && h[3] != 0;
+  trace.mark("stats readback");
   static const bool cf = [] {
     const char* e = getenv("SFFT_TRI_CF");
     return !(e && atoi(e) == 0);
   }();
-  if (p->d_tri_perm && dtype == SFFT_C64 && cf && (rc = tri_conflict_free_tables(p, st))) return done(rc);
-  if (p->d_tri_perm) {  // blocked output maps (k_fin2)
-    const int64_t nq = A >> 4;
-    std::vector<int32_t> inv(A);
-    for (int which = 0; which < 2; ++which) {
-      SFFT_CUDA(cudaMemcpy(inv.data(), which ? p->d_tri_inv_node : p->d_tri_inv_elem, 4 * (size_t)A,
-                           cudaMemcpyDeviceToHost));
-      bool ok = true;
-      for (int64_t i = 0; i < A && ok; ++i) ok = inv[i] >= 0 && (inv[i] & (nq - 1)) == (i & (nq - 1));
-      (which ? p->tri_blocked_node : p->tri_blocked_elem) = ok ? 1 : 0;
-    }
-  }
+  if (p->d_tri_perm && dtype == SFFT_C64 && cf && !head_covers(p) && (rc = tri_conflict_free_tables(p, st)))
+    return done(rc);
+  trace.mark("conflict-free tables");
   *out_plan = p;
   return SFFT_OK;
 }

@@ -76,6 +76,10 @@ int max_supported_s(int dtype);
 // its outputs (or restarts the chain when it must launch fully ordered)
 using ByteRange = std::pair<uintptr_t, uintptr_t>;
 bool pdl_join(cudaStream_t st, const ByteRange* in, int nin, const ByteRange* out, int nout, bool eligible);
+// device-resident transforms of this plan take the TMA head path (sfft_split.cu)
+bool head_covers(const sfft_plan* p);
+// SFFT_SPLIT_PASSES=2: the two-pass split (its block-major tables are built only then)
+bool split_two_pass();
 // per-signal plans only serve sfft_hidft(SFFT_OUT_DFT)
 int reject_per_signal(const sfft_plan* p, const char* entry);
 // hidft_to_dft for per-signal supports (sfft_hidft_to_dft_fused's body)

@@ -884,6 +884,15 @@ static int run_tri(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, c
   return SFFT_OK;
 }
 
+// SFFT_SPLIT_PASSES=2 selects the two-pass split (A/B measurements)
+static bool use_tri() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_SPLIT_PASSES");
+    return !(e && atoi(e) == 2);
+  }();
+  return v;
+}
+
 // ------------------------------------------ TMA head + final (two-pass) ---
 //
 // The three-pass split reads whole 128 B lines in its front pass and needs a
@@ -1504,6 +1513,15 @@ static int head_mode() {
   return v;
 }
 
+bool split_two_pass() { return !use_tri(); }
+
+// the plan's device-resident transforms take the head path (plan build skips
+// the three-pass middle pass's conflict-free tables then)
+bool head_covers(const sfft_plan* p) {
+  HeadTma ht;
+  return use_tri() && head_mode() && p->dtype == SFFT_C64 && p->s == 16 && head_plan(p, head_mode(), &ht);
+}
+
 static int try_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st, bool* ran) {
   *ran = false;
   const int P = head_mode();
@@ -1514,14 +1532,6 @@ static int try_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
   }
 }
 
-// SFFT_SPLIT_PASSES=2 selects the two-pass split (A/B measurements)
-static bool use_tri() {
-  static const bool v = [] {
-    const char* e = getenv("SFFT_SPLIT_PASSES");
-    return !(e && atoi(e) == 2);
-  }();
-  return v;
-}
 
 int run_large(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st) {
   if (use_tri()) {
