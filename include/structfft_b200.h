@@ -186,6 +186,17 @@ SFFT_API int sfft_synthesize(const int64_t* J, const void* coeffs, int64_t k, in
 /* select_pivots("auto") profile (sas.py:80-113): for each prefix t = 0..s of the
  * pivot list piv (ascending pivots of J), the largest node weight mu[t] and the
  * sum of squared node weights sumsq[t] at level piv[t-1]+1 (host outputs, s+1 each). */
+/* Congruence tree T^depth(J) levels level_lo..level_hi (congruence.py:134-222,
+ * build_tree 217-222), built on the device.  Level l holds one node per
+ * residue class mod 2^l meeting J, ascending by residue, members ascending.
+ * Outputs per level i = l - level_lo: members[i*k .. i*k+k) (J permuted into
+ * node order), node_off[i*(k+1) ..] (CSR: node n has members
+ * node_off[n] .. node_off[n+1]-1), n_nodes[i].  Residue of node n = first
+ * member mod 2^l.  Outputs may be host (synchronous) or device memory.
+ * M <= 28 (one 2^M-bit rank per level). */
+SFFT_API int sfft_tree_build(const int64_t* J, int64_t k, int M, int level_lo, int level_hi, int64_t* members,
+                             int32_t* node_off, int32_t* n_nodes, sfft_stream_t stream);
+
 SFFT_API int sfft_prefix_weights(const int64_t* J, int64_t k, int M, const int32_t* piv, int s,
                                  uint64_t* mu, uint64_t* sumsq, sfft_stream_t stream);
 

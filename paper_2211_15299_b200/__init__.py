@@ -8,8 +8,9 @@ C-ABI library libsfft_b200.so (include/structfft_b200.h); there is no CPU
 fallback.
 """
 
-from .congruence import (Classification, SupportSet, as_support, assert_part_homogeneous, classify,
-                         height_of, is_part_homogeneous, pivots, v2, validate_pivot_vector)
+from .congruence import (Classification, CongruenceTree, SupportSet, TreeNode, as_support,
+                         assert_part_homogeneous, build_tree, classify, height_of, is_part_homogeneous,
+                         level_weights, pivots, v2, validate_pivot_vector)
 from .counting import OpCounter
 from .errors import (BudgetExceededError, ContractViolationError, DeviceError, InvalidInputError,
                      StructFFTError)

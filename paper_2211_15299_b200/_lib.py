@@ -53,6 +53,7 @@ SIGNATURES = [
     ("sfft_synthesize", _c.c_int, [_P, _P, _I64, _c.c_int, _P, _I64, _P, _P]),
     ("sfft_prefix_weights", _c.c_int, [_P, _I64, _c.c_int, _P, _c.c_int, _P, _P, _P]),
     ("sfft_plan_nodes", _c.c_int, [_P, _P, _P, _P]),
+    ("sfft_tree_build", _c.c_int, [_P, _I64, _c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P]),
     ("sfft_hidft_shifts", _c.c_int, [_P, _P, _I64, _I64, _c.c_int, _I64, _I64, _c.c_int, _P, _I64, _P]),
     ("sfft_sas_decode", _c.c_int, [_P, _P, _I64, _c.c_int, _I64, _I64, _c.c_double, _P, _I64, _c.c_int, _P, _P,
                                    _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),

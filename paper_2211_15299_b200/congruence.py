@@ -213,3 +213,149 @@ def height_of(level: int, r: Sequence[int]) -> int:
     if not r:
         return 0
     return sum(1 for x in r if level <= x <= r[-1])
+
+
+# ------------------------------------------------------ congruence tree ---
+
+@dataclass(frozen=True)
+class TreeNode:
+    """A residue class mod 2^level meeting J (congruence.py:123-131)."""
+    level: int
+    residue: int
+    members: tuple[int, ...]
+
+    @property
+    def weight(self) -> int:
+        return len(self.members)
+
+
+class CongruenceTree:
+    """The mod-2^l refinement tree of J truncated at `depth` levels
+    (congruence.py:134-214), built on the device by sfft_tree_build: per
+    level, J sorted by rotr_M(j, l) is the node order (ascending residue,
+    members ascending) and a node starts where neighbours differ in the low
+    l bits.  The per-level arrays stay in numpy; TreeNode objects (tuples of
+    members, as the reference stores them) are made on access."""
+
+    def __init__(self, J, depth: int):
+        J = as_support(J)
+        if depth < 0 or depth > J.M:
+            raise InvalidInputError(f"depth must be in [0, {J.M}]")
+        self.support = J
+        self.N = J.N
+        self.M = J.M
+        self.depth = int(depth)
+        self._members, self._off, self._n = _tree_levels(J, 0, self.depth)
+        self._levels = None
+
+    # arrays ---------------------------------------------------------------
+    def _residues(self, level: int) -> np.ndarray:
+        n = int(self._n[level])
+        return self._members[level][self._off[level][:n]] & ((1 << level) - 1)
+
+    def node_weights(self, level: int) -> np.ndarray:
+        """Weights of the nodes of `level` in ascending residue order."""
+        self._check_level(level)
+        n = int(self._n[level])
+        return np.diff(self._off[level][:n + 1]).astype(np.int64)
+
+    def _node_at(self, level: int, i: int) -> TreeNode:
+        a, b = int(self._off[level][i]), int(self._off[level][i + 1])
+        mem = self._members[level][a:b]
+        return TreeNode(level, int(mem[0]) & ((1 << level) - 1), tuple(int(x) for x in mem))
+
+    # reference interface --------------------------------------------------
+    @property
+    def levels(self) -> list:
+        """[{residue: TreeNode}] per level, as the reference stores them."""
+        if self._levels is None:
+            self._levels = [{nd.residue: nd for nd in (self._node_at(l, i) for i in range(int(self._n[l])))}
+                            for l in range(self.depth + 1)]
+        return self._levels
+
+    @property
+    def root(self) -> TreeNode:
+        return self._node_at(0, 0)
+
+    def nodes_at_level(self, level: int) -> list:
+        self._check_level(level)
+        return [self._node_at(level, i) for i in range(int(self._n[level]))]
+
+    def node(self, level: int, residue: int):
+        self._check_level(level)
+        res = self._residues(level)
+        i = int(np.searchsorted(res, int(residue)))
+        if i < res.size and int(res[i]) == int(residue):
+            return self._node_at(level, i)
+        return None
+
+    def node_weight(self, level: int, residue: int) -> int:
+        n = self.node(level, residue)
+        return 0 if n is None else n.weight
+
+    def induced_weight(self, level: int, residue: int, w) -> complex:
+        """Sum of w over the node's members; 0 for absent nodes."""
+        n = self.node(level, residue)
+        if n is None:
+            return 0j
+        return complex(sum(w[j] for j in n.members))
+
+    def children(self, node: TreeNode):
+        """(left, right) children; left carries bit `node.level` set."""
+        if node.level >= self.depth:
+            raise InvalidInputError("node has no stored children (below tree depth)")
+        right = self.node(node.level + 1, node.residue)
+        left = self.node(node.level + 1, node.residue + (1 << node.level))
+        return left, right
+
+    def parent(self, node: TreeNode):
+        if node.level == 0:
+            return None
+        return self.node(node.level - 1, node.residue % (1 << (node.level - 1)))
+
+    def max_weight_at_level(self, level: int) -> int:
+        return int(self.node_weights(level).max())
+
+    def split_levels(self) -> tuple[int, ...]:
+        """Levels (below depth) at which some stored node has two children."""
+        return tuple(l for l in range(self.depth) if int(self._n[l + 1]) > int(self._n[l]))
+
+    def _check_level(self, level: int) -> None:
+        if level < 0 or level > self.depth:
+            raise InvalidInputError(f"level {level} outside stored depth {self.depth}")
+
+
+def _tree_levels(J: SupportSet, lo: int, hi: int):
+    """(members (L, k) int64, node_off (L, k+1) int32, n_nodes (L,)) for levels lo..hi."""
+    k = len(J)
+    L = hi - lo + 1
+    if J.M == 0:  # N = 1: the one-element tree
+        return (np.zeros((L, 1), np.int64), np.tile(np.array([0, 1], np.int32), (L, 1)), np.ones(L, np.int32))
+    dev = _lib.require_device()
+    lib = _lib.load()
+    dj = J.device_tensor(dev)
+    members = np.empty((L, k), dtype=np.int64)
+    off = np.empty((L, k + 1), dtype=np.int32)
+    n = np.empty(L, dtype=np.int32)
+    _lib.check(lib.sfft_tree_build(dj.data_ptr(), k, J.M, lo, hi, members.ctypes.data, off.ctypes.data,
+                                   n.ctypes.data, _lib.stream_ptr(dev)))
+    return members, off, n
+
+
+def level_weights(J, level: int) -> np.ndarray:
+    """Node weights of T(J) at one level, ascending residue (device)."""
+    J = as_support(J)
+    if level < 0 or level > J.M:
+        raise InvalidInputError(f"depth must be in [0, {J.M}]")
+    _, off, n = _tree_levels(J, level, level)
+    return np.diff(off[0][:int(n[0]) + 1]).astype(np.int64)
+
+
+def build_tree(J, depth: int, counter=None) -> CongruenceTree:
+    """Construct T^depth(J) (congruence.py:217-222); counts |J| * depth bit
+    operations like the reference."""
+    J = as_support(J)
+    tree = CongruenceTree(J, depth)
+    if counter is not None:
+        counter.count_bit_ops(len(J) * max(depth, 1))
+    return tree

@@ -1093,6 +1093,118 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   return SFFT_OK;
 }
 
+// ------------------------------------------------------ congruence tree ---
+//
+// T^depth(J) (congruence.py:134-222): level l holds one node per residue
+// class mod 2^l that meets J, in ascending residue order, its members in
+// ascending j.  Sorting J by K_l = rotr_M(j, l) = (j mod 2^l) 2^(M-l) +
+// (j >> l) gives exactly that order (the key is a bijection of j, so the
+// bit-map rank sorts it); a node starts where two neighbours differ in the
+// low l bits.  One rank per level, O(k + 2^M / 32) work each.
+__global__ void k_tree_keys(const int64_t* __restrict__ J, int64_t k, int M, int l, uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ bitmap) {
+  const uint32_t lowmask = l >= 32 ? 0xffffffffu : ((1u << l) - 1u);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = (uint32_t)J[e];
+    const uint32_t key = l == 0 ? j : (((j & lowmask) << (M - l)) | (j >> l));
+    keys[e] = key;
+    atomicOr(&bitmap[key >> 5], 1u << (key & 31));
+  }
+}
+__global__ void k_tree_scatter(const int64_t* __restrict__ J, const uint32_t* __restrict__ keys, int64_t k,
+                               const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ wprefix,
+                               const uint32_t* __restrict__ bprefix, int64_t* __restrict__ members) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k; e += (int64_t)gridDim.x * blockDim.x)
+    members[bit_rank(keys[e], bitmap, wprefix, bprefix)] = J[e];
+}
+// node starts: a k-bit bitmap of positions where the residue mod 2^l changes
+__global__ void k_tree_starts(const int64_t* __restrict__ members, int64_t k, int l, uint32_t* __restrict__ sbits) {
+  const int64_t lowmask = (1ll << l) - 1;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < k; p += (int64_t)gridDim.x * blockDim.x)
+    if (p == 0 || ((members[p] ^ members[p - 1]) & lowmask) != 0) atomicOr(&sbits[p >> 5], 1u << (p & 31));
+}
+__global__ void k_tree_offsets(const uint32_t* __restrict__ sbits, int64_t k, const uint32_t* __restrict__ wprefix,
+                               const uint32_t* __restrict__ bprefix, int32_t* __restrict__ node_off,
+                               int32_t* __restrict__ n_nodes) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < k; p += (int64_t)gridDim.x * blockDim.x) {
+    if (!((sbits[p >> 5] >> (p & 31)) & 1u)) continue;
+    const uint32_t r = bit_rank((uint32_t)p, sbits, wprefix, bprefix);
+    node_off[r] = (int32_t)p;
+    if (p == 0) {
+      // total node count = rank of k (one past the last bit), written by thread 0
+      const int64_t last = k - 1;
+      uint32_t cnt = bit_rank((uint32_t)last, sbits, wprefix, bprefix) + ((sbits[last >> 5] >> (last & 31)) & 1u);
+      *n_nodes = (int32_t)cnt;
+    }
+  }
+}
+__global__ void k_tree_close(int32_t* __restrict__ node_off, const int32_t* __restrict__ n_nodes, int64_t k) {
+  node_off[*n_nodes] = (int32_t)k;
+}
+
+extern "C" int sfft_tree_build(const int64_t* J, int64_t k, int M, int level_lo, int level_hi, int64_t* members,
+                               int32_t* node_off, int32_t* n_nodes, sfft_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M < 1 || M > 28) return fail(SFFT_ERR_UNSUPPORTED, "congruence tree on the device needs 1 <= M <= 28");
+  if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
+  if (level_lo < 0 || level_hi < level_lo || level_hi > M)
+    return fail(SFFT_ERR_INVALID, "depth must be in [0, " + std::to_string(M) + "]");
+  if (!members || !node_off || !n_nodes) return fail(SFFT_ERR_INVALID, "null output");
+  DevBuf tmpJ;
+  const int64_t* dJ = nullptr;
+  int rc;
+  if ((rc = to_device_J(J, k, st, tmpJ, &dJ))) return rc;
+  uint64_t mask = 0;
+  if ((rc = analyze_device(dJ, k, M, &mask, st))) return rc;  // validates J (sorted, distinct, in range)
+  const int nl = level_hi - level_lo + 1;
+  DevBuf keys, dm, doff, dn;
+  if ((rc = alloc(keys, 4 * k, st))) return rc;
+  const bool dev_out = is_device_pointer(members) && is_device_pointer(node_off) && is_device_pointer(n_nodes);
+  int64_t* m_out = members;
+  int32_t* o_out = node_off;
+  int32_t* n_out = n_nodes;
+  if (!dev_out) {
+    if ((rc = alloc(dm, 8 * k * (size_t)nl, st))) return rc;
+    if ((rc = alloc(doff, 4 * (k + 1) * (size_t)nl, st))) return rc;
+    if ((rc = alloc(dn, 4 * (size_t)nl, st))) return rc;
+    m_out = (int64_t*)dm.p;
+    o_out = (int32_t*)doff.p;
+    n_out = (int32_t*)dn.p;
+  }
+  for (int l = level_lo; l <= level_hi; ++l) {
+    const int i = l - level_lo;
+    int64_t* mem = m_out + (size_t)i * k;
+    int32_t* off = o_out + (size_t)i * (k + 1);
+    {
+      RankCtx R;
+      if ((rc = rank_prepare(R, nullptr, nullptr, k, M, st))) return rc;
+      k_tree_keys<<<grid_1d(k), 256, 0, st>>>(dJ, k, M, l, (uint32_t*)keys.p, (uint32_t*)R.bitmap.p);
+      if ((rc = rank_scan(R, st))) return rc;
+      k_tree_scatter<<<grid_1d(k), 256, 0, st>>>(dJ, (const uint32_t*)keys.p, k, (const uint32_t*)R.bitmap.p,
+                                                 (const uint32_t*)R.wprefix.p, (const uint32_t*)R.bsum.p, mem);
+    }
+    {
+      RankCtx R;
+      int lg = 0;
+      while ((1ll << lg) < k) ++lg;
+      if ((rc = rank_prepare(R, nullptr, nullptr, k, std::max(lg, 5), st))) return rc;
+      k_tree_starts<<<grid_1d(k), 256, 0, st>>>(mem, k, l, (uint32_t*)R.bitmap.p);
+      if ((rc = rank_scan(R, st))) return rc;
+      k_tree_offsets<<<grid_1d(k), 256, 0, st>>>((const uint32_t*)R.bitmap.p, k, (const uint32_t*)R.wprefix.p,
+                                                 (const uint32_t*)R.bsum.p, off, n_out + i);
+      k_tree_close<<<1, 1, 0, st>>>(off, n_out + i, k);
+    }
+  }
+  SFFT_CUDA(cudaGetLastError());
+  if (!dev_out) {
+    SFFT_CUDA(cudaMemcpyAsync(members, m_out, 8 * k * (size_t)nl, cudaMemcpyDeviceToHost, st));
+    SFFT_CUDA(cudaMemcpyAsync(node_off, o_out, 4 * (k + 1) * (size_t)nl, cudaMemcpyDeviceToHost, st));
+    SFFT_CUDA(cudaMemcpyAsync(n_nodes, n_out, 4 * (size_t)nl, cudaMemcpyDeviceToHost, st));
+    SFFT_CUDA(cudaStreamSynchronize(st));
+  }
+  return SFFT_OK;
+}
+
 extern "C" int sfft_plan_batched(const int64_t* J, int64_t k, int64_t n_supports, int M, int dtype,
                                  sfft_stream_t stream, sfft_plan** out_plan) {
   cudaStream_t st = (cudaStream_t)stream;

@@ -106,6 +106,23 @@ class SasPlan:
     def shifts(self) -> range:
         return range(self.mu_star)
 
+    @classmethod
+    def plan(cls, J, r: Sequence[int], counter=None) -> "SasPlan":
+        """sas.py:69-77: validate r, require r-part-homogeneity, take the node
+        weights of T(J) at the decode level r_max+1 (one level of the device
+        tree, sfft_tree_build; the counter is charged the reference's
+        build_tree cost |J| * level)."""
+        from .congruence import level_weights
+        J = as_support(J)
+        rt = validate_pivot_vector(r, J.M)
+        assert_part_homogeneous(J, rt)
+        level = rt[-1] + 1 if rt else 0
+        if counter is not None:
+            counter.count_bit_ops(len(J) * max(level, 1))
+        weights = tuple(int(w) for w in level_weights(J, level))
+        mu = max(weights)
+        return cls(rt, level, mu, weights, predicted_cost(len(rt), mu, weights))
+
 
 @dataclass
 class CostReport:
