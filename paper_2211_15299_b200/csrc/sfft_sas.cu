@@ -25,7 +25,8 @@
 
 namespace sfft {
 
-constexpr int kMaxMu = 64;  // largest node weight the device decoder handles
+constexpr int kMaxMu = 64;       // node weights decoded one (signal, node) per thread, arrays in registers
+constexpr int kMaxMuBig = 1024;  // heavier nodes: one CTA per (signal, node), arrays in shared memory
 
 // ------------------------------------------------------ double-double ---
 // Same formulas as _ddc.py (no FMA contraction: explicit _rn intrinsics);
@@ -172,10 +173,8 @@ __device__ void bp_core(const C64x* x, const int* perm, C64x* c, int n) {
   }
 }
 
-// sas.py:135-150
-__device__ void leja_order(const C64x* x, int n, int* order) {
-  double prod[kMaxMu];
-  bool chosen[kMaxMu];
+// sas.py:135-150 (scratch: prod, chosen of n entries)
+__device__ void leja_order_s(const C64x* x, int n, int* order, double* prod, bool* chosen) {
   int i0 = 0;
   double best = -1.0;
   for (int i = 0; i < n; ++i) {
@@ -198,13 +197,21 @@ __device__ void leja_order(const C64x* x, int n, int* order) {
     for (int i = 0; i < n; ++i) prod[i] *= cabs2(cs(x[i], x[ib]));
   }
 }
+__device__ void leja_order(const C64x* x, int n, int* order) {
+  double prod[kMaxMu];
+  bool chosen[kMaxMu];
+  leja_order_s(x, n, order, prod, chosen);
+}
 
 // vandermonde_solve (sas.py:166-203): c[perm] = bp_core(x[perm], y)
-__device__ void vandermonde_solve(const C64x* x, const C64x* y, int n, const int* perm, C64x* out) {
-  C64x c[kMaxMu];
+__device__ void vandermonde_solve_s(const C64x* x, const C64x* y, int n, const int* perm, C64x* out, C64x* c) {
   for (int i = 0; i < n; ++i) c[i] = y[i];
   bp_core(x, perm, c, n);
   for (int i = 0; i < n; ++i) out[perm[i]] = c[i];
+}
+__device__ void vandermonde_solve(const C64x* x, const C64x* y, int n, const int* perm, C64x* out) {
+  C64x c[kMaxMu];
+  vandermonde_solve_s(x, y, n, perm, out, c);
 }
 
 // out[j] = sum_m x_m^j c_m, the powers by repeated multiplication and each
@@ -239,7 +246,8 @@ struct SasDecodeArgs {
   const double* node_amp;
   int32_t* esc_list;         // (signal, node) ids to escalate / to refactor densely,
   int32_t* fb_list;          // appended in any order (each node is decoded on its own)
-  unsigned int* counts;      // [2] lengths of esc_list / fb_list
+  int32_t* big_list;         // (signal, node) ids of weight > kMaxMu (k_sas_decode_f64_big)
+  unsigned int* counts;      // [3] lengths of esc_list / fb_list / big_list
 };
 
 __device__ __forceinline__ C64x nodeval(const SasDecodeArgs& a, int64_t row, int64_t node) {
@@ -255,9 +263,8 @@ __device__ __forceinline__ C64x nodeval(const SasDecodeArgs& a, int64_t row, int
 // coefficients of the Lagrange basis L_q(z) = P(z) / ((z - x_q) P'(x_q)),
 // P(z) = prod_i (z - x_i); synthetic division per node (the reference
 // inverts V densely, sas.py:229-233; this is the same norm)
-__device__ double lagrange_inv_norm(const C64x* x, int m) {
+__device__ double lagrange_inv_norm_s(const C64x* x, int m, C64x* P) {  // P: m + 1 entries
   double amp = 0.0;
-  C64x P[kMaxMu + 1];
   P[0] = {1.0, 0.0};
   for (int i = 1; i <= m; ++i) P[i] = {0.0, 0.0};
   for (int i = 0; i < m; ++i)  // multiply by (z - x_i)
@@ -278,6 +285,10 @@ __device__ double lagrange_inv_norm(const C64x* x, int m) {
   }
   return amp;
 }
+__device__ double lagrange_inv_norm(const C64x* x, int m) {
+  C64x P[kMaxMu + 1];
+  return lagrange_inv_norm_s(x, m, P);
+}
 
 // Per-node quantities that do not depend on the signal, computed once per
 // plan: the nodes x_l = e^{-2 pi i l / N} of each member (node-member order),
@@ -289,6 +300,7 @@ __global__ void k_node_prep(const int32_t* __restrict__ node_off, const int32_t*
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_nodes;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int off = node_off[v], m = node_off[v + 1] - off;
+    if (m > kMaxMu) continue;  // k_node_prep_big
     C64x x[kMaxMu];
     int perm[kMaxMu];
     for (int j = 0; j < m; ++j) {
@@ -308,10 +320,108 @@ __global__ void k_node_prep(const int32_t* __restrict__ node_off, const int32_t*
   }
 }
 
+// k_node_prep for nodes heavier than kMaxMu: one CTA per node, its arrays in
+// shared memory, the same sequential operations on thread 0
+__global__ void k_node_prep_big(const int32_t* __restrict__ node_off, const int32_t* __restrict__ node_mem,
+                                const int64_t* __restrict__ J, int64_t n_nodes, int M, C64x* __restrict__ node_x,
+                                int32_t* __restrict__ node_perm, double* __restrict__ node_amp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const double N = ldexp(1.0, M);
+  for (int64_t v = blockIdx.x; v < n_nodes; v += gridDim.x) {
+    const int off = node_off[v], m = node_off[v + 1] - off;
+    if (m <= kMaxMu || threadIdx.x != 0) continue;
+    C64x* x = reinterpret_cast<C64x*>(smem_raw);  // m
+    C64x* P = x + m;                                // m + 1
+    double* prod = reinterpret_cast<double*>(P + m + 1);
+    int* perm = reinterpret_cast<int*>(prod + m);
+    bool* chosen = reinterpret_cast<bool*>(perm + m);
+    for (int j = 0; j < m; ++j) {
+      const double l = (double)J[node_mem[off + j]];
+      double sn, co;
+      sincospi(-2.0 * l / N, &sn, &co);
+      x[j] = {co, sn};
+      node_x[off + j] = x[j];
+    }
+    leja_order_s(x, m, perm, prod, chosen);
+    for (int j = 0; j < m; ++j) node_perm[off + j] = perm[j];
+    node_amp[v] = lagrange_inv_norm_s(x, m, P);
+  }
+}
+
+// decode one (signal b, node v) of weight m (sas.py:343-399, float64 part):
+// BP solve, forward-error estimate, residual; arrays are caller scratch
+// (registers for m <= kMaxMu, shared memory above)
+__device__ void decode_node(const SasDecodeArgs& a, int64_t b, int64_t v, int off, int m, C64x* x, C64x* y, C64x* c,
+                            C64x* r, C64x* d, C64x* cs_scratch, int* perm) {
+  const double noise_eps = 100.0 * 2.220446049250313e-16;
+  const int64_t fid = b * a.n_nodes + v;  // flags / resid stay (signal, node) row-major
+  C64x* out = reinterpret_cast<C64x*>(a.out) + b * a.ld_out;
+  for (int j = 0; j < m; ++j) {
+    const C64x raw = nodeval(a, b * a.mu + j, v);
+    y[j] = {raw.x * a.scale, raw.y * a.scale};
+    x[j] = a.node_x[off + j];  // per-plan tables (k_node_prep)
+    perm[j] = a.node_perm[off + j];
+  }
+  vandermonde_solve_s(x, y, m, perm, c, cs_scratch);
+  // forward-error estimate (sas.py:214-235)
+  double cmax = 0.0, ymax = 0.0;
+  for (int i = 0; i < m; ++i) {
+    cmax = fmax(cmax, cabs2(c[i]));
+    ymax = fmax(ymax, cabs2(y[i]));
+  }
+  const double denom = fmax(cmax, 1e-300);
+  forward_apply(x, c, m, r);
+  for (int j = 0; j < m; ++j) r[j] = cs(r[j], y[j]);
+  vandermonde_solve_s(x, r, m, perm, d, cs_scratch);
+  double dmax = 0.0;
+  for (int i = 0; i < m; ++i) dmax = fmax(dmax, cabs2(d[i]));
+  double est = dmax / denom;
+  const double amp = a.node_amp[v];
+  est = fmax(est, amp * noise_eps * ymax / denom);
+  int flag = 0;
+  double res = 0.0;
+  if (!(est <= a.tol / 20.0)) {
+    flag = 1;  // escalate to double-double
+  } else {
+    forward_apply(x, c, m, r);
+    double num = 0.0, den = 0.0;
+    for (int j = 0; j < m; ++j) {
+      const C64x e = cs(r[j], y[j]);
+      num += e.x * e.x + e.y * e.y;
+      den += y[j].x * y[j].x + y[j].y * y[j].y;
+    }
+    res = sqrt(num) / fmax(sqrt(den), 1e-300);
+    if (res > fmax(a.tol, 1e-9)) flag = 2;
+  }
+  for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = c[i];
+  a.flags[fid] = flag;
+  a.resid[fid] = res;
+  if (flag == 1) a.esc_list[atomicAdd(&a.counts[0], 1u)] = (int32_t)fid;
+  else if (flag == 2) a.fb_list[atomicAdd(&a.counts[1], 1u)] = (int32_t)fid;
+}
+
+// nodes heavier than kMaxMu (listed by k_sas_decode_f64): one CTA per item
+__global__ void k_sas_decode_f64_big(const SasDecodeArgs a, const int32_t* __restrict__ work, int64_t n_work) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    if (threadIdx.x != 0) continue;
+    const int64_t id = work[w];
+    const int64_t b = id / a.n_nodes, v = id % a.n_nodes;
+    const int off = a.node_off[v], m = a.node_off[v + 1] - off;
+    C64x* x = reinterpret_cast<C64x*>(smem_raw);
+    C64x* y = x + m;
+    C64x* c = y + m;
+    C64x* r = c + m;
+    C64x* d = r + m;
+    C64x* t = d + m;
+    int* perm = reinterpret_cast<int*>(t + m);
+    decode_node(a, b, v, off, m, x, y, c, r, d, t, perm);
+  }
+}
+
 // one thread per (signal, node)
 __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
   const int64_t total = a.B * a.n_nodes;
-  const double noise_eps = 100.0 * 2.220446049250313e-16;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
     // node-major: a warp decodes one node for 32 signals, so every lane runs
@@ -327,50 +437,13 @@ __global__ void k_sas_decode_f64(const SasDecodeArgs a) {
       a.resid[fid] = 0.0;
       continue;
     }
-    C64x x[kMaxMu], y[kMaxMu], c[kMaxMu], r[kMaxMu], d[kMaxMu];
+    if (m > kMaxMu) {  // k_sas_decode_f64_big
+      a.big_list[atomicAdd(&a.counts[2], 1u)] = (int32_t)fid;
+      continue;
+    }
+    C64x x[kMaxMu], y[kMaxMu], c[kMaxMu], r[kMaxMu], d[kMaxMu], t[kMaxMu];
     int perm[kMaxMu];
-    for (int j = 0; j < m; ++j) {
-      const C64x raw = nodeval(a, b * a.mu + j, v);
-      y[j] = {raw.x * a.scale, raw.y * a.scale};
-      x[j] = a.node_x[off + j];  // per-plan tables (k_node_prep)
-      perm[j] = a.node_perm[off + j];
-    }
-    vandermonde_solve(x, y, m, perm, c);
-    // forward-error estimate (sas.py:214-235)
-    double cmax = 0.0, ymax = 0.0;
-    for (int i = 0; i < m; ++i) {
-      cmax = fmax(cmax, cabs2(c[i]));
-      ymax = fmax(ymax, cabs2(y[i]));
-    }
-    const double denom = fmax(cmax, 1e-300);
-    forward_apply(x, c, m, r);
-    for (int j = 0; j < m; ++j) r[j] = cs(r[j], y[j]);
-    vandermonde_solve(x, r, m, perm, d);
-    double dmax = 0.0;
-    for (int i = 0; i < m; ++i) dmax = fmax(dmax, cabs2(d[i]));
-    double est = dmax / denom;
-    const double amp = a.node_amp[v];
-    est = fmax(est, amp * noise_eps * ymax / denom);
-    int flag = 0;
-    double res = 0.0;
-    if (!(est <= a.tol / 20.0)) {
-      flag = 1;  // escalate to double-double
-    } else {
-      forward_apply(x, c, m, r);
-      double num = 0.0, den = 0.0;
-      for (int j = 0; j < m; ++j) {
-        const C64x e = cs(r[j], y[j]);
-        num += e.x * e.x + e.y * e.y;
-        den += y[j].x * y[j].x + y[j].y * y[j].y;
-      }
-      res = sqrt(num) / fmax(sqrt(den), 1e-300);
-      if (res > fmax(a.tol, 1e-9)) flag = 2;
-    }
-    for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = c[i];
-    a.flags[fid] = flag;
-    a.resid[fid] = res;
-    if (flag == 1) a.esc_list[atomicAdd(&a.counts[0], 1u)] = (int32_t)fid;
-    else if (flag == 2) a.fb_list[atomicAdd(&a.counts[1], 1u)] = (int32_t)fid;
+    decode_node(a, b, v, off, m, x, y, c, r, d, t, perm);
   }
 }
 
@@ -421,6 +494,7 @@ __global__ void k_sas_decode_dd(const SasDDArgs a) {
     const SasDecodeArgs& s = a.base;
     const int64_t b = id / s.n_nodes, v = id % s.n_nodes;
     const int off = s.node_off[v], m = s.node_off[v + 1] - off;
+    if (m > kMaxMu) continue;  // k_sas_decode_dd_big
     const uint64_t resid = (uint64_t)(int64_t)a.node_res[v];
     cdd y[kMaxMu];
     // shifts in groups of JG: each root kernel value serves JG shifts (per
@@ -529,6 +603,51 @@ __global__ void k_sas_decode_dd(const SasDDArgs a) {
   }
 }
 
+// escalation of nodes heavier than kMaxMu: one warp per node re-measures
+// (the same lane-split dd dot products as k_sas_decode_dd), lane 0 solves in
+// dd sequentially on shared memory -- the same operations per entry, in the
+// same order, as the lane-parallel sweeps (_ddc.py:235-254)
+__global__ void k_sas_decode_dd_big(const SasDDArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = blockIdx.x; w < a.n_work; w += gridDim.x) {
+    const int64_t id = a.work[w];
+    const SasDecodeArgs& s = a.base;
+    const int64_t b = id / s.n_nodes, v = id % s.n_nodes;
+    const int off = s.node_off[v], m = s.node_off[v + 1] - off;
+    if (m <= kMaxMu) continue;
+    cdd* y = reinterpret_cast<cdd*>(smem_raw);  // m
+    cdd* xl = y + m;                              // m
+    const uint64_t resid = (uint64_t)(int64_t)a.node_res[v];
+    for (int j = 0; j < m; ++j) {
+      cdd acc = {{0.0, 0.0}, {0.0, 0.0}};
+      for (int64_t i = lane; i < a.A; i += 32) {
+        const cdd kern = a.tab.get((uint64_t)(-(int64_t)(resid * (uint64_t)a.pattern[i])));
+        acc = cdd_add(acc, cdd_mul(dd_sample(a, b, j, i), kern));
+      }
+      for (int d = 16; d > 0; d >>= 1) {
+        const cdd o = {shfl_dd(acc.re, d), shfl_dd(acc.im, d)};
+        acc = cdd_add(acc, o);
+      }
+      if (lane == 0) y[j] = cdd_mul_complex(acc, s.scale, 0.0);
+    }
+    for (int j = lane; j < m; j += 32) xl[j] = a.tab.get((uint64_t)(-(int64_t)s.J[s.node_mem[off + j]]));
+    __syncwarp();
+    if (lane == 0) {
+      for (int k = 0; k < m - 1; ++k)
+        for (int j = m - 1; j > k; --j) y[j] = cdd_sub(y[j], cdd_mul(xl[k], y[j - 1]));
+      for (int k = m - 2; k >= 0; --k) {
+        for (int j = k + 1; j < m; ++j) y[j] = cdd_div(y[j], cdd_sub(xl[j], xl[j - k - 1]));
+        for (int j = k; j < m - 1; ++j) y[j] = cdd_sub(y[j], y[j + 1]);
+      }
+      C64x* out = reinterpret_cast<C64x*>(s.out) + b * s.ld_out;
+      for (int j = 0; j < m; ++j)
+        out[s.node_mem[off + j]] = {__dadd_rn(y[j].re.hi, y[j].re.lo), __dadd_rn(y[j].im.hi, y[j].im.lo)};
+    }
+    __syncwarp();
+  }
+}
+
 // band-limited source: dd samples at (pattern_i - j) mod N for j < mu (synthesize_dd, _ddc.py:212-224)
 __global__ void k_dd_samples(RootTab tab, const int64_t* __restrict__ pattern, int64_t A, int64_t mu,
                              const int64_t* __restrict__ Jsrc, const double2* __restrict__ csrc, int64_t ksrc,
@@ -549,58 +668,78 @@ __global__ void k_dd_samples(RootTab tab, const int64_t* __restrict__ pattern, i
 }
 
 // dense fallback (sas.py:389-395): LU with partial pivoting of V (V[j][m] = x_m^j)
+__device__ void dense_node(const SasDecodeArgs& a, int64_t b, int64_t v, int off, int m, C64x* V, C64x* rhs, C64x* x,
+                           C64x* sol) {
+  const double N = ldexp(1.0, a.M);
+  for (int i = 0; i < m; ++i) {
+    double sn, co;
+    sincospi(-2.0 * (double)a.J[a.node_mem[off + i]] / N, &sn, &co);
+    x[i] = {co, sn};
+  }
+  for (int j = 0; j < m; ++j) {
+    const C64x raw = nodeval(a, b * a.mu + j, v);
+    rhs[j] = {raw.x * a.scale, raw.y * a.scale};
+    for (int i = 0; i < m; ++i) {
+      C64x p = {1.0, 0.0};
+      for (int e = 0; e < j; ++e) p = cm(p, x[i]);
+      V[j * m + i] = p;
+    }
+  }
+  for (int col = 0; col < m; ++col) {
+    int piv = col;
+    double best = cabs2(V[col * m + col]);
+    for (int r = col + 1; r < m; ++r)
+      if (cabs2(V[r * m + col]) > best) { best = cabs2(V[r * m + col]); piv = r; }
+    if (piv != col) {
+      for (int c2 = 0; c2 < m; ++c2) {
+        const C64x t = V[col * m + c2];
+        V[col * m + c2] = V[piv * m + c2];
+        V[piv * m + c2] = t;
+      }
+      const C64x t = rhs[col];
+      rhs[col] = rhs[piv];
+      rhs[piv] = t;
+    }
+    for (int r = col + 1; r < m; ++r) {
+      const C64x f = cdv(V[r * m + col], V[col * m + col]);
+      for (int c2 = col; c2 < m; ++c2) V[r * m + c2] = cs(V[r * m + c2], cm(f, V[col * m + c2]));
+      rhs[r] = cs(rhs[r], cm(f, rhs[col]));
+    }
+  }
+  C64x* out = reinterpret_cast<C64x*>(a.out) + b * a.ld_out;
+  for (int r = m - 1; r >= 0; --r) {
+    C64x acc = rhs[r];
+    for (int c2 = r + 1; c2 < m; ++c2) acc = cs(acc, cm(V[r * m + c2], sol[c2]));
+    sol[r] = cdv(acc, V[r * m + r]);
+  }
+  for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = sol[i];
+}
+
 __global__ void k_sas_dense(const SasDecodeArgs a, const int32_t* __restrict__ work, int64_t n_work,
                             C64x* __restrict__ scratch) {
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_work; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t id = work[w];
     const int64_t b = id / a.n_nodes, v = id % a.n_nodes;
     const int off = a.node_off[v], m = a.node_off[v + 1] - off;
-    const double N = ldexp(1.0, a.M);
-    C64x* V = scratch + w * kMaxMu * kMaxMu;
-    C64x rhs[kMaxMu], x[kMaxMu];
-    for (int i = 0; i < m; ++i) {
-      double sn, co;
-      sincospi(-2.0 * (double)a.J[a.node_mem[off + i]] / N, &sn, &co);
-      x[i] = {co, sn};
-    }
-    for (int j = 0; j < m; ++j) {
-      const C64x raw = nodeval(a, b * a.mu + j, v);
-      rhs[j] = {raw.x * a.scale, raw.y * a.scale};
-      for (int i = 0; i < m; ++i) {
-        C64x p = {1.0, 0.0};
-        for (int e = 0; e < j; ++e) p = cm(p, x[i]);
-        V[j * m + i] = p;
-      }
-    }
-    for (int col = 0; col < m; ++col) {
-      int piv = col;
-      double best = cabs2(V[col * m + col]);
-      for (int r = col + 1; r < m; ++r)
-        if (cabs2(V[r * m + col]) > best) { best = cabs2(V[r * m + col]); piv = r; }
-      if (piv != col) {
-        for (int c2 = 0; c2 < m; ++c2) {
-          const C64x t = V[col * m + c2];
-          V[col * m + c2] = V[piv * m + c2];
-          V[piv * m + c2] = t;
-        }
-        const C64x t = rhs[col];
-        rhs[col] = rhs[piv];
-        rhs[piv] = t;
-      }
-      for (int r = col + 1; r < m; ++r) {
-        const C64x f = cdv(V[r * m + col], V[col * m + col]);
-        for (int c2 = col; c2 < m; ++c2) V[r * m + c2] = cs(V[r * m + c2], cm(f, V[col * m + c2]));
-        rhs[r] = cs(rhs[r], cm(f, rhs[col]));
-      }
-    }
-    C64x* out = reinterpret_cast<C64x*>(a.out) + b * a.ld_out;
-    C64x sol[kMaxMu];
-    for (int r = m - 1; r >= 0; --r) {
-      C64x acc = rhs[r];
-      for (int c2 = r + 1; c2 < m; ++c2) acc = cs(acc, cm(V[r * m + c2], sol[c2]));
-      sol[r] = cdv(acc, V[r * m + r]);
-    }
-    for (int i = 0; i < m; ++i) out[a.node_mem[off + i]] = sol[i];
+    if (m > kMaxMu) continue;  // k_sas_dense_big
+    C64x rhs[kMaxMu], x[kMaxMu], sol[kMaxMu];
+    dense_node(a, b, v, off, m, scratch + w * kMaxMu * kMaxMu, rhs, x, sol);
+  }
+}
+
+// dense fallback for nodes heavier than kMaxMu: one CTA per item, thread 0,
+// vectors in shared memory, V (mu x mu) in global scratch
+__global__ void k_sas_dense_big(const SasDecodeArgs a, const int32_t* __restrict__ work, int64_t n_work,
+                                C64x* __restrict__ scratch, int64_t mu) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    if (threadIdx.x != 0) continue;
+    const int64_t id = work[w];
+    const int64_t b = id / a.n_nodes, v = id % a.n_nodes;
+    const int off = a.node_off[v], m = a.node_off[v + 1] - off;
+    if (m <= kMaxMu) continue;
+    C64x* rhs = reinterpret_cast<C64x*>(smem_raw);
+    dense_node(a, b, v, off, m, scratch + blockIdx.x * mu * mu, rhs, rhs + m, rhs + 2 * m);
   }
 }
 
@@ -767,7 +906,7 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
   if (int rj = reject_per_signal(p, "sfft_sas_decode")) return rj;
   if (p->height != 0) return fail(SFFT_ERR_CONTRACT, "sas decode needs height 0");
   if (mu != p->mu_star) return fail(SFFT_ERR_INVALID, "mu must equal the plan's mu*");
-  if (mu > kMaxMu) return fail(SFFT_ERR_UNSUPPORTED, "node weight above " + std::to_string(kMaxMu));
+  if (mu > kMaxMuBig) return fail(SFFT_ERR_UNSUPPORTED, "node weight above " + std::to_string(kMaxMuBig));
   int rc = sfft_plan_nodes(p, nullptr, nullptr, stream);
   if (rc) return rc;
   if (!J_dev) return fail(SFFT_ERR_INVALID, "null support pointer");
@@ -779,6 +918,13 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
       SFFT_CUDA(cudaMalloc((void**)&p->d_node_amp, sizeof(double) * std::max<int64_t>(p->n_nodes, 1)));
       k_node_prep<<<grid_for(p->n_nodes, 128), 128, 0, st>>>(p->d_node_off, p->d_node_mem, J_dev, p->n_nodes, p->M,
                                                              (C64x*)p->d_node_x, p->d_node_perm, p->d_node_amp);
+      if (mu > kMaxMu) {
+        const size_t sm = (2 * mu + 1) * sizeof(C64x) + mu * (sizeof(double) + sizeof(int) + 1);
+        SFFT_CUDA(cudaFuncSetAttribute(k_node_prep_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_node_prep_big<<<(unsigned)std::min<int64_t>(p->n_nodes, (int64_t)num_sms() * 8), 32, sm, st>>>(
+            p->d_node_off, p->d_node_mem, J_dev, p->n_nodes, p->M, (C64x*)p->d_node_x, p->d_node_perm,
+            p->d_node_amp);
+      }
       SFFT_CUDA(cudaGetLastError());
     }
   }
@@ -807,16 +953,26 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
   // lengths come back to the host
   const int64_t total = B * p->n_nodes;
   int32_t* lists = nullptr;
-  SFFT_CUDA(cudaMallocAsync((void**)&lists, sizeof(int32_t) * (2 * total + 2), st));
+  SFFT_CUDA(cudaMallocAsync((void**)&lists, sizeof(int32_t) * (3 * total + 3), st));
   a.esc_list = lists;
   a.fb_list = lists + total;
-  a.counts = reinterpret_cast<unsigned int*>(lists + 2 * total);
-  SFFT_CUDA(cudaMemsetAsync(a.counts, 0, 2 * sizeof(unsigned int), st));
+  a.big_list = lists + 2 * total;
+  a.counts = reinterpret_cast<unsigned int*>(lists + 3 * total);
+  SFFT_CUDA(cudaMemsetAsync(a.counts, 0, 3 * sizeof(unsigned int), st));
   k_sas_decode_f64<<<grid_for(total), 128, 0, st>>>(a);
   SFFT_CUDA(cudaGetLastError());
-  unsigned int hc[2] = {0, 0};
+  unsigned int hc[3] = {0, 0, 0};
   SFFT_CUDA(cudaMemcpyAsync(hc, a.counts, sizeof(hc), cudaMemcpyDeviceToHost, st));
   SFFT_CUDA(cudaStreamSynchronize(st));
+  if (hc[2] > 0) {  // nodes heavier than kMaxMu: one CTA each
+    const size_t sm = 6 * mu * sizeof(C64x) + mu * sizeof(int);
+    SFFT_CUDA(cudaFuncSetAttribute(k_sas_decode_f64_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_sas_decode_f64_big<<<(unsigned)std::min<int64_t>(hc[2], (int64_t)num_sms() * 8), 32, sm, st>>>(
+        a, a.big_list, (int64_t)hc[2]);
+    SFFT_CUDA(cudaGetLastError());
+    SFFT_CUDA(cudaMemcpyAsync(hc, a.counts, 2 * sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    SFFT_CUDA(cudaStreamSynchronize(st));
+  }
   const int64_t n_esc = hc[0], n_fb = hc[1];
   *n_escalated = n_esc;
   *n_fallback = n_fb;
@@ -857,6 +1013,11 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
       d.samples_dd = samples;
     }
     k_sas_decode_dd<<<grid_for(d.n_work * 32, 128), 128, 0, st>>>(d);
+    if (mu > kMaxMu) {
+      const size_t sm = 2 * mu * sizeof(cdd);
+      SFFT_CUDA(cudaFuncSetAttribute(k_sas_decode_dd_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_sas_decode_dd_big<<<(unsigned)std::min<int64_t>(d.n_work, (int64_t)num_sms() * 8), 32, sm, st>>>(d);
+    }
     SFFT_CUDA(cudaGetLastError());
     cudaFreeAsync(pattern, st);
     if (sigs) cudaFreeAsync(sigs, st);
@@ -868,6 +1029,16 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
     k_sas_dense<<<grid_for(n_fb, 32), 32, 0, st>>>(a, a.fb_list, n_fb, scratch);
     SFFT_CUDA(cudaGetLastError());
     cudaFreeAsync(scratch, st);
+    if (mu > kMaxMu) {
+      const int64_t g = std::min<int64_t>(n_fb, (int64_t)num_sms() * 2);
+      C64x* big = nullptr;
+      SFFT_CUDA(cudaMallocAsync(&big, sizeof(C64x) * mu * mu * g, st));
+      const size_t sm = 3 * mu * sizeof(C64x);
+      SFFT_CUDA(cudaFuncSetAttribute(k_sas_dense_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_sas_dense_big<<<(unsigned)g, 32, sm, st>>>(a, a.fb_list, n_fb, big, mu);
+      SFFT_CUDA(cudaGetLastError());
+      cudaFreeAsync(big, st);
+    }
   }
   cudaFreeAsync(lists, st);
   return SFFT_OK;

@@ -9,7 +9,8 @@ Bjorck-Pereyra with Leja order in float64, the reference's forward-error
 estimate, double-double re-measure and re-solve above tolerance/20 and a
 dense LU fallback (sfft_sas_decode).  With mu* = 1 (e.g. r = pivots(J),
 config 3) it is a single Hi-DFT read scaled by N/|I| in the input precision.
-Node weights up to 64 are decoded on the device.
+Node weights up to 64 are decoded one (signal, node) per thread, heavier
+nodes (up to 1024) one per CTA with their arrays in shared memory.
 """
 
 from __future__ import annotations
@@ -286,8 +287,8 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
         n_esc = n_fb = 0
         resid_h = flags_h = None
     else:
-        if mu > 64:
-            raise NotImplementedError(f"node weight mu*={mu} above the device decoder's 64")
+        if mu > 1024:
+            raise NotImplementedError(f"node weight mu*={mu} above the device decoder's 1024")
         nodevals = torch.empty((B * mu, nn), dtype=torch.complex128, device=dev)
         sig_ptr, ld_sig, sig_dt, table, blJ, blc, ksrc = None, 0, 0, None, None, None, 0
         if src.kind in ("callable", "synth"):

@@ -164,3 +164,29 @@ def test_select_pivots_policies(S):
     sub = S.SupportSet(1 << 12, K[:9])
     t = int(math.floor(math.log2(9) - math.log2(math.log2(9))))
     assert S.select_pivots(sub, "random_subset", {"base_pivots": base}) == base[:t]
+
+
+def test_sas_heavy_nodes_match_reference(S):
+    """Node weights above 64 (the CTA-per-node decode path, up to 1024):
+    mu* = 100 (one node: the k x k Vandermonde of the submatrix method) and
+    prefixes leaving nodes of weight 74-91, band-limited sources with
+    double-double escalation, against the unmodified reference
+    (tests/golden/make_golden_sas_big.py): plan and node weights identical,
+    coefficients equal to the reference's within the accuracy the
+    reference's own conditioning leaves (its error against the planted
+    spectrum)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_sas_big.npz"))
+    for i in range(int(g["n_cases"][0])):
+        p = f"b{i}_"
+        N, J, c = int(g[p + "N"][0]), g[p + "J"], g[p + "c"]
+        r = tuple(int(x) for x in g[p + "r"])
+        Js = S.SupportSet(N, J)
+        res = S.sas_transform(S.BandlimitedSignal(Js, c), Js, r=r, policy="balanced", family_meta={"pivots": r})
+        assert (res.plan.decode_level, res.plan.mu_star) == tuple(int(x) for x in g[p + "plan"])
+        assert res.plan.node_weights == tuple(int(x) for x in g[p + "weights"])
+        got = res.coeffs.detach().cpu().numpy() if hasattr(res.coeffs, "detach") else np.asarray(res.coeffs)
+        want = g[p + "coeffs"]
+        ref_err = float(np.max(np.abs(want - c)))
+        diff = float(np.max(np.abs(got - want)))
+        assert diff <= max(1e-8, 2.0 * ref_err), (i, diff, ref_err)
