@@ -379,6 +379,76 @@ def measure_config(args, cfg: int, S, W, torch, dev, rank: int, world: int, dist
     return res, state
 
 
+def measure_interleaved(args, cfg: int, S, W, torch, dev, steps: int) -> dict:
+    """The same transform on the batch stored sample-major ((N, B): column b =
+    signal b, sfft_hidft_interleaved): each needed sample index of a CTA's
+    signals is one contiguous run, so G (32 B sectors) equals the element
+    bytes.  Secondary line beside the (B, N) headline."""
+    spec = W.CONFIGS[cfg]
+    B = args.batch or spec["B"]
+    wl = W.make_workload(cfg, B)
+    cdt = torch.complex64 if wl.dtype == "complex64" else torch.complex128
+    esz = 8 if cdt == torch.complex64 else 16
+    J = S.SupportSet(wl.N, wl.support)
+    piv = S.pivots(J)
+    A = 1 << len(piv)
+    step_bytes = A * B * esz
+    # L2: one copy of the batch, the steps rotate over R shifts; the pattern's
+    # offsets are multiples of q = 2^(M-1-r_max), so shifts 0..q-1 read
+    # disjoint sample rows (config 2: q = 32, 32 x 8 MiB of rows vs 126 MB L2)
+    q = 1 << (wl.M - 1 - piv[-1])
+    R = max(1, min(q, 64))
+    rows = torch.empty((B, wl.N), dtype=cdt, device=dev)
+    W.synthesize_into(rows, wl.support, wl.coeffs)
+    nb = rows.T.contiguous()
+    del rows
+    out = torch.empty((B, wl.k), dtype=cdt, device=dev)
+    S.hidft_to_dft_interleaved(nb, J, out=out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    err = float(np.max(np.linalg.norm(got - wl.coeffs, axis=1) / np.linalg.norm(wl.coeffs, axis=1)))
+    tol = 1e-5 if esz == 8 else 1e-11
+    if not err < tol:
+        raise SystemExit(f"interleaved parity gate failed: rel L2 {err:.3e}")
+    GS = R * max(1, math.ceil(args.graph_steps / R))
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for i in range(R):
+            S.hidft_to_dft_interleaved(nb, J, out=out, shift=i)
+    torch.cuda.current_stream(dev).wait_stream(side)
+    with torch.cuda.graph(g):
+        with S.stream_chain():
+            for i in range(GS):
+                S.hidft_to_dft_interleaved(nb, J, out=out, shift=i % R)
+    reps = max(1, steps // GS)
+    for _ in range(max(1, args.warmup // GS + 1)):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * GS)
+    hbm = float(measured_peaks().get("hbm_gbs", 6650.0))
+    G = step_bytes + B * wl.k * esz + wl.support.size * 8
+    ach = G / (ms / 1e3) / 1e9
+    del nb
+    torch.cuda.empty_cache()
+    return {"layout": "(N, B) sample-major: sample n of signal b at n * B + b (sfft_hidft_interleaved)",
+            "value": B * wl.k / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": reps * GS,
+            "gpu_launches": reps * GS,
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(ach / hbm, 4), "algorithmic_bytes_per_launch": int(G),
+                         "note": "gather runs of 8 signals (64 B): G at 32 B sectors = element bytes"},
+            "parity": {"rel_l2_vs_planted_max": err, "tol": tol},
+            "l2": f"rotating {R} shifts reading disjoint sample rows, {R * step_bytes / 2**20:.0f} MiB of gathered "
+                  f"samples per cycle vs 126 MB L2"}
+
+
 def fma_peaks() -> dict:
     """Non-tensor FMA peaks: profiles/fma_peak.json (tools/fma_peak.cu on the
     GPU box, committed) or the round-1 measurement."""
@@ -454,6 +524,13 @@ def run_b200(args) -> None:
     del st
     torch.cuda.empty_cache()
 
+    layouts = {}
+    if world == 1 and not args.no_per_config and args.config in (1, 2):
+        try:
+            layouts["interleaved"] = measure_interleaved(args, args.config, S, W, torch, dev, args.steps)
+        except SystemExit as e:
+            layouts["interleaved"] = {"error": str(e)}
+
     # every other config on the record (N = 1): same discipline, same run
     per_config = {}
     if world == 1 and not args.no_per_config:
@@ -495,6 +572,8 @@ def run_b200(args) -> None:
             line["peer_gather"] = peer_info
         if cpu:
             line["cpu_baseline"] = cpu
+        if layouts:
+            line["layouts"] = layouts
         if per_config:
             line["per_config"] = per_config
         print(json.dumps(line), flush=True)

@@ -140,6 +140,15 @@ SFFT_API int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B, i
                int64_t shift, int out_kind, void* out, int64_t ld_out, void* slot_out,
                int64_t ld_slot, sfft_stream_t stream);
 
+/* sfft_hidft on a batch stored sample-major: sample n of signal b at
+ * signals[n * ld + b] (an (N, B) matrix, ld >= B), e.g. a device array
+ * filled signal-interleaved.  The SG signals of a CTA read each needed
+ * sample index as one contiguous run, so the gather moves useful sectors
+ * instead of one 128 B line per sample (configs 2-4).  Outputs as
+ * sfft_hidft (B rows of ld_out); 2^s <= 4096 (c64) / 2048 (c128). */
+SFFT_API int sfft_hidft_interleaved(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld,
+                                    int64_t shift, int out_kind, void* out, int64_t ld_out, sfft_stream_t stream);
+
 /* Number of kernel launches sfft_hidft / sfft_hidft_gathered issue on the
  * stream for `rows` rows with this plan (1, or 2 per row chunk of the split
  * transform for 2^s beyond one CTA). */

@@ -15,7 +15,7 @@ from .counting import OpCounter
 from .errors import (BudgetExceededError, ContractViolationError, DeviceError, InvalidInputError,
                      StructFFTError)
 from .hidft import (ButterflyPlan, HiDftResult, get_plan, hidft, hidft_to_dft, hidft_to_dft_batched,
-                    stream_chain)
+                    hidft_to_dft_interleaved, stream_chain)
 from .sampling import SamplingPattern, pivoted_pattern, pivoted_pattern_tensor
 from .signals import BandlimitedSignal
 from .sas import (CostReport, NodeSystem, SasPlan, SasResult, predicted_cost, sas_transform,

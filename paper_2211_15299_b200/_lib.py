@@ -60,6 +60,7 @@ SIGNATURES = [
     ("sfft_host_gather", _c.c_int, [_P, _I64, _I64, _c.c_int, _P, _I64, _P, _c.c_int]),
     ("sfft_plan_batched", _c.c_int, [_P, _I64, _I64, _c.c_int, _c.c_int, _P, _P]),
     ("sfft_launch_count", _c.c_int, [_P, _I64, _P]),
+    ("sfft_hidft_interleaved", _c.c_int, [_P, _P, _I64, _I64, _I64, _c.c_int, _P, _I64, _P]),
     ("sfft_stream_chain", _c.c_int, [_P, _c.c_int]),
     ("sfft_hidft_to_dft_fused_host", _c.c_int, [_P, _I64, _c.c_int, _P, _I64, _I64, _c.c_int, _P, _I64,
                                                 _c.c_int, _P]),

@@ -8,7 +8,17 @@
 
 #include "structfft_b200.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no cost without an attached tool
+
 namespace sfft {
+
+// NVTX range over one C-ABI call (nsys / ncu --nvtx show the library's calls
+// as named ranges around their kernels); SFFT_NVTX(name) at function entry
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define SFFT_NVTX(name) ::sfft::NvtxRange sfft_nvtx_range__(name)
 
 // ------------------------------------------------------------ complex ---
 template <typename T> struct Cx;

@@ -276,6 +276,7 @@ extern "C" int sfft_hidft_to_dft_fused(const int64_t* J, int64_t k, int64_t n_su
                                        const void* signals, int64_t B, int64_t ld, int dtype,
                                        void* out, int64_t ld_out, int32_t* status,
                                        sfft_stream_t stream) {
+  SFFT_NVTX("sfft_hidft_to_dft_fused");
   return fused_to_dft(J, k, n_supports, M, signals, B, ld, dtype, out, ld_out, status, (cudaStream_t)stream);
 }
 

@@ -369,6 +369,7 @@ extern "C" int sfft_launch_count(const sfft_plan* plan, int64_t rows, int64_t* l
 extern "C" int sfft_hidft(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld,
                           int64_t shift, int out_kind, void* out, int64_t ld_out, void* slot_out,
                           int64_t ld_slot, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_hidft");
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   return hidft_common(plan, signals, B, ld, 1ll << plan->M, shift, out_kind, out, ld_out, slot_out,
                       ld_slot, 0, (cudaStream_t)stream);
@@ -385,6 +386,7 @@ int hidft_gathered(const sfft_plan* plan, const void* samples, int64_t B, int64_
 extern "C" int sfft_hidft_staged(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld, int order,
                                  int out_kind, void* out, int64_t ld_out, void* slot_out, int64_t ld_slot,
                                  sfft_stream_t stream) {
+  SFFT_NVTX("sfft_hidft_staged");
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   if (order != SFFT_ORDER_SLOT && order != SFFT_ORDER_PATTERN) return fail(SFFT_ERR_INVALID, "unknown sample order");
   return hidft_gathered(plan, samples, B, ld, order == SFFT_ORDER_PATTERN, out_kind, out, ld_out, slot_out, ld_slot,
@@ -394,6 +396,7 @@ extern "C" int sfft_hidft_staged(const sfft_plan* plan, const void* samples, int
 extern "C" int sfft_hidft_gathered(const sfft_plan* plan, const void* samples, int64_t B, int64_t ld,
                                    int out_kind, void* out, int64_t ld_out, void* slot_out,
                                    int64_t ld_slot, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_hidft_gathered");
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   return hidft_common(plan, samples, B, ld, plan->A, 0, out_kind, out, ld_out, slot_out, ld_slot, 1,
                       (cudaStream_t)stream);
@@ -402,6 +405,7 @@ extern "C" int sfft_hidft_gathered(const sfft_plan* plan, const void* samples, i
 extern "C" int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const void* slot_values,
                                    int64_t B, int64_t ld, void* out, int64_t ld_out,
                                    sfft_stream_t stream) {
+  SFFT_NVTX("sfft_plan_apply_map");
   cudaStream_t st = (cudaStream_t)stream;
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   if (int rj = reject_per_signal(plan, "sfft_plan_apply_map")) return rj;

@@ -320,6 +320,7 @@ using namespace sfft;
 
 extern "C" int sfft_host_gather(const void* signals, int64_t B, int64_t ld, int esz, const int64_t* locations,
                                 int64_t A, void* out, int nthreads) {
+  SFFT_NVTX("sfft_host_gather");
   if (!signals || !locations || !out) return fail(SFFT_ERR_INVALID, "null pointer");
   if (esz != 8 && esz != 16) return fail(SFFT_ERR_INVALID, "element size must be 8 or 16 bytes");
   if (B < 0 || A < 0 || ld < 0) return fail(SFFT_ERR_INVALID, "negative size");
@@ -345,6 +346,7 @@ extern "C" int sfft_host_gather(const void* signals, int64_t B, int64_t ld, int 
 extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int64_t shift,
                                int out_kind, void* out, int64_t ld_out, void* slot_out, int64_t ld_slot,
                                int64_t chunk_rows, int nthreads, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_hidft_host");
   cudaStream_t st = (cudaStream_t)stream;
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   if (int rj = reject_per_signal(plan, "sfft_hidft_host")) return rj;
@@ -501,6 +503,7 @@ extern "C" int sfft_hidft_host(const sfft_plan* plan, const void* signals, int64
 extern "C" int sfft_host_stage(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int in_dtype,
                                int64_t shift0, int64_t nshift, int order, int out_dtype, void* dev_out,
                                int64_t ld_out, int nthreads, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_host_stage");
   cudaStream_t st = (cudaStream_t)stream;
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   if (int rj = reject_per_signal(plan, "sfft_host_stage")) return rj;
@@ -570,6 +573,7 @@ extern "C" int sfft_host_stage(const sfft_plan* plan, const void* signals, int64
 extern "C" int sfft_hidft_to_dft_fused_host(const int64_t* J, int64_t k, int M, const void* signals, int64_t B,
                                             int64_t ld, int dtype, void* out, int64_t ld_out, int nthreads,
                                             sfft_stream_t stream) {
+  SFFT_NVTX("sfft_hidft_to_dft_fused_host");
   cudaStream_t st = (cudaStream_t)stream;
   if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
   if (dtype != SFFT_C64 && dtype != SFFT_C128) return fail(SFFT_ERR_INVALID, "unknown dtype");

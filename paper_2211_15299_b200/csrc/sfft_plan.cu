@@ -581,6 +581,7 @@ extern "C" int sfft_device_ok(void) {
 
 extern "C" int sfft_analyze(const int64_t* J, int64_t k, int M, uint64_t* pivot_mask, int* homogeneous,
                             sfft_stream_t stream) {
+  SFFT_NVTX("sfft_analyze");
   cudaStream_t st = (cudaStream_t)stream;
   if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
   if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
@@ -608,6 +609,7 @@ __global__ void k_pattern(const int32_t* __restrict__ r, int n, int M, int64_t* 
 }
 
 extern "C" int sfft_pivoted_pattern(const int32_t* r, int n_r, int M, int64_t* out, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_pivoted_pattern");
   cudaStream_t st = (cudaStream_t)stream;
   if (M < 1 || M > 62) return fail(SFFT_ERR_INVALID, "M out of range");
   int rc = validate_r(r, n_r, M);
@@ -900,6 +902,7 @@ static void plan_free(sfft_plan* p) {
 
 extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_t* r, int n_r, int height,
                                 int dtype, sfft_stream_t stream, sfft_plan** out_plan) {
+  SFFT_NVTX("sfft_plan_create");
   cudaStream_t st = (cudaStream_t)stream;
   if (!out_plan) return fail(SFFT_ERR_INVALID, "null plan output");
   *out_plan = nullptr;
@@ -1144,6 +1147,7 @@ __global__ void k_tree_close(int32_t* __restrict__ node_off, const int32_t* __re
 
 extern "C" int sfft_tree_build(const int64_t* J, int64_t k, int M, int level_lo, int level_hi, int64_t* members,
                                int32_t* node_off, int32_t* n_nodes, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_tree_build");
   cudaStream_t st = (cudaStream_t)stream;
   if (M < 1 || M > 28) return fail(SFFT_ERR_UNSUPPORTED, "congruence tree on the device needs 1 <= M <= 28");
   if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");
@@ -1207,6 +1211,7 @@ extern "C" int sfft_tree_build(const int64_t* J, int64_t k, int M, int level_lo,
 
 extern "C" int sfft_plan_batched(const int64_t* J, int64_t k, int64_t n_supports, int M, int dtype,
                                  sfft_stream_t stream, sfft_plan** out_plan) {
+  SFFT_NVTX("sfft_plan_batched");
   cudaStream_t st = (cudaStream_t)stream;
   if (!out_plan) return fail(SFFT_ERR_INVALID, "null plan output");
   *out_plan = nullptr;
@@ -1347,6 +1352,7 @@ __global__ void k_prefix_reduce(const uint32_t* __restrict__ hist, int s, unsign
 
 extern "C" int sfft_prefix_weights(const int64_t* J, int64_t k, int M, const int32_t* piv, int s,
                                    uint64_t* mu_out, uint64_t* sumsq_out, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_prefix_weights");
   cudaStream_t st = (cudaStream_t)stream;
   if (M < 1 || M > 31) return fail(SFFT_ERR_INVALID, "M must lie in [1, 31]");
   if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");

@@ -838,6 +838,7 @@ using namespace sfft;
 static std::mutex g_nodes_mu;
 
 extern "C" int sfft_plan_nodes(sfft_plan* p, int32_t* off_out, int32_t* mem_out, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_plan_nodes");
   cudaStream_t st = (cudaStream_t)stream;
   if (!p) return fail(SFFT_ERR_INVALID, "null plan");
   if (int rj = reject_per_signal(p, "sfft_plan_nodes")) return rj;
@@ -875,6 +876,7 @@ extern "C" int sfft_plan_nodes(sfft_plan* p, int32_t* off_out, int32_t* mem_out,
 extern "C" int sfft_hidft_shifts(const sfft_plan* plan, const void* signals, int64_t B, int64_t ld, int in_dtype,
                                  int64_t shift0, int64_t nshift, int out_kind, void* out, int64_t ld_out,
                                  sfft_stream_t stream) {
+  SFFT_NVTX("sfft_hidft_shifts");
   if (!plan) return fail(SFFT_ERR_INVALID, "null plan");
   if (int rj = reject_per_signal(plan, "sfft_hidft_shifts")) return rj;
   if (nshift < 1) return fail(SFFT_ERR_INVALID, "nshift must be >= 1");
@@ -901,6 +903,7 @@ extern "C" int sfft_sas_decode(sfft_plan* p, const void* nodevals, int64_t ld_nv
                                const int64_t* J_dev,
                                void* out, int64_t ld_out, int32_t* flags, double* resid, int64_t* n_escalated,
                                int64_t* n_fallback, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_sas_decode");
   cudaStream_t st = (cudaStream_t)stream;
   if (!p) return fail(SFFT_ERR_INVALID, "null plan");
   if (int rj = reject_per_signal(p, "sfft_sas_decode")) return rj;

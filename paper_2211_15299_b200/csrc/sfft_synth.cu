@@ -50,6 +50,7 @@ using namespace sfft;
 
 extern "C" int sfft_synthesize(const int64_t* J, const void* coeffs, int64_t k, int M, const int64_t* locations,
                                int64_t n, void* out, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_synthesize");
   cudaStream_t st = (cudaStream_t)stream;
   if (M < 1 || M > 62) return fail(SFFT_ERR_INVALID, "M out of range");
   if (k < 1) return fail(SFFT_ERR_INVALID, "support set is empty");

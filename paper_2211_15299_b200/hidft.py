@@ -471,6 +471,41 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
     return out[0] if single else out
 
 
+def hidft_to_dft_interleaved(signals, J, out=None, shift: int = 0):
+    """hidft_to_dft for a batch stored sample-major: `signals` is an (N, B)
+    CUDA tensor whose column b is signal b (any row stride >= B, unit column
+    stride).  Returns (B, k) coefficients in ascending-J order, identical to
+    hidft_to_dft_batched(signals.T.contiguous(), J); `shift` reads the
+    samples at (I - shift) mod N (core.py:3-6).  The gather reads each
+    needed sample index of SG neighbouring signals as one contiguous run
+    (sfft_hidft_interleaved) instead of one 128 B line per sample."""
+    torch = _torch()
+    _lib.require_device()
+    if not torch.is_tensor(signals) or not signals.is_cuda or signals.dim() != 2:
+        raise InvalidInputError("signals must be an (N, B) CUDA tensor")
+    if signals.dtype not in (torch.complex64, torch.complex128):
+        raise InvalidInputError("signals must be complex64 or complex128")
+    N, B = signals.shape
+    if signals.stride(1) != 1 or signals.stride(0) < B:
+        raise InvalidInputError("signals need unit column stride and row stride >= B")
+    Js = as_support(J)
+    if Js.N != N:
+        raise InvalidInputError("signal modulus does not match support")
+    cls = classify(Js)
+    if not cls.is_homogeneous:
+        raise ContractViolationError("hidft_to_dft requires a homogeneous support")
+    dev = signals.device
+    plan = get_plan(Js, cls.pivots, 0, _DT[signals.dtype], dev)
+    k = len(Js)
+    if out is None:
+        out = torch.empty((B, k), dtype=signals.dtype, device=dev)
+    else:
+        _check_out(out, (B, k), signals.dtype, dev, "out")
+    _lib.check(_lib.load().sfft_hidft_interleaved(plan.handle, signals.data_ptr(), B, signals.stride(0), int(shift),
+                                                  _lib.OUT_DFT, out.data_ptr(), out.stride(0), _lib.stream_ptr(dev)))
+    return out
+
+
 class stream_chain:
     """Context manager: consecutive library calls on `stream` (default: the
     current stream of the current device) may overlap through programmatic

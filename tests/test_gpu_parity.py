@@ -949,3 +949,27 @@ def test_output_guard_regions(S, torch, case):
     row = sig[0].cpu().numpy()
     ref = O.hidft_to_dft(row, J[0].cpu().numpy() if torch.is_tensor(J) else J.as_array(), M)
     assert rel_l2(want[0].cpu().numpy(), ref) < (1e-5 if dt == torch.complex64 else 1e-11)
+
+
+@pytest.mark.parametrize("M,piv,B,dt,pad", [(20, (0, 1, 2, 4, 5, 7, 8, 11, 12, 14), 37, "c64", 0),
+                                             (16, (2, 3, 6, 9, 12, 13, 14, 15), 16, "c128", 3),
+                                             (14, tuple(range(12)), 9, "c64", 5),
+                                             (13, tuple(range(11)), 6, "c128", 0),
+                                             (10, (1, 4), 3, "c64", 1)])
+def test_interleaved_layout_matches_row_major(S, torch, M, piv, B, dt, pad):
+    """sfft_hidft_interleaved on an (N, B) sample-major batch (row stride
+    B + pad) gives bitwise the coefficients of the row-major call on the same
+    signals (same plan, same butterfly), and the oracle's."""
+    N = 1 << M
+    cdt = torch.complex64 if dt == "c64" else torch.complex128
+    Jn = O.gen_homogeneous(piv, M, 21)
+    J = S.SupportSet(N, Jn)
+    rows = torch.randn(B, N, dtype=cdt, device="cuda")
+    store = torch.zeros(N, B + pad, dtype=cdt, device="cuda")
+    store[:, :B] = rows.T
+    got = S.hidft_to_dft_interleaved(store[:, :B], J)
+    want = S.hidft_to_dft_batched(rows, J)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    ref = O.hidft_to_dft(rows[B - 1].cpu().numpy(), Jn, M)
+    assert rel_l2(got[B - 1].cpu().numpy(), ref) < (1e-5 if dt == "c64" else 1e-11)
