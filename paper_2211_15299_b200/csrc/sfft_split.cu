@@ -933,8 +933,12 @@ struct HeadGeo {
   static constexpr int NTT = NT + 32;        // + one warp that issues the tensor copies
   static constexpr int NPASS = (SQ + LE - 1) / LE;
   static constexpr int NTW = NQ - 16;        // stage-major twiddles 15 .. NQ-2 (stages 5 .. SQ)
-  // landing buffer (TMA) + working buffer (swizzled slots) + twiddles + 2 mbarriers
-  static constexpr size_t SMEM = 2 * (size_t)P * NQ * sizeof(Cx<T>) + (size_t)NTW * sizeof(Cx<T>) + 16;
+  // NL landing buffers (TMA) + working buffer (swizzled slots) + twiddles + 2 NL mbarriers
+#ifndef SFFT_HEAD_NL  // landing buffers (config 5, one box: 1 -> 126.5 us, 2 -> 126.1 us per step)
+#define SFFT_HEAD_NL 1
+#endif
+  static constexpr int NL = P == 2 ? SFFT_HEAD_NL : 1;
+  static constexpr size_t SMEM = (NL + 1) * (size_t)P * NQ * sizeof(Cx<T>) + (size_t)NTW * sizeof(Cx<T>) + 16 * NL;
   static_assert(sizeof(T) == 4 && SQ >= 2 * LE && E <= TPB, "head pass: complex64, at least 2 register passes");
 };
 
@@ -956,11 +960,30 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
 // barrier among the NT transform threads only (the copy warp runs its own loop)
 template <int NT>
 __device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
+// barrier among the warps of one b value's group (named barrier 2 + group);
+// SFFT_HEAD_GROUPS=0 (default): one barrier over all transform threads
+// (config 5: per-group barriers 126.1-126.4 us against 126.5 us per step; the
+// pass is bound by the TMA row rate and the transform's latency, tools/tma_box_probe.cu)
+#ifndef SFFT_HEAD_GROUPS
+#define SFFT_HEAD_GROUPS 0
+#endif
+#if SFFT_HEAD_GROUPS
+#define HEAD_SYNC() group_sync<NTG>(bl)
+#else
+#define HEAD_SYNC() work_sync<NT>()
+#endif
+template <int NTG>
+__device__ __forceinline__ void group_sync(int grp) { asm volatile("bar.sync %0, %1;" :: "r"(2 + grp), "n"(NTG) : "memory"); }
 
 // Persistent: CTA i serves units i, i + grid, ...; a copy warp fills the
 // landing buffer with unit u+1 (tensor copies; it alone stalls when the TMA
 // queue is full) as soon as the transform threads have read unit u from it,
 // so the copies run while unit u is transformed in the working buffer.
+// Persistent: CTA i serves units i, i + grid, ...; a copy warp fills NL
+// landing buffers with the next units (tensor copies; it alone stalls when
+// the TMA queue is full) as soon as the transform threads have read the
+// buffer's previous unit, so the copies of units u+1 and u+2 run while unit
+// u is transformed in the working buffer.
 template <typename T, int S, int P>
 __global__ void __launch_bounds__(HeadGeo<T, S, P>::NTT, 1)
 k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 ftw, const Cx<T>* __restrict__ tw,
@@ -969,14 +992,17 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
   constexpr int SQ = HG::SQ, NQ = HG::NQ, E = HG::E, LE = HG::LE, TPB = HG::TPB, NT = HG::NT, NC = HG::NC;
   constexpr int LP = P == 4 ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Cx<T>* land = reinterpret_cast<Cx<T>*>(smem_raw);  // P x NQ, TMA box order
-  Cx<T>* work = land + P * NQ;                       // P x NQ, swizzled slots per b value
+  constexpr int NL = HG::NL, NTG = NT / P;
+  Cx<T>* land = reinterpret_cast<Cx<T>*>(smem_raw);  // NL x P x NQ, TMA box order
+  Cx<T>* work = land + NL * P * NQ;                  // P x NQ, swizzled slots per b value
   Cx<T>* stw = work + P * NQ;                        // twiddles of stages 5 .. SQ
-  const uint32_t full = smem_addr(stw + HG::NTW), empty = full + 8;
+  const uint32_t full0 = smem_addr(stw + HG::NTW), empty0 = full0 + 8 * NL;  // full[NL], empty[NL]
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(full, 1);
-    mbar_init(empty, NT / 32);
+    for (int i = 0; i < NL; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, NT / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -985,7 +1011,17 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
     const int box = (NQ / ht.nops) * P;
     uint32_t it = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-      if (it > 0) mbar_wait(empty, (it - 1) & 1);  // the transform threads have read the landing buffer
+      const int lb = it % NL;
+      const uint32_t full = full0 + 8 * lb;
+      Cx<T>* lbuf = land + lb * P * NQ;
+      // landing buffer lb is free once the transform threads read unit it - NL from it
+      if (it >= (uint32_t)NL) mbar_wait(empty0 + 8 * lb, ((it - NL) / NL) & 1);
+#if defined(SFFT_HEAD_PROBE) && SFFT_HEAD_PROBE == 2  // timing probe: copies of the first units only
+      if (it >= (uint32_t)NL) {
+        if (lane == 0) mbar_arrive(full);
+        continue;
+      }
+#endif
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
@@ -1009,19 +1045,22 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
         const int c4 = (int)(row0 + rr);
         asm volatile(
             "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
-            :: "r"(smem_addr(land + (size_t)o * box)), "l"(&tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+            :: "r"(smem_addr(lbuf + (size_t)o * box)), "l"(&tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
                "r"(full) : "memory");
       }
     }
     return;
   }
-  // Thread bits 4..4+LP-1 pick the b value inside the piece, so each
-  // half-warp works on one b value: its 16 lanes hit 16 distinct 8 B word
-  // slots in the swizzled passes (conflict-free); pass-0 thread bit i holds
-  // q bit tq[i] (host order: ascending landing weight).
+  // Warp bits 0..LP-1 pick the b value inside the piece: each b value's
+  // transform is done by its own group of NT/P threads with its own named
+  // barriers, so the groups drift out of phase and overlap each other's
+  // shared-memory and FMA phases (as two CTAs would); a half-warp works on
+  // one b value, so its 16 lanes hit 16 distinct 8 B word slots in the
+  // swizzled passes (conflict-free).  Pass-0 thread bit i holds q bit tq[i]
+  // (host order: ascending landing weight).
   for (int i = tid; i < HG::NTW; i += NT) cp_async_elem(stw + i, tw + 15 + i);
   cp_async_commit();
-  const int bl = (tid >> 4) & (P - 1), tt = (tid & 15) | ((tid >> (4 + LP)) << 4);
+  const int bl = (tid >> 5) & (P - 1), tt = (tid & 31) | ((tid >> (5 + LP)) << 5);
   uint32_t qt = 0, base = 0;
 #pragma unroll
   for (int i = 0; i < SQ - LE; ++i)
@@ -1032,21 +1071,39 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
   const int tb0 = swz<T, SQ>((int)qt);
   Cx<T>* sb = work + bl * NQ;
   cp_async_wait<0>();
+  work_sync<NT>();  // twiddles staged by all groups
   bool waited = false;
   uint32_t it = 0;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
     Cx<T> v[E];
-    mbar_wait(full, it & 1);
+    const int lb = it % NL;
+    const Cx<T>* lbuf = land + lb * P * NQ;
+    mbar_wait(full0 + 8 * lb, (it / NL) & 1);
 #pragma unroll
     for (int x = 0; x < E; ++x) {
       uint32_t q = base;
 #pragma unroll
       for (int i = 0; i < LE; ++i)
         if ((x >> i) & 1) q += ht.qw[i];
-      v[x] = land[q * P + bl];
+      v[x] = lbuf[q * P + bl];
     }
-    work_sync<NT>();  // landing reads done; the previous unit's epilogue reads of work done
-    if ((tid & 31) == 0) mbar_arrive(empty);
+    HEAD_SYNC();  // the group's landing reads and its previous epilogue reads of work done
+    if ((tid & 31) == 0) mbar_arrive(empty0 + 8 * lb);
+#if defined(SFFT_HEAD_PROBE) && SFFT_HEAD_PROBE == 1  // timing probe: copies and scratch stores only
+    if (!waited) {
+      pdl_wait();
+      pdl_release();
+      waited = true;
+    }
+    {
+      const int64_t rr = u / NC;
+      const int b = (int)(u % NC) | (LP == 1 ? (bl << 3) : (((bl & 1) << 3) | ((bl >> 1) << 2)));
+      Cx<T>* dst = scratch + ((int64_t)rr << S) + ((int64_t)b << SQ) + tt;
+#pragma unroll
+      for (int n = 0; n < E; ++n) dst[n * TPB] = v[n];
+    }
+    continue;
+#endif
     // stages 1..LE: twiddle index a mod 2^beta = x mod 2^beta, uniform over the grid
 #pragma unroll
     for (int beta = 0; beta < LE; ++beta) {
@@ -1059,7 +1116,7 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
     }
 #pragma unroll
     for (int x = 0; x < E; ++x) sb[tb0 ^ swz<T, SQ>(x)] = v[x];
-    work_sync<NT>();
+    HEAD_SYNC();
 #pragma unroll
     for (int p = 1; p < HG::NPASS; ++p) {
       const int tb = swz<T, SQ>(slot_t<SQ, LE>(p, tt));
@@ -1084,7 +1141,7 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
       }
 #pragma unroll
       for (int x = 0; x < E; ++x) sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))] = v[x];  // in place: same positions
-      work_sync<NT>();
+      HEAD_SYNC();
     }
     if (!waited) {
       pdl_wait();  // scratch is free (the previous chunk's final pass completed)
