@@ -37,7 +37,11 @@ namespace sfft {
 // complex64 rows (config 3) use 32 per thread: 512 threads, three register
 // passes (5 + 5 + 4 stages) instead of four, so the one CTA per SM spends
 // less time in the butterfly with its share of HBM idle (209 -> 197 us)
-template <typename T, int S> constexpr int plan_e() { return (sizeof(T) == 4 && S == 14) ? SFFT_PLAN_E14 : 0; }
+// 2^13-slot complex128 rows: 16 per thread (512 threads, up to 128 registers)
+// instead of 8 (1024 threads at 64 registers spilled 24 B)
+template <typename T, int S> constexpr int plan_e() {
+  return (sizeof(T) == 4 && S == 14) ? SFFT_PLAN_E14 : (sizeof(T) == 8 && S == 13) ? 16 : 0;
+}
 
 template <typename T, int S>
 __global__ void __launch_bounds__(Geo<T, S, plan_e<T, S>()>::NT, Geo<T, S, plan_e<T, S>()>::MINB)

@@ -973,3 +973,23 @@ def test_interleaved_layout_matches_row_major(S, torch, M, piv, B, dt, pad):
     assert torch.equal(got, want)
     ref = O.hidft_to_dft(rows[B - 1].cpu().numpy(), Jn, M)
     assert rel_l2(got[B - 1].cpu().numpy(), ref) < (1e-5 if dt == "c64" else 1e-11)
+
+
+@pytest.mark.parametrize("dt", ["c64", "c128"])
+def test_s13_single_cta_plan_kernel(S, torch, dt):
+    """2^13 slots on one CTA (complex128: 16 slots per thread, 512 threads)
+    against the oracle, with a shift and at height 0."""
+    M, piv = 16, tuple(range(2, 15))
+    N = 1 << M
+    cdt = torch.complex64 if dt == "c64" else torch.complex128
+    Jn = O.gen_homogeneous(piv, M, 8)
+    J = S.SupportSet(N, Jn)
+    sig = torch.randn(3, N, dtype=cdt, device="cuda")
+    got = S.hidft_to_dft_batched(sig, J).cpu().numpy()
+    for b in range(3):
+        want = O.hidft_to_dft(sig[b].cpu().numpy(), Jn, M)
+        assert rel_l2(got[b], want) < (1e-5 if dt == "c64" else 1e-11)
+    res = S.hidft(sig[1], J, S.pivots(J), shift=123)
+    ref = O.hidft(sig[1].cpu().numpy()[None, :], Jn, M, S.pivots(J), shift=123)
+    vals = res.node_values.cpu().numpy() if hasattr(res.node_values, "cpu") else res.node_values
+    assert rel_l2(np.asarray(vals).reshape(-1), np.asarray(ref.node_values).reshape(-1)) < (1e-5 if dt == "c64" else 1e-11)
