@@ -71,6 +71,31 @@ int main(void) {
   free(hsig);
   if (herr != 0.0) return 4;
 
+  /* the same signal stored sample-major (an (N, 2) batch: two copies side by side),
+   * inside a PDL chain scope on the default stream */
+  double* dnb;
+  cudaMalloc((void**)&dnb, 32 * N);
+  cudaMemcpy2D(dnb, 32, dsig, 16, 16, N, cudaMemcpyDeviceToDevice);
+  cudaMemcpy2D((char*)dnb + 16, 32, dsig, 16, 16, N, cudaMemcpyDeviceToDevice);
+  CHECK(sfft_stream_chain(0, 1));
+  double* dout2;
+  cudaMalloc((void**)&dout2, 32 * k);
+  CHECK(sfft_hidft_interleaved(plan, dnb, 2, 2, 0, SFFT_OUT_DFT, dout2, k, 0));
+  CHECK(sfft_stream_chain(0, 0));
+  double out2[32];
+  cudaMemcpy(out2, dout2, sizeof out2, cudaMemcpyDeviceToHost);
+  double ierr = 0;
+  for (int i = 0; i < 2 * k; ++i) ierr = fmax(ierr, fmax(fabs(out2[i] - out[i]), fabs(out2[2 * k + i] - out[i])));
+  printf("interleaved layout: max |diff| vs row-major = %.3e\n", ierr);
+  if (ierr != 0.0) return 5;
+
+  /* congruence tree, levels 0..3, host outputs (congruence.py:134-222) */
+  int64_t members[4 * 8];
+  int32_t node_off[4 * 9], n_nodes[4];
+  CHECK(sfft_tree_build(J, k, M, 0, 3, members, node_off, n_nodes, 0));
+  printf("tree nodes per level: %d %d %d %d\n", n_nodes[0], n_nodes[1], n_nodes[2], n_nodes[3]);
+  if (n_nodes[0] != 1 || n_nodes[1] != 2 || n_nodes[2] != 2 || n_nodes[3] != 4) return 6; /* pivots 0, 2 */
+
   /* the contract errors come back as status codes */
   int32_t bad[1] = {5};
   sfft_plan* p2 = NULL;
