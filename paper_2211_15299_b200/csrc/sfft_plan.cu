@@ -797,6 +797,66 @@ static void euler_split(const std::vector<int>& edges, const std::vector<int>& e
   }
 }
 
+// Conflict-free word slots for one store/read pattern: edge e = (store group
+// eu[e], read group ev[e]) is the value q = qof[e]; both groupings are
+// 16-regular over NQ/16 groups.  Four Euler splits cut the edges into 16
+// perfect matchings; matching c is word slot c: posq[q] = 16 * (rank of q
+// in its class) + c.  False when a split is unbalanced (keep the swizzle).
+static bool conflict_free_positions(const std::vector<int>& eu, const std::vector<int>& ev,
+                                    const std::vector<int>& qof, int NQ, std::vector<int32_t>& posq) {
+  const int nv = NQ / 16;
+  std::vector<std::vector<int>> cls(1);
+  cls[0].resize(NQ);
+  for (int e = 0; e < NQ; ++e) cls[0][e] = e;
+  for (int lvl = 0; lvl < 4; ++lvl) {
+    std::vector<std::vector<int>> next;
+    for (auto& c : cls) {
+      std::vector<int> A, B;
+      euler_split(c, eu, ev, nv, A, B);
+      next.push_back(std::move(A));
+      next.push_back(std::move(B));
+    }
+    cls.swap(next);
+  }
+  posq.assign(NQ, -1);
+  for (int c = 0; c < 16; ++c) {
+    if ((int)cls[c].size() != NQ / 16) return false;
+    for (int r = 0; r < (int)cls[c].size(); ++r) posq[qof[cls[c][r]]] = 16 * r + c;
+  }
+  std::vector<char> seen(NQ, 0);
+  for (int q = 0; q < NQ; ++q) {
+    if (posq[q] < 0 || posq[q] >= NQ || seen[posq[q]]) return false;
+    seen[posq[q]] = 1;
+  }
+  // every store and read group hits each word slot once
+  std::vector<int> cs((size_t)nv * 16, 0), cr((size_t)nv * 16, 0);
+  for (int e = 0; e < NQ; ++e) {
+    if (++cs[(size_t)eu[e] * 16 + (posq[qof[e]] & 15)] > 1) return false;
+    if (++cr[(size_t)ev[e] * 16 + (posq[qof[e]] & 15)] > 1) return false;
+  }
+  return true;
+}
+
+static int upload_tables(const std::vector<int32_t>& a, const std::vector<int32_t>& b, int32_t** da, int32_t** db) {
+  int32_t* x = nullptr;
+  int32_t* y = nullptr;
+  SFFT_CUDA(cudaMalloc((void**)&x, 4 * a.size()));
+  if (cudaMalloc((void**)&y, 4 * b.size()) != cudaSuccess) {
+    cudaFree(x);
+    return cuda_fail(cudaGetLastError(), "conflict-free table allocation");
+  }
+  const cudaError_t e1 = cudaMemcpy(x, a.data(), 4 * a.size(), cudaMemcpyHostToDevice);
+  const cudaError_t e2 = cudaMemcpy(y, b.data(), 4 * b.size(), cudaMemcpyHostToDevice);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaFree(x);
+    cudaFree(y);
+    return cuda_fail(e1 != cudaSuccess ? e1 : e2, "conflict-free table upload");
+  }
+  *da = x;
+  *db = y;
+  return SFFT_OK;
+}
+
 static int tri_conflict_free_tables(sfft_plan* p, cudaStream_t st) {
   const int s = p->s;
   const int F = s == 15 ? 3 : 4, L = 4, MID = s - F - L, SQ = s - L;
@@ -820,62 +880,43 @@ static int tri_conflict_free_tables(sfft_plan* p, cudaStream_t st) {
       eu[e] = (tid >> 4) * E2 + x;  // store group: a half-warp's lanes for register x
       ev[e] = pinv[q] >> 4;         // read group: 16 consecutive pi
     }
-  const int nv = NQ / 16;
-  std::vector<std::vector<int>> cls(1);
-  cls[0].resize(NQ);
-  for (int e = 0; e < NQ; ++e) cls[0][e] = e;
-  for (int lvl = 0; lvl < 4; ++lvl) {
-    std::vector<std::vector<int>> next;
-    for (auto& c : cls) {
-      std::vector<int> A, B;
-      euler_split(c, eu, ev, nv, A, B);
-      next.push_back(std::move(A));
-      next.push_back(std::move(B));
-    }
-    cls.swap(next);
-  }
-  std::vector<int32_t> posq(NQ, -1), spos(NQ), ppos(NQ);
-  for (int c = 0; c < 16; ++c) {
-    if ((int)cls[c].size() != NQ / 16) return SFFT_OK;  // not balanced: keep the swizzled layout
-    for (int r = 0; r < (int)cls[c].size(); ++r) posq[qof[cls[c][r]]] = 16 * r + c;
-  }
+  std::vector<int32_t> posq;
+  if (!conflict_free_positions(eu, ev, qof, NQ, posq)) return SFFT_OK;  // keep the swizzled layout
+  std::vector<int32_t> spos(NQ), ppos(NQ);
   for (int e = 0; e < NQ; ++e) spos[e] = posq[qof[e]];
   for (int pi = 0; pi < NQ; ++pi) ppos[pi] = posq[perm[pi]];
-  // check: a bijection, and every store / read half-warp hits each word slot once
-  {
-    std::vector<char> seen(NQ, 0);
-    for (int q = 0; q < NQ; ++q) {
-      if (posq[q] < 0 || posq[q] >= NQ || seen[posq[q]]) return SFFT_OK;
-      seen[posq[q]] = 1;
+  return upload_tables(spos, ppos, &p->d_tri_spos, &p->d_tri_ppos);
+}
+
+// The head pass (sfft_split.cu, k_head) in the same way: its last register
+// pass stores slot(tt, x) from thread tt's register x (a half-warp: 16
+// consecutive tt, fixed x), its epilogue reads pi = tt + n * 2^(SQ-4), q =
+// perm[pi] (a half-warp: 16 consecutive pi).  Tables: spos[x * TPB + tt],
+// ppos[pi], positions inside one b value's 2^SQ-slot block.
+static int head_conflict_free_tables(sfft_plan* p, cudaStream_t st) {
+  const int SQ = p->s - 4, NQ = 1 << SQ, LE = 4, E = 16, TPB = NQ / E;
+  const int NPASS = (SQ + LE - 1) / LE, last = NPASS - 1;
+  const int w0 = (last * LE < SQ - LE) ? last * LE : SQ - LE;
+  if (TPB % 16) return SFFT_OK;
+  std::vector<int32_t> perm(NQ), pinv(NQ);
+  SFFT_CUDA(cudaMemcpyAsync(perm.data(), p->d_tri_perm, 4 * (size_t)NQ, cudaMemcpyDeviceToHost, st));
+  SFFT_CUDA(cudaStreamSynchronize(st));
+  for (int pi = 0; pi < NQ; ++pi) pinv[perm[pi]] = pi;
+  std::vector<int> eu(NQ), ev(NQ), qof(NQ);  // edge index = x * TPB + tt
+  for (int x = 0; x < E; ++x)
+    for (int tt = 0; tt < TPB; ++tt) {
+      const int q = (tt & ((1 << w0) - 1)) | ((tt >> w0) << (w0 + LE)) | (x << w0);
+      const int e = x * TPB + tt;
+      qof[e] = q;
+      eu[e] = x * (TPB / 16) + (tt >> 4);
+      ev[e] = pinv[q] >> 4;
     }
-    for (int g = 0; g < NQ / 16; ++g) {
-      int cs[16] = {0}, cr[16] = {0};
-      for (int l = 0; l < 16; ++l) {
-        const int x = g % E2, h = g / E2;
-        ++cs[spos[x * NT + h * 16 + l] & 15];
-        ++cr[ppos[g * 16 + l] & 15];
-      }
-      for (int c = 0; c < 16; ++c)
-        if (cs[c] != 1 || cr[c] != 1) return SFFT_OK;
-    }
-  }
-  int32_t* ds = nullptr;
-  int32_t* dp = nullptr;
-  SFFT_CUDA(cudaMalloc((void**)&ds, 4 * (size_t)NQ));
-  if (cudaMalloc((void**)&dp, 4 * (size_t)NQ) != cudaSuccess) {
-    cudaFree(ds);
-    return cuda_fail(cudaGetLastError(), "conflict-free table allocation");
-  }
-  cudaError_t e1 = cudaMemcpy(ds, spos.data(), 4 * (size_t)NQ, cudaMemcpyHostToDevice);
-  cudaError_t e2 = cudaMemcpy(dp, ppos.data(), 4 * (size_t)NQ, cudaMemcpyHostToDevice);
-  if (e1 != cudaSuccess || e2 != cudaSuccess) {
-    cudaFree(ds);
-    cudaFree(dp);
-    return cuda_fail(e1 != cudaSuccess ? e1 : e2, "conflict-free table upload");
-  }
-  p->d_tri_spos = ds;
-  p->d_tri_ppos = dp;
-  return SFFT_OK;
+  std::vector<int32_t> posq;
+  if (!conflict_free_positions(eu, ev, qof, NQ, posq)) return SFFT_OK;
+  std::vector<int32_t> spos(NQ), ppos(NQ);
+  for (int e = 0; e < NQ; ++e) spos[e] = posq[qof[e]];
+  for (int pi = 0; pi < NQ; ++pi) ppos[pi] = posq[perm[pi]];
+  return upload_tables(spos, ppos, &p->d_head_spos, &p->d_head_ppos);
 }
 
 static void plan_free(sfft_plan* p) {
@@ -902,6 +943,8 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_tri_inv_node);
   cudaFree(p->d_tri_spos);
   cudaFree(p->d_tri_ppos);
+  cudaFree(p->d_head_spos);
+  cudaFree(p->d_head_ppos);
   cudaFree(p->d_J);
   delete p;
 }
@@ -1095,8 +1138,18 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     const char* e = getenv("SFFT_TRI_CF");
     return !(e && atoi(e) == 0);
   }();
-  if (p->d_tri_perm && dtype == SFFT_C64 && cf && !head_covers(p) && (rc = tri_conflict_free_tables(p, st)))
-    return done(rc);
+  // head-path plans: the conflict-free epilogue tables are opt-in
+  // (SFFT_HEAD_CF=1: k_head 46.1 -> 43.3 us per chunk, the step unchanged at
+  // 126.5-126.9 us, and the host Euler splits add ~4 ms to the plan build)
+  static const bool head_cf = [] {
+    const char* e = getenv("SFFT_HEAD_CF");
+    return e && atoi(e) == 1;
+  }();
+  if (p->d_tri_perm && dtype == SFFT_C64 && cf) {
+    if ((rc = head_covers(p) ? (head_cf ? head_conflict_free_tables(p, st) : SFFT_OK)
+                             : tri_conflict_free_tables(p, st)))
+      return done(rc);
+  }
   trace.mark("conflict-free tables");
   *out_plan = p;
   return SFFT_OK;

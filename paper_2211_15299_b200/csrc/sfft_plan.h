@@ -43,6 +43,9 @@ struct sfft_plan {
   // the permuted epilogue reads, chosen so both are bank-conflict free
   int32_t* d_tri_spos;       // 2^(s-4)  [x][tid] -> position of the value thread tid stores from register x
   int32_t* d_tri_ppos;       // 2^(s-4)  [pi] -> position of q = perm[pi]
+  // the same for the head pass's last register pass and epilogue (k_head)
+  int32_t* d_head_spos;      // 2^(s-4)  [x][tt] -> position of the value thread tt stores from register x
+  int32_t* d_head_ppos;      // 2^(s-4)  [pi] -> position of q = perm[pi]
   // the final pass's output map is blocked: d_tri_inv_*[b][pi] = T * 2^(s-4) + pi
   // for a per-pi bijection b -> T (coalesced staged stores, sfft_split.cu k_fin2)
   int tri_blocked_elem, tri_blocked_node;

@@ -987,7 +987,8 @@ __device__ __forceinline__ void group_sync(int grp) { asm volatile("bar.sync %0,
 template <typename T, int S, int P>
 __global__ void __launch_bounds__(HeadGeo<T, S, P>::NTT, 1)
 k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 ftw, const Cx<T>* __restrict__ tw,
-       const int32_t* __restrict__ perm, Cx<T>* __restrict__ scratch, int64_t row0, int64_t units) {
+       const int32_t* __restrict__ perm, Cx<T>* __restrict__ scratch, int64_t row0, int64_t units,
+       const int32_t* __restrict__ cf_spos, const int32_t* __restrict__ cf_ppos) {
   using HG = HeadGeo<T, S, P>;
   constexpr int SQ = HG::SQ, NQ = HG::NQ, E = HG::E, LE = HG::LE, TPB = HG::TPB, NT = HG::NT, NC = HG::NC;
   constexpr int LP = P == 4 ? 2 : 1;
@@ -1139,8 +1140,17 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
           }
         }
       }
+      if (cf_spos && p == HG::NPASS - 1) {
+        // conflict-free layout of the last stores and the epilogue reads
+        // (plan->d_head_spos / d_head_ppos, sfft_plan.cu): other positions
+        // than this pass read, so every thread must have read its inputs first
+        HEAD_SYNC();
 #pragma unroll
-      for (int x = 0; x < E; ++x) sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))] = v[x];  // in place: same positions
+        for (int x = 0; x < E; ++x) sb[__ldg(cf_spos + x * TPB + tt)] = v[x];
+      } else {
+#pragma unroll
+        for (int x = 0; x < E; ++x) sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))] = v[x];  // in place: same positions
+      }
       HEAD_SYNC();
     }
     if (!waited) {
@@ -1152,8 +1162,13 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
     const int c = (int)(u % NC);
     const int b = c | (LP == 1 ? (bl << 3) : (((bl & 1) << 3) | ((bl >> 1) << 2)));
     Cx<T>* dst = scratch + ((int64_t)rr << S) + ((int64_t)b << SQ) + tt;
+    if (cf_ppos) {
 #pragma unroll
-    for (int n = 0; n < E; ++n) dst[n * TPB] = sb[swz<T, SQ>(__ldg(perm + tt + n * TPB))];
+      for (int n = 0; n < E; ++n) dst[n * TPB] = sb[__ldg(cf_ppos + tt + n * TPB)];
+    } else {
+#pragma unroll
+      for (int n = 0; n < E; ++n) dst[n * TPB] = sb[swz<T, SQ>(__ldg(perm + tt + n * TPB))];
+    }
   }
 }
 
@@ -1547,7 +1562,8 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
     else
       e = launch_k(head, (unsigned)std::min<int64_t>(units, sms * occ1), HG::NTT, HG::SMEM, st,
                    pdl && (r0 > 0 || pdl_first), tm, ht, ftw, tw, (const int32_t*)p->d_tri_perm, (Cx<T>*)scr, r0,
-                   units);
+                   units, (const int32_t*)(P == 2 ? p->d_head_spos : nullptr),
+                   (const int32_t*)(P == 2 ? p->d_head_ppos : nullptr));
     const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / FG::NQB));
     if (e == cudaSuccess)
       e = launch_k(fin, (unsigned)(nper * FG::NQB), FG::NT, FG::SMEM, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
