@@ -1122,7 +1122,7 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     k_blocked_check<<<grid_1d(A), 256, 0, st>>>(p->d_tri_inv_elem, A, A >> 4, fl);
     k_blocked_check<<<grid_1d(A), 256, 0, st>>>(p->d_tri_inv_node, A, A >> 4, fl + 1);
   }
-  if (p->d_tri_perm && cudaMemcpyAsync(p->tri_front_tw, p->d_twiddles, csz * std::min<int64_t>(15, A - 1),
+  if (p->d_tri_perm && cudaMemcpyAsync(p->tri_front_tw, p->d_twiddles, csz * std::min<int64_t>(31, A - 1),
                                        cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return done(cuda_fail(cudaGetLastError(), "plan build"));
   if (cudaGetLastError() != cudaSuccess ||

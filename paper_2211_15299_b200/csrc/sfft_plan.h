@@ -38,7 +38,7 @@ struct sfft_plan {
   void* d_tri_tw;            // 15 x 2^(s-4) twiddles of the last 4 stages, [j][pi]
   int32_t* d_tri_inv_elem;   // 16 x 2^(s-4)  [b][pi] = d_inv_elem[(b << (s-4)) | perm[pi]]
   int32_t* d_tri_inv_node;   // 16 x 2^(s-4)  same for d_inv_node
-  unsigned char tri_front_tw[16 * 15];  // host copy of twiddles 0..14 (stages 1..4), plan dtype
+  unsigned char tri_front_tw[16 * 31];  // host copy of twiddles 0..30 (stages 1..5), plan dtype
   // complex64 middle pass: shared-memory positions of its last stores and of
   // the permuted epilogue reads, chosen so both are bank-conflict free
   int32_t* d_tri_spos;       // 2^(s-4)  [x][tid] -> position of the value thread tid stores from register x

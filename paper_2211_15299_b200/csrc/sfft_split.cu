@@ -957,6 +957,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(a) : "memory");
 }
+// SFFT_TIMELINE=1 (host env): per launch of the head path's kernels, the
+// first CTA start, the first CTA past griddepcontrol.wait and the last CTA
+// end (globaltimer, ns) are recorded and printed at exit (stderr) -- a
+// device-side timeline of the pipeline (probe only; tl == nullptr otherwise)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int what) {
+  if (tl && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    if (what == 2) atomicMax(tl + 2, t);
+    else atomicMin(tl + what, t);
+  }
+}
+
 // barrier among the NT transform threads only (the copy warp runs its own loop)
 template <int NT>
 __device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
@@ -988,12 +1005,14 @@ template <typename T, int S, int P>
 __global__ void __launch_bounds__(HeadGeo<T, S, P>::NTT, 1)
 k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 ftw, const Cx<T>* __restrict__ tw,
        const int32_t* __restrict__ perm, Cx<T>* __restrict__ scratch, int64_t row0, int64_t units,
-       const int32_t* __restrict__ cf_spos, const int32_t* __restrict__ cf_ppos) {
+       const int32_t* __restrict__ cf_spos, const int32_t* __restrict__ cf_ppos, unsigned long long* tl) {
+  tl_mark(tl, 0);
   using HG = HeadGeo<T, S, P>;
   constexpr int SQ = HG::SQ, NQ = HG::NQ, E = HG::E, LE = HG::LE, TPB = HG::TPB, NT = HG::NT, NC = HG::NC;
   constexpr int LP = P == 4 ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int NL = HG::NL, NTG = NT / P;
+  constexpr int NL = HG::NL;
+  [[maybe_unused]] constexpr int NTG = NT / P;
   Cx<T>* land = reinterpret_cast<Cx<T>*>(smem_raw);  // NL x P x NQ, TMA box order
   Cx<T>* work = land + NL * P * NQ;                  // P x NQ, swizzled slots per b value
   Cx<T>* stw = work + P * NQ;                        // twiddles of stages 5 .. SQ
@@ -1156,6 +1175,7 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
     if (!waited) {
       pdl_wait();  // scratch is free (the previous chunk's final pass completed)
       pdl_release();
+      tl_mark(tl, 1);
       waited = true;
     }
     const int64_t rr = u / NC;
@@ -1170,6 +1190,7 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
       for (int n = 0; n < E; ++n) dst[n * TPB] = sb[swz<T, SQ>(__ldg(perm + tt + n * TPB))];
     }
   }
+  tl_mark(tl, 2);
 }
 
 // In-place variant (SFFT_HEAD_IP=1): the landing buffer is also the working
@@ -1327,7 +1348,8 @@ template <typename T, int S>
 __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T>* __restrict__ scr2, int64_t row0,
                                                  int64_t nrows, int nper, const Cx<T>* __restrict__ twf,
                                                  const int32_t* __restrict__ invf, const int32_t* __restrict__ perm,
-                                                 int blocked) {
+                                                 int blocked, unsigned long long* tl) {
+  tl_mark(tl, 0);
   using FG = Fin2Geo<T, S>;
   constexpr int NQ = FG::NQ, SQ = FG::SQ, EXL = FG::EXL, L = FG::L, NT = FG::NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1361,6 +1383,7 @@ __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T
   }
   pdl_wait();  // scratch written by this chunk's head pass
   pdl_release();
+  tl_mark(tl, 1);
   fetch(first);
   const T scale = (T)args.scale1;
   const int pib = qb * NT + wid * 32;  // this warp's first pi
@@ -1397,6 +1420,7 @@ __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T
       for (int b = 0; b < EXL; ++b) o2[(b << SQ) | q] = v[b];
     }
   }
+  tl_mark(tl, 2);
 }
 
 // host: the tensor-map decomposition of a plan's pattern (false: not eligible)
@@ -1485,6 +1509,38 @@ static int head_launches(int64_t rows, int64_t* n) {
   return SFFT_OK;
 }
 
+// SFFT_TIMELINE: launch records (start, past wait, end) printed at exit
+struct Timeline {
+  unsigned long long* d = nullptr;
+  std::vector<std::string> names;
+  static constexpr int kSlots = 4096;
+  ~Timeline() {
+    if (!d || names.empty()) return;
+    std::vector<unsigned long long> h(3 * (size_t)kSlots);
+    if (cudaMemcpy(h.data(), d, 8 * h.size(), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    const unsigned long long t0 = h[0];
+    for (size_t i = 0; i < names.size() && i < (size_t)kSlots; ++i)
+      fprintf(stderr, "[sfft timeline] %4zu %-6s start %10.2f us  past-wait %10.2f us  end %10.2f us\n", i,
+              names[i].c_str(), (h[3 * i] - t0) * 1e-3, (h[3 * i + 1] - t0) * 1e-3, (h[3 * i + 2] - t0) * 1e-3);
+  }
+};
+static Timeline g_tl;
+static std::mutex g_tl_mu;
+static unsigned long long* timeline_slot(const char* name) {
+  static const bool on = getenv("SFFT_TIMELINE") != nullptr;
+  if (!on) return nullptr;
+  std::lock_guard<std::mutex> lk(g_tl_mu);
+  if (!g_tl.d) {
+    if (cudaMalloc(&g_tl.d, 8 * 3 * (size_t)Timeline::kSlots) != cudaSuccess) return nullptr;
+    std::vector<unsigned long long> init(3 * (size_t)Timeline::kSlots);
+    for (size_t i = 0; i < init.size(); ++i) init[i] = (i % 3 == 2) ? 0ull : ~0ull;
+    cudaMemcpy(g_tl.d, init.data(), 8 * init.size(), cudaMemcpyHostToDevice);
+  }
+  if (g_tl.names.size() >= (size_t)Timeline::kSlots) return nullptr;
+  g_tl.names.push_back(name);
+  return g_tl.d + 3 * (g_tl.names.size() - 1);
+}
+
 // 1: launched; 0: not eligible (caller falls back); <0 never; >1 error code
 template <typename T, int S, int P>
 static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st, bool* ran) {
@@ -1563,11 +1619,11 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
       e = launch_k(head, (unsigned)std::min<int64_t>(units, sms * occ1), HG::NTT, HG::SMEM, st,
                    pdl && (r0 > 0 || pdl_first), tm, ht, ftw, tw, (const int32_t*)p->d_tri_perm, (Cx<T>*)scr, r0,
                    units, (const int32_t*)(P == 2 ? p->d_head_spos : nullptr),
-                   (const int32_t*)(P == 2 ? p->d_head_ppos : nullptr));
+                   (const int32_t*)(P == 2 ? p->d_head_ppos : nullptr), timeline_slot("head"));
     const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / FG::NQB));
     if (e == cudaSuccess)
       e = launch_k(fin, (unsigned)(nper * FG::NQB), FG::NT, FG::SMEM, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
-                   invf, (const int32_t*)p->d_tri_perm, blocked);
+                   invf, (const int32_t*)p->d_tri_perm, blocked, timeline_slot("fin"));
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (pooled) cudaFreeAsync(scr, st);
