@@ -180,6 +180,11 @@ inline int kernel_occupancy(K kernel, int nt, size_t smem, int* occ) {
       return SFFT_OK;
     }
   }
+  int smem_max = 0;
+  SFFT_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (smem > (size_t)smem_max)
+    return fail(SFFT_ERR_UNSUPPORTED, "kernel needs " + std::to_string(smem) + " B of shared memory, the device " +
+                                          "allows " + std::to_string(smem_max));
   SFFT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int o = 0;
   SFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, nt, smem));

@@ -1572,15 +1572,19 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
   auto fin = k_fin2<T, S>;
   using FG = Fin2Geo<T, S>;
   int occ1 = 0, occ3 = 0, rc;
-  if ((rc = kernel_occupancy(head, HG::NTT, HG::SMEM, &occ1))) return rc;
+  // a variant that does not fit on an SM (e.g. SFFT_HEAD_P=4: 288 KB of
+  // shared memory) leaves the call to the three-pass split
+  auto soft = [](int r) { return r == SFFT_ERR_UNSUPPORTED ? -1 : r; };
+  if ((rc = soft(kernel_occupancy(head, HG::NTT, HG::SMEM, &occ1)))) return rc < 0 ? SFFT_OK : rc;
   static const bool ip = [] {
     const char* e = getenv("SFFT_HEAD_IP");
     return e && atoi(e) == 1;
   }();
   auto head_ip = k_head_ip<T, S, P>;
   int occ_ip = 0;
-  if (ip && (rc = kernel_occupancy(head_ip, HG::NT, HeadIpGeo<T, S, P>::SMEM, &occ_ip))) return rc;
-  if ((rc = kernel_occupancy(fin, FG::NT, FG::SMEM, &occ3))) return rc;
+  if (ip && (rc = soft(kernel_occupancy(head_ip, HG::NT, HeadIpGeo<T, S, P>::SMEM, &occ_ip))))
+    return rc < 0 ? SFFT_OK : rc;
+  if ((rc = soft(kernel_occupancy(fin, FG::NT, FG::SMEM, &occ3)))) return rc < 0 ? SFFT_OK : rc;
   const int blocked = inv1 == p->d_inv_elem ? p->tri_blocked_elem : inv1 == p->d_inv_node ? p->tri_blocked_node : 0;
   *ran = true;
   const int64_t rows = a.B;
@@ -1648,7 +1652,7 @@ bool split_two_pass() { return !use_tri(); }
 // the three-pass middle pass's conflict-free tables then)
 bool head_covers(const sfft_plan* p) {
   HeadTma ht;
-  return use_tri() && head_mode() && p->dtype == SFFT_C64 && p->s == 16 && head_plan(p, head_mode(), &ht);
+  return use_tri() && head_mode() == 2 && p->dtype == SFFT_C64 && p->s == 16 && head_plan(p, 2, &ht);
 }
 
 static int try_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaStream_t st, bool* ran) {
@@ -1704,7 +1708,7 @@ int run_large(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, cudaSt
 int large_launch_count(const sfft_plan* p, int64_t rows, int64_t* launches) {
   if (use_tri()) {
     HeadTma ht;
-    if (head_mode() && p->dtype == SFFT_C64 && p->s == 16 && p->d_tri_perm && head_plan(p, head_mode(), &ht))
+    if (head_mode() == 2 && p->dtype == SFFT_C64 && p->s == 16 && p->d_tri_perm && head_plan(p, 2, &ht))
       return head_launches<float, 16, 2>(rows, launches);
     if (p->dtype == SFFT_C64) {
       switch (p->s) {
