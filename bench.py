@@ -147,7 +147,42 @@ def config_dict(cfg: int, B_total: int, B_rank: int, world: int, scaling: str) -
             "global_batch": B_total, "N": 1 << spec["M"], "k": k, "parallelism": f"batch shard x{world}"}
 
 
-def measure_config(args, cfg: int, S, W, torch, dev, rank: int, world: int, dist, steps: int, headline: bool):
+def plan_times_all(S, W, torch, dev, configs) -> dict:
+    """Plan build of a fresh SupportSet per config, synchronised, twice (the
+    first includes loading the plan kernels), before any signal memory is
+    allocated.  The reference rebuilds its plan on every call (hidft.py:154);
+    per-signal supports (config 4) derive theirs on chip inside each call, so
+    their figure is a one-row call."""
+    from paper_2211_15299_b200.hidft import get_plan
+    out = {}
+    for cfg in configs:
+        spec = W.CONFIGS[cfg]
+        cdt = torch.complex64 if spec["dtype"] == "complex64" else torch.complex128
+        t = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if cfg == 4:
+                sup = torch.from_numpy(W.config_supports_batch(4, 1)).to(dev)
+                row = torch.zeros((1, 1 << spec["M"]), dtype=cdt, device=dev)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                S.hidft_to_dft_batched(row, sup, check=False)
+            else:
+                sup, M = W.config_support(cfg)
+                J = S.SupportSet(1 << M, sup)  # host validation of the indices is not timed
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                get_plan(J, S.pivots(J), 0, 0 if cdt == torch.complex64 else 1, dev)
+            torch.cuda.synchronize()
+            t.append((time.perf_counter() - t0) * 1e3)
+        out[cfg] = {"cold_ms": round(t[0], 3), "warm_ms": round(t[1], 3)}
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_config(args, cfg: int, S, W, torch, dev, rank: int, world: int, dist, steps: int, headline: bool,
+                   plan_times: dict):
     """Device-timed steps of one config on this rank; returns (result dict,
     state for the e2e / peer legs).  The caller holds the barrier discipline."""
     spec = W.CONFIGS[cfg]
@@ -183,6 +218,12 @@ def measure_config(args, cfg: int, S, W, torch, dev, rank: int, world: int, dist
             per_sig_sector.append(gb)
             ub_sum += ub
             lines += line_bytes(pat, esz)
+    if wl.support.ndim == 1:
+        J = S.SupportSet(N, wl.support)
+    else:
+        J = torch.from_numpy(wl.support).to(dev)
+    plan_ms = plan_times.get(cfg, {}).get("cold_ms")
+
     footprint = sum(per_sig_sector)
     R = max(2, math.ceil(4 * L2 / max(footprint, 1)))
     R = min(R, args.max_sets)
@@ -195,23 +236,6 @@ def measure_config(args, cfg: int, S, W, torch, dev, rank: int, world: int, dist
         st_.copy_(sets[0])
     out = torch.empty((B, wl.k), dtype=cdt, device=dev)
     status = torch.zeros(wl.support.shape[0] if wl.support.ndim == 2 else 1, dtype=torch.int32, device=dev)
-
-    # cold plan: a fresh SupportSet pays the whole device plan build (pivots,
-    # pattern, tables, twiddles, synchronised) before its first transform (the
-    # reference rebuilds its plan on every call, hidft.py:154); per-signal
-    # supports (config 4) derive their plans on chip inside every call, so
-    # their figure is the first one-row call
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if wl.support.ndim == 1:
-        from paper_2211_15299_b200.hidft import get_plan
-        J = S.SupportSet(N, wl.support)
-        get_plan(J, S.pivots(J), 0, 0 if cdt == torch.complex64 else 1, dev)
-    else:
-        J = torch.from_numpy(wl.support).to(dev)
-        S.hidft_to_dft_batched(sets[0][:1], J[:1], check=False)
-    torch.cuda.synchronize()
-    plan_ms = (time.perf_counter() - t0) * 1e3
 
     # kernels one step launches (the split transforms launch 2-3 per row chunk)
     launches_per_step = 1
@@ -366,7 +390,7 @@ def measure_config(args, cfg: int, S, W, torch, dev, rank: int, world: int, dist
             roof["sector_efficiency_ncu"] = tr["sector_efficiency_ncu"]
     res = {"config": config_dict(cfg, B_total, B, world, args.scaling), "value": value, "ms_per_step": ms_per_step,
            "steps": steps, "gpu_launches": steps * launches_per_step, "roofline": roof, "clocks": clocks,
-           "plan_ms": round(plan_ms, 3),
+           "plan_ms": plan_ms, "plan_warm_ms": plan_times.get(cfg, {}).get("warm_ms"),
            "parity": {"rel_l2_vs_planted_max": err, "tol": tol, "status_max": worst, "rows": B},
            "method": {"launch": "eager calls in a stream_chain scope" if args.no_graph else (
                           f"CUDA graphs of {GS} consecutive step calls (rotating over the input sets), "
@@ -500,7 +524,10 @@ def run_b200(args) -> None:
         else:  # host-side collectives only (CPU tests of the multi-rank path)
             dist.init_process_group("gloo")
 
-    head, st = measure_config(args, args.config, S, W, torch, dev, rank, world, dist, args.steps, True)
+    configs = [args.config] + ([c for c in (1, 2, 3, 4, 5, 6) if c != args.config]
+                               if world == 1 and not args.no_per_config else [])
+    plan_times = plan_times_all(S, W, torch, dev, configs)
+    head, st = measure_config(args, args.config, S, W, torch, dev, rank, world, dist, args.steps, True, plan_times)
 
     # N > 1, timed: one step with the result rows written straight into
     # rank 0's device buffer over peer memory (dist.PeerRows),
@@ -536,7 +563,7 @@ def run_b200(args) -> None:
         for c in [c for c in (1, 2, 3, 4, 5, 6) if c != args.config]:
             steps_c = max(20, min(args.steps, args.per_config_steps))
             try:
-                r, stc = measure_config(args, c, S, W, torch, dev, rank, world, dist, steps_c, False)
+                r, stc = measure_config(args, c, S, W, torch, dev, rank, world, dist, steps_c, False, plan_times)
                 del stc
                 if not args.no_cpu:
                     r["reference_single_call"] = reference_single_call(c)
@@ -562,7 +589,7 @@ def run_b200(args) -> None:
             "gpu_launches": head["gpu_launches"],
             "roofline": head["roofline"],
             "clocks": head["clocks"],
-            "plan_ms": head["plan_ms"],
+            "plan_ms": head["plan_ms"], "plan_warm_ms": head["plan_warm_ms"],
             "parity": head["parity"],
         }
         if e2e:
