@@ -155,6 +155,9 @@ extern "C" int sfft_hidft_interleaved(const sfft_plan* plan, const void* signals
   if (!signals || !out) return fail(SFFT_ERR_INVALID, "null signal or output pointer");
   if (ld < B) return fail(SFFT_ERR_INVALID, "sample stride ld must be >= B");
   if (plan->s < 1) return fail(SFFT_ERR_UNSUPPORTED, "interleaved layout needs s >= 1");
+  int dev = 0;
+  SFFT_CUDA(cudaGetDevice(&dev));
+  if (dev != plan->device) return fail(SFFT_ERR_INVALID, "plan belongs to another device");
   const int32_t *map = nullptr, *inv = nullptr;
   int64_t n_out = 0;
   double scale = 1.0;

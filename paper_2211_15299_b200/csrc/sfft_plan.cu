@@ -1259,10 +1259,10 @@ extern "C" int sfft_tree_build(const int64_t* J, int64_t k, int M, int level_lo,
     }
   }
   SFFT_CUDA(cudaGetLastError());
-  if (!dev_out) {
-    SFFT_CUDA(cudaMemcpyAsync(members, m_out, 8 * k * (size_t)nl, cudaMemcpyDeviceToHost, st));
-    SFFT_CUDA(cudaMemcpyAsync(node_off, o_out, 4 * (k + 1) * (size_t)nl, cudaMemcpyDeviceToHost, st));
-    SFFT_CUDA(cudaMemcpyAsync(n_nodes, n_out, 4 * (size_t)nl, cudaMemcpyDeviceToHost, st));
+  if (!dev_out) {  // host (or mixed host / device) outputs: copied back, synchronous
+    SFFT_CUDA(cudaMemcpyAsync(members, m_out, 8 * k * (size_t)nl, cudaMemcpyDefault, st));
+    SFFT_CUDA(cudaMemcpyAsync(node_off, o_out, 4 * (k + 1) * (size_t)nl, cudaMemcpyDefault, st));
+    SFFT_CUDA(cudaMemcpyAsync(n_nodes, n_out, 4 * (size_t)nl, cudaMemcpyDefault, st));
     SFFT_CUDA(cudaStreamSynchronize(st));
   }
   return SFFT_OK;

@@ -25,6 +25,7 @@ Results are CUDA tensors for CUDA sources and host arrays otherwise.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass, field
 from typing import Any, Sequence
@@ -63,8 +64,9 @@ class ButterflyPlan:
         self.handle = ctypes.c_void_p(0)
         rr = np.asarray(r if r else [0], dtype=np.int32)
         dj = J.device_tensor(device)
-        _lib.check(lib.sfft_plan_create(dj.data_ptr(), len(J), J.M, rr.ctypes.data, len(r), int(height),
-                                        dtype_code, _lib.stream_ptr(device), ctypes.byref(self.handle)))
+        with _torch().cuda.device(device):  # the plan belongs to the current device
+            _lib.check(lib.sfft_plan_create(dj.data_ptr(), len(J), J.M, rr.ctypes.data, len(r), int(height),
+                                            dtype_code, _lib.stream_ptr(device), ctypes.byref(self.handle)))
         info = _lib.PlanInfo()
         _lib.check(lib.sfft_plan_get_info(self.handle, ctypes.byref(info)))
         self.r = tuple(r)
@@ -291,11 +293,25 @@ def _finish(x, src: _Src):
     return x.cpu().numpy()
 
 
+def _device_guard(x):
+    """Make a CUDA tensor argument's device current for the library calls
+    (kernels launch on the current device's stream; plans belong to it)."""
+    torch = _torch()
+    if torch.is_tensor(x) and x.is_cuda:
+        return torch.cuda.device(x.device)
+    return contextlib.nullcontext()
+
+
 def hidft(source, J, r: Sequence[int], height: int = 0, shift: int = 0, counter=None) -> HiDftResult:
     """Generalised radix-2 transform of tau^shift f (hidft.py:135-185).
 
     Output equals F(node representatives, I_{r^{n-}}) applied to the shifted
     samples, unscaled; exactly 1.5*A*log2(A) complex operations are counted."""
+    with _device_guard(source):
+        return _hidft(source, J, r, height, shift, counter)
+
+
+def _hidft(source, J, r, height, shift, counter) -> HiDftResult:
     torch = _torch()
     J = as_support(J)
     rt = validate_pivot_vector(r, J.M)
@@ -392,6 +408,11 @@ def hidft_to_dft_batched(signals, J, out=None, status=None, check: bool = True):
     sorted support per row (config 4).  Per-row statuses land in `status`
     (int32 device tensor) when given; with check=True a non-homogeneous or
     invalid support raises like the reference would."""
+    with _device_guard(signals):
+        return _hidft_to_dft_batched(signals, J, out, status, check)
+
+
+def _hidft_to_dft_batched(signals, J, out, status, check):
     torch = _torch()
     dev = _lib.require_device()
     if not torch.is_tensor(signals):  # numpy rows stay on the host: only the needed samples move
@@ -479,6 +500,11 @@ def hidft_to_dft_interleaved(signals, J, out=None, shift: int = 0):
     samples at (I - shift) mod N (core.py:3-6).  The gather reads each
     needed sample index of SG neighbouring signals as one contiguous run
     (sfft_hidft_interleaved) instead of one 128 B line per sample."""
+    with _device_guard(signals):
+        return _hidft_to_dft_interleaved(signals, J, out, shift)
+
+
+def _hidft_to_dft_interleaved(signals, J, out, shift):
     torch = _torch()
     _lib.require_device()
     if not torch.is_tensor(signals) or not signals.is_cuda or signals.dim() != 2:

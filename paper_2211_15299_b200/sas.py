@@ -249,6 +249,12 @@ def sas_transform(source, J, r: Sequence[int] | None = None, policy: str = "auto
                   family_meta: dict | None = None, counter=None, tolerance: float = 1e-8) -> SasResult:
     """Recover (F f)_J from mu* shifted Hi-DFTs plus per-node Vandermonde
     decodes (sas.py:313-409), all on the device."""
+    from .hidft import _device_guard
+    with _device_guard(source):
+        return _sas_transform(source, J, r, policy, family_meta, counter, tolerance)
+
+
+def _sas_transform(source, J, r, policy, family_meta, counter, tolerance) -> SasResult:
     import ctypes
     torch = _torch()
     from .counting import OpCounter
