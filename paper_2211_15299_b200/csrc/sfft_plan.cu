@@ -742,12 +742,13 @@ template <typename T>
 __global__ void k_tri_tables(const Cx<T>* __restrict__ tw, const int32_t* __restrict__ inv_elem,
                              const int32_t* __restrict__ inv_node, const int32_t* __restrict__ perm, int s,
                              Cx<T>* __restrict__ tw_fin, int32_t* __restrict__ inv_elem_fin,
-                             int32_t* __restrict__ inv_node_fin) {
+                             int32_t* __restrict__ inv_node_fin, int32_t* __restrict__ pinv) {
   const int sq = s - 4;
   const int64_t nq = 1ll << sq;
   const int64_t pi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (pi >= nq) return;
   const int64_t q = perm[pi];
+  pinv[q] = (int32_t)pi;
   for (int b = 0; b < 16; ++b) {
     inv_elem_fin[b * nq + pi] = inv_elem[((int64_t)b << sq) | q];
     inv_node_fin[b * nq + pi] = inv_node[((int64_t)b << sq) | q];
@@ -938,6 +939,7 @@ static void plan_free(sfft_plan* p) {
   cudaFree(p->d_inv_elem_blk);
   cudaFree(p->d_inv_node_blk);
   cudaFree(p->d_tri_perm);
+  cudaFree(p->d_tri_pinv);
   cudaFree(p->d_tri_tw);
   cudaFree(p->d_tri_inv_elem);
   cudaFree(p->d_tri_inv_node);
@@ -1091,6 +1093,7 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     // three-pass tables (k_tri_*)
     const int64_t nq = A >> 4;
     M_((void**)&p->d_tri_perm, 4 * nq);
+    M_((void**)&p->d_tri_pinv, 4 * nq);
     M_(&p->d_tri_tw, csz * 15 * nq);
     M_((void**)&p->d_tri_inv_elem, 4 * A);
     M_((void**)&p->d_tri_inv_node, 4 * A);
@@ -1108,12 +1111,12 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
     if (dtype == SFFT_C64)
       k_tri_tables<float><<<grid_1d(nq), 256, 0, st>>>((const Cx<float>*)p->d_twiddles, p->d_inv_elem,
                                                         p->d_inv_node, p->d_tri_perm, s, (Cx<float>*)p->d_tri_tw,
-                                                        p->d_tri_inv_elem, p->d_tri_inv_node);
+                                                        p->d_tri_inv_elem, p->d_tri_inv_node, p->d_tri_pinv);
     else
       k_tri_tables<double><<<grid_1d(nq), 256, 0, st>>>((const Cx<double>*)p->d_twiddles, p->d_inv_elem,
                                                          p->d_inv_node, p->d_tri_perm, s,
                                                          (Cx<double>*)p->d_tri_tw, p->d_tri_inv_elem,
-                                                         p->d_tri_inv_node);
+                                                         p->d_tri_inv_node, p->d_tri_pinv);
   }
   trace.mark("split / three-pass tables");
   unsigned long long h[4] = {0, 0, 0, 0};

@@ -35,6 +35,7 @@ struct sfft_plan {
   // three-pass split (sfft_split.cu, k_tri_*): slot = (b << (s-4)) | q; the
   // final pass owns the q of one position pi = rank of q in d_tri_perm order
   int32_t* d_tri_perm;       // 2^(s-4)  pi -> q, sorted by mean output position
+  int32_t* d_tri_pinv;       // 2^(s-4)  q -> pi (the head pass's bulk epilogue stores position pi)
   void* d_tri_tw;            // 15 x 2^(s-4) twiddles of the last 4 stages, [j][pi]
   int32_t* d_tri_inv_elem;   // 16 x 2^(s-4)  [b][pi] = d_inv_elem[(b << (s-4)) | perm[pi]]
   int32_t* d_tri_inv_node;   // 16 x 2^(s-4)  same for d_inv_node

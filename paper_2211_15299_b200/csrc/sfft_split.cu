@@ -641,7 +641,14 @@ static int scratch_pool(int dev, cudaMemPool_t* pool) {
   props.location.type = cudaMemLocationTypeDevice;
   props.location.id = dev;
   cudaMemPool_t p;
-  SFFT_CUDA(cudaMemPoolCreate(&p, &props));
+  {
+    // legal while a stream captures once this thread's capture mode is relaxed
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    SFFT_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+    const cudaError_t e = cudaMemPoolCreate(&p, &props);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch pool creation");
+  }
   uint64_t keep = ~0ull;
   SFFT_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep));
   pools[dev] = p;
@@ -681,14 +688,16 @@ static int stream_scratch(int dev, cudaStream_t st, size_t bytes, void** ptr, bo
       if (e.stream != st) continue;
       listed = true;
       if (e.bytes < bytes) {
-        // grow outside a capture (a capture takes the pool path instead)
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        SFFT_CUDA(cudaStreamIsCapturing(st, &cs));
-        if (cs != cudaStreamCaptureStatusNone) break;
         // the old buffer is retired, not freed: a CUDA graph captured
-        // earlier on this stream may still reference it
+        // earlier on this stream may still reference it; the
+        // plain allocation is legal inside a capture with the thread's
+        // capture mode relaxed (as below)
         void* np = nullptr;
-        SFFT_CUDA(cudaMalloc(&np, bytes));
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        SFFT_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+        const cudaError_t ge = cudaMalloc(&np, bytes);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (ge != cudaSuccess) return cuda_fail(ge, "stream scratch allocation");
         g_ss_retired.push_back(e.ptr);
         e.ptr = np;
         e.bytes = bytes;
@@ -934,8 +943,8 @@ struct HeadGeo {
   static constexpr int NPASS = (SQ + LE - 1) / LE;
   static constexpr int NTW = NQ - 16;        // stage-major twiddles 15 .. NQ-2 (stages 5 .. SQ)
   // NL landing buffers (TMA) + working buffer (swizzled slots) + twiddles + 2 NL mbarriers
-#ifndef SFFT_HEAD_NL  // landing buffers (config 5, one box: 1 -> 126.5 us, 2 -> 126.1 us per step)
-#define SFFT_HEAD_NL 1
+#ifndef SFFT_HEAD_NL  // landing buffers (config 5 with the bulk epilogue and per-b-value groups: 1 -> 120.6 us, 2 -> 116.2 us per step)
+#define SFFT_HEAD_NL 2
 #endif
   static constexpr int NL = P == 2 ? SFFT_HEAD_NL : 1;
   static constexpr size_t SMEM = (NL + 1) * (size_t)P * NQ * sizeof(Cx<T>) + (size_t)NTW * sizeof(Cx<T>) + 16 * NL;
@@ -974,6 +983,14 @@ __device__ __forceinline__ void tl_mark(unsigned long long* tl, int what) {
   }
 }
 
+// -DSFFT_HEAD_CLK: per-phase cycle counts of CTA 0 (warps 0 and NT/32-1), printed
+// at kernel exit (probe only)
+#ifdef SFFT_HEAD_CLK
+#define HCLK(i) do { const long long t__ = clock64(); hacc[i] += t__ - hlast; hlast = t__; } while (0)
+#else
+#define HCLK(i) do { } while (0)
+#endif
+
 // barrier among the NT transform threads only (the copy warp runs its own loop)
 template <int NT>
 __device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
@@ -982,7 +999,7 @@ __device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, %0;" :: 
 // (config 5: per-group barriers 126.1-126.4 us against 126.5 us per step; the
 // pass is bound by the TMA row rate and the transform's latency, tools/tma_box_probe.cu)
 #ifndef SFFT_HEAD_GROUPS
-#define SFFT_HEAD_GROUPS 0
+#define SFFT_HEAD_GROUPS 1
 #endif
 #if SFFT_HEAD_GROUPS
 #define HEAD_SYNC() group_sync<NTG>(bl)
@@ -1005,7 +1022,8 @@ template <typename T, int S, int P>
 __global__ void __launch_bounds__(HeadGeo<T, S, P>::NTT, 1)
 k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 ftw, const Cx<T>* __restrict__ tw,
        const int32_t* __restrict__ perm, Cx<T>* __restrict__ scratch, int64_t row0, int64_t units,
-       const int32_t* __restrict__ cf_spos, const int32_t* __restrict__ cf_ppos, unsigned long long* tl) {
+       const int32_t* __restrict__ cf_spos, const int32_t* __restrict__ cf_ppos, int bulk,
+       unsigned long long* tl) {
   tl_mark(tl, 0);
   using HG = HeadGeo<T, S, P>;
   constexpr int SQ = HG::SQ, NQ = HG::NQ, E = HG::E, LE = HG::LE, TPB = HG::TPB, NT = HG::NT, NC = HG::NC;
@@ -1094,11 +1112,26 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
   work_sync<NT>();  // twiddles staged by all groups
   bool waited = false;
   uint32_t it = 0;
+  // the thread that issues (and waits for) the bulk epilogue copies: one per barrier group
+  const int issuer = SFFT_HEAD_GROUPS ? bl * 32 : 0;
+#if defined(SFFT_HEAD_LAG) && SFFT_HEAD_GROUPS
+  // probe: group 1 starts SFFT_HEAD_LAG cycles late, so the two groups' shared-memory
+  // and FMA phases interleave instead of running in lockstep
+  if (bl == 1) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < SFFT_HEAD_LAG) { }
+  }
+#endif
+#ifdef SFFT_HEAD_CLK
+  long long hacc[12] = {0}, hlast = clock64();
+#endif
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
     Cx<T> v[E];
     const int lb = it % NL;
     const Cx<T>* lbuf = land + lb * P * NQ;
+    HCLK(11);
     mbar_wait(full0 + 8 * lb, (it / NL) & 1);
+    HCLK(0);
 #pragma unroll
     for (int x = 0; x < E; ++x) {
       uint32_t q = base;
@@ -1107,7 +1140,10 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
         if ((x >> i) & 1) q += ht.qw[i];
       v[x] = lbuf[q * P + bl];
     }
+    // bulk epilogue: the previous unit's stores have read the working buffer
+    if (bulk && tid == issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     HEAD_SYNC();  // the group's landing reads and its previous epilogue reads of work done
+    HCLK(1);
     if ((tid & 31) == 0) mbar_arrive(empty0 + 8 * lb);
 #if defined(SFFT_HEAD_PROBE) && SFFT_HEAD_PROBE == 1  // timing probe: copies and scratch stores only
     if (!waited) {
@@ -1134,9 +1170,12 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
         bfly2(v[x], v[x | (1 << beta)], ftw.w[j], ftw.iw[j]);
       }
     }
+    HCLK(2);
 #pragma unroll
     for (int x = 0; x < E; ++x) sb[tb0 ^ swz<T, SQ>(x)] = v[x];
+    HCLK(3);
     HEAD_SYNC();
+    HCLK(4);
 #pragma unroll
     for (int p = 1; p < HG::NPASS; ++p) {
       const int tb = swz<T, SQ>(slot_t<SQ, LE>(p, tt));
@@ -1159,6 +1198,7 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
           }
         }
       }
+      HCLK(5);
       if (cf_spos && p == HG::NPASS - 1) {
         // conflict-free layout of the last stores and the epilogue reads
         // (plan->d_head_spos / d_head_ppos, sfft_plan.cu): other positions
@@ -1166,11 +1206,14 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
         HEAD_SYNC();
 #pragma unroll
         for (int x = 0; x < E; ++x) sb[__ldg(cf_spos + x * TPB + tt)] = v[x];
+        if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       } else {
 #pragma unroll
         for (int x = 0; x < E; ++x) sb[tb ^ swz<T, SQ>(slot_x<SQ, LE>(p, x))] = v[x];  // in place: same positions
       }
+      HCLK(6);
       HEAD_SYNC();
+      HCLK(7);
     }
     if (!waited) {
       pdl_wait();  // scratch is free (the previous chunk's final pass completed)
@@ -1178,18 +1221,43 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
       tl_mark(tl, 1);
       waited = true;
     }
+    HCLK(8);
     const int64_t rr = u / NC;
     const int c = (int)(u % NC);
     const int b = c | (LP == 1 ? (bl << 3) : (((bl & 1) << 3) | ((bl >> 1) << 2)));
     Cx<T>* dst = scratch + ((int64_t)rr << S) + ((int64_t)b << SQ) + tt;
-    if (cf_ppos) {
+    if (bulk) {
+      // the last pass stored position pi (cf_spos = the inverse of perm): each b
+      // value's block leaves as one bulk copy, read by the async proxy while
+      // the transform threads start the next unit
+      if (tid == issuer) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+          if (SFFT_HEAD_GROUPS && j != bl) continue;
+          const int bj = c | (LP == 1 ? (j << 3) : (((j & 1) << 3) | ((j >> 1) << 2)));
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(scratch + ((int64_t)rr << S) + ((int64_t)bj << SQ)), "r"(smem_addr(work + j * NQ)),
+                          "n"(NQ * (int)sizeof(Cx<T>)) : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else if (cf_ppos) {
 #pragma unroll
       for (int n = 0; n < E; ++n) dst[n * TPB] = sb[__ldg(cf_ppos + tt + n * TPB)];
     } else {
 #pragma unroll
       for (int n = 0; n < E; ++n) dst[n * TPB] = sb[swz<T, SQ>(__ldg(perm + tt + n * TPB))];
     }
+    HCLK(9);
   }
+  if (bulk && tid == issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifdef SFFT_HEAD_CLK
+  if (blockIdx.x == 0 && (tid == 0 || tid == NT - 32))
+    printf("[head clk] warp %d units %u: wait_full %lld land_rd+sync %lld p0math %lld p0sts %lld sync %lld "
+           "p12 lds+math %lld sts %lld sync %lld pdl %lld epi %lld loop %lld\n", tid >> 5, it, hacc[0] / it, hacc[1] / it,
+           hacc[2] / it, hacc[3] / it, hacc[4] / it, hacc[5] / it, hacc[6] / it, hacc[7] / it, hacc[8] / it, hacc[9] / it,
+           hacc[11] / it);
+#endif
   tl_mark(tl, 2);
 }
 
@@ -1582,6 +1650,12 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
     const char* e = getenv("SFFT_HEAD_IP");
     return e && atoi(e) == 1;
   }();
+  // SFFT_HEAD_BULK=0: the epilogue reads the working buffer through perm and
+  // stores from registers; default: bulk copies (cp.async.bulk shared -> global)
+  static const bool bulk = [] {
+    const char* e = getenv("SFFT_HEAD_BULK");
+    return !(e && atoi(e) == 0);
+  }();
   auto head_ip = k_head_ip<T, S, P>;
   int occ_ip = 0;
   if (ip && (rc = soft(kernel_occupancy(head_ip, HG::NT, HeadIpGeo<T, S, P>::SMEM, &occ_ip))))
@@ -1624,9 +1698,15 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
     else
       e = launch_k(head, (unsigned)std::min<int64_t>(units, sms * occ1), HG::NTT, HG::SMEM, st,
                    pdl && (r0 > 0 || pdl_first), tm, ht, ftw, tw, (const int32_t*)p->d_tri_perm, (Cx<T>*)scr, r0,
-                   units, (const int32_t*)(P == 2 ? p->d_head_spos : nullptr),
-                   (const int32_t*)(P == 2 ? p->d_head_ppos : nullptr), timeline_slot("head"));
-    const int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / FG::NQB));
+                   units, (const int32_t*)(bulk ? p->d_tri_pinv : P == 2 ? p->d_head_spos : nullptr),
+                   (const int32_t*)(bulk ? nullptr : P == 2 ? p->d_head_ppos : nullptr), (int)bulk,
+                   timeline_slot("head"));
+    int nper = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ3 / FG::NQB));
+    static const int nper_env = [] {
+      const char* e = getenv("SFFT_FIN_NPER");
+      return e ? atoi(e) : 0;
+    }();
+    if (nper_env > 0) nper = (int)std::min<int64_t>(n, nper_env);  // probe: more, shorter final-pass CTAs
     if (e == cudaSuccess)
       e = launch_k(fin, (unsigned)(nper * FG::NQB), FG::NT, FG::SMEM, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
                    invf, (const int32_t*)p->d_tri_perm, blocked, timeline_slot("fin"));
