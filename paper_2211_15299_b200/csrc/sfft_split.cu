@@ -951,6 +951,21 @@ struct HeadGeo {
   static_assert(sizeof(T) == 4 && SQ >= 2 * LE && E <= TPB, "head pass: complex64, at least 2 register passes");
 };
 
+// L2 eviction priorities for the scratch round trip (SFFT_L2_HINTS=0: none)
+#ifndef SFFT_L2_HINTS
+#define SFFT_L2_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // twiddles of stages 1..4 and their rotations i*w (uniform over the grid)
 struct FrontTw2 { Cx<float> w[15], iw[15]; };
 
@@ -1235,9 +1250,16 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
         for (int j = 0; j < P; ++j) {
           if (SFFT_HEAD_GROUPS && j != bl) continue;
           const int bj = c | (LP == 1 ? (j << 3) : (((j & 1) << 3) | ((j >> 1) << 2)));
+#if SFFT_L2_HINTS
+          // scratch is read once more, by this chunk's final pass: keep it in L2
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                       :: "l"(scratch + ((int64_t)rr << S) + ((int64_t)bj << SQ)), "r"(smem_addr(work + j * NQ)),
+                          "n"(NQ * (int)sizeof(Cx<T>)), "l"(l2_policy_evict_last()) : "memory");
+#else
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                        :: "l"(scratch + ((int64_t)rr << S) + ((int64_t)bj << SQ)), "r"(smem_addr(work + j * NQ)),
                           "n"(NQ * (int)sizeof(Cx<T>)) : "memory");
+#endif
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
@@ -1409,25 +1431,27 @@ k_head_ip(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontT
 template <typename T, int S>
 struct Fin2Geo {
   static constexpr int L = 4, EXL = 16, SQ = S - L, NQ = 1 << SQ, NT = 128, NW = NT / 32, NQB = NQ / NT;
-  static constexpr size_t SMEM = (size_t)NW * EXL * 32 * sizeof(Cx<T>);  // output staging
+  static constexpr size_t SMEM = 2 * (size_t)NW * EXL * 32 * sizeof(Cx<T>);  // output staging, two buffers per warp
 };
 
 template <typename T, int S>
 __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T>* __restrict__ scr2, int64_t row0,
                                                  int64_t nrows, int nper, const Cx<T>* __restrict__ twf,
                                                  const int32_t* __restrict__ invf, const int32_t* __restrict__ perm,
-                                                 int blocked, unsigned long long* tl) {
+                                                 int blocked, const __grid_constant__ CUtensorMap otm, int tmaout,
+                                                 unsigned long long* tl) {
   tl_mark(tl, 0);
   using FG = Fin2Geo<T, S>;
   constexpr int NQ = FG::NQ, SQ = FG::SQ, EXL = FG::EXL, L = FG::L, NT = FG::NT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Cx<T>* stg = reinterpret_cast<Cx<T>*>(smem_raw);  // [warp][T][lane] output staging
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Cx<T>* stg = reinterpret_cast<Cx<T>*>(smem_raw);  // [warp][buffer][T][lane] output staging
   const int qb = blockIdx.x % FG::NQB;
   const int64_t first = blockIdx.x / FG::NQB;
   if (first >= nrows) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int pi = qb * NT + threadIdx.x;
-  Cx<T>* st = stg + wid * EXL * 32;
+  Cx<T>* st = stg + wid * 2 * EXL * 32;
+  uint32_t sbuf = 0;
   Cx<T> nx[EXL];
   auto fetch = [&](int64_t rr) {
     const Cx<T>* src = scr2 + (rr << S) + pi;
@@ -1453,11 +1477,29 @@ __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T
   fetch(first);
   const T scale = (T)args.scale1;
   const int pib = qb * NT + wid * 32;  // this warp's first pi
+#ifdef SFFT_HEAD_CLK
+  long long hacc[12] = {0}, hlast = clock64();
+  int it = 0;
+#endif
   for (int64_t rr = first; rr < nrows; rr += nper) {
     Cx<T> v[EXL];
+#ifdef SFFT_HEAD_CLK
+    ++it;
+    {
+      float acc = 0.f;
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) acc += nx[b].x;
+      if (acc == 12345.678f) printf("x");
+    }
+    HCLK(0);
+#endif
 #pragma unroll
     for (int b = 0; b < EXL; ++b) v[b] = nx[b];
+#if defined(SFFT_FIN_PROBE) && SFFT_FIN_PROBE == 1  // timing probe: no scratch loads after the first row
+    if (false)
+#endif
     if (rr + nper < nrows) fetch(rr + nper);
+    HCLK(1);
 #pragma unroll
     for (int t = 0; t < L; ++t) {  // global stage SQ + t + 1 pairs slot bit SQ + t = b bit t
 #pragma unroll
@@ -1470,13 +1512,43 @@ __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T
     }
     const int64_t r = row0 + rr;
     Cx<T>* o1 = reinterpret_cast<Cx<T>*>(args.out1) + r * args.ld1;
-    if (blocked) {
+    HCLK(2);
+#if defined(SFFT_FIN_PROBE) && SFFT_FIN_PROBE == 2  // timing probe: no output stores
+    if (v[0].x == 12345.678f)
+#endif
+    if (blocked && tmaout) {
+      // the warp's 16 x 32 outputs leave as one tensor store (box: 32 pi x 16
+      // blocks T of row r), read by the async proxy while the warp works on
+      // the next row in the other staging buffer
+      Cx<T>* sw = st + sbuf * EXL * 32;
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer sbuf's previous store was read
+      __syncwarp();
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) sw[(int)((epk >> (4 * b)) & 15) * 32 + lane] = cscale(v[b], scale);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+#if SFFT_L2_HINTS
+        // outputs are not read again by this call: first out of L2
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
+                     :: "l"(&otm), "r"(pib), "r"(0), "r"((int)r), "r"(smem_addr(sw)), "l"(l2_policy_evict_first())
+                     : "memory");
+#else
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                     :: "l"(&otm), "r"(pib), "r"(0), "r"((int)r), "r"(smem_addr(sw)) : "memory");
+#endif
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      sbuf ^= 1;
+    } else if (blocked) {
 #pragma unroll
       for (int b = 0; b < EXL; ++b) st[(int)((epk >> (4 * b)) & 15) * 32 + lane] = cscale(v[b], scale);
       __syncwarp();
+      HCLK(3);
 #pragma unroll
       for (int t = 0; t < EXL; ++t) st_cs(o1 + ((int64_t)t << SQ) + pib + lane, st[t * 32 + lane]);
       __syncwarp();
+      HCLK(4);
     } else {
 #pragma unroll
       for (int b = 0; b < EXL; ++b) {
@@ -1490,6 +1562,12 @@ __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T
       for (int b = 0; b < EXL; ++b) o2[(b << SQ) | q] = v[b];
     }
   }
+  if (tmaout && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifdef SFFT_HEAD_CLK
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+    printf("[fin clk] warp %d iters %d: wait_nx %lld issue_fetch %lld math %lld stage %lld store %lld\n", wid, it,
+           hacc[0] / it, hacc[1] / it, hacc[2] / it, hacc[3] / it, hacc[4] / it);
+#endif
   tl_mark(tl, 2);
 }
 
@@ -1662,6 +1740,25 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
     return rc < 0 ? SFFT_OK : rc;
   if ((rc = soft(kernel_occupancy(fin, FG::NT, FG::SMEM, &occ3)))) return rc < 0 ? SFFT_OK : rc;
   const int blocked = inv1 == p->d_inv_elem ? p->tri_blocked_elem : inv1 == p->d_inv_node ? p->tri_blocked_node : 0;
+  // blocked output map: each final-pass warp writes its 32 pi x 16 blocks of a
+  // row with one tensor store (SFFT_FIN_TMA=0: staged per-thread stores)
+  static const bool fin_tma = [] {
+    const char* e = getenv("SFFT_FIN_TMA");
+    return !(e && atoi(e) == 0);
+  }();
+  CUtensorMap otm;
+  std::memset(&otm, 0, sizeof(otm));
+  int tmaout = 0;
+  if (blocked && fin_tma && !a.out2 && a.n1 == ((int64_t)1 << S) && !(reinterpret_cast<uintptr_t>(a.out1) & 15) &&
+      !((a.ld1 * (int64_t)sizeof(Cx<T>)) & 15)) {
+    const cuuint64_t od[3] = {(cuuint64_t)HG::NQ, 16, (cuuint64_t)a.B};
+    const cuuint64_t os[2] = {(cuuint64_t)sizeof(Cx<T>) << HG::SQ, (cuuint64_t)(a.ld1 * (int64_t)sizeof(Cx<T>))};
+    const cuuint32_t ob[3] = {32, 16, 1};
+    const cuuint32_t oe[3] = {1, 1, 1};
+    tmaout = enc(&otm, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, a.out1, od, os, ob, oe, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   *ran = true;
   const int64_t rows = a.B;
   if (rows == 0) return SFFT_OK;
@@ -1709,7 +1806,7 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
     if (nper_env > 0) nper = (int)std::min<int64_t>(n, nper_env);  // probe: more, shorter final-pass CTAs
     if (e == cudaSuccess)
       e = launch_k(fin, (unsigned)(nper * FG::NQB), FG::NT, FG::SMEM, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
-                   invf, (const int32_t*)p->d_tri_perm, blocked, timeline_slot("fin"));
+                   invf, (const int32_t*)p->d_tri_perm, blocked, otm, tmaout, timeline_slot("fin"));
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (pooled) cudaFreeAsync(scr, st);
