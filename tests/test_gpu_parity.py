@@ -693,10 +693,12 @@ import torch
 import structfft_oracle as O
 import paper_2211_15299_b200 as S
 ok = True
-for dt, s in [(np.complex64, 16), (np.complex64, 17), (np.complex128, 16), (np.complex128, 14)]:
-    rng = np.random.default_rng(3000 + s)
+for dt, s, top in [(np.complex64, 16, 0), (np.complex64, 17, 0), (np.complex128, 16, 0), (np.complex128, 14, 0),
+                   (np.complex64, 16, 4), (np.complex64, 16, 2)]:
+    rng = np.random.default_rng(3000 + s + top)
     M, B = 22, 3
-    piv = sorted(rng.choice(M, size=s, replace=False).tolist())
+    # top > 0: the `top` largest levels are pivots (head-pass eligible; top = 4: blocked output map)
+    piv = sorted(rng.choice(M - top, size=s - top, replace=False).tolist()) + list(range(M - top, M))
     J = O.gen_homogeneous(piv, M, int(rng.integers(0, 2 ** 62)))
     coef = rng.normal(size=(B, J.size)) + 1j * rng.normal(size=(B, J.size))
     f = np.stack([O.synthesize(J, coef[b], M) for b in range(B)]).astype(dt)
@@ -711,12 +713,16 @@ sys.exit(0 if ok else 1)
 """
 
 
-@pytest.mark.parametrize("env", [{"SFFT_SPLIT_PASSES": "2"}, {"SFFT_TRI_SCRATCH_MB": "1"}])
+@pytest.mark.parametrize("env", [{"SFFT_SPLIT_PASSES": "2"}, {"SFFT_TRI_SCRATCH_MB": "1"}, {"SFFT_HEAD_BULK": "0"},
+                                 {"SFFT_FIN_TMA": "0"}, {"SFFT_HEAD": "0"}])
 def test_alternate_split_configurations(S, env):
-    """The two-pass split (SFFT_SPLIT_PASSES=2, kept for A/B measurements)
-    and the three-pass split with many small row chunks (a 1 MiB scratch
-    budget: 1-4 rows per chunk, the PDL chain across chunks) against the
-    oracle.  Each runs in a fresh process: the settings are read once."""
+    """The two-pass split (SFFT_SPLIT_PASSES=2, kept for A/B measurements),
+    the three-pass split with many small row chunks (a 1 MiB scratch
+    budget: 1-4 rows per chunk, the PDL chain across chunks), the head pass
+    with its register epilogue (SFFT_HEAD_BULK=0) or the final pass with
+    per-thread stores (SFFT_FIN_TMA=0) and head-eligible patterns on the
+    three-pass split (SFFT_HEAD=0), against the oracle.  Each runs in a
+    fresh process: the settings are read once."""
     import os
     import subprocess
     import sys
@@ -993,3 +999,39 @@ def test_s13_single_cta_plan_kernel(S, torch, dt):
     ref = O.hidft(sig[1].cpu().numpy()[None, :], Jn, M, S.pivots(J), shift=123)
     vals = res.node_values.cpu().numpy() if hasattr(res.node_values, "cpu") else res.node_values
     assert rel_l2(np.asarray(vals).reshape(-1), np.asarray(ref.node_values).reshape(-1)) < (1e-5 if dt == "c64" else 1e-11)
+
+
+@pytest.mark.parametrize("top", [4, 0])
+def test_graph_capture_with_growing_scratch(S, torch, top):
+    """The large-transform paths inside CUDA graph captures: the first
+    capture on a stream sees a small batch, the second a larger one, so the
+    per-stream scratch grows while the stream captures (a plain allocation
+    with the capture mode relaxed; the outgrown buffer stays alive for the
+    first graph).  Both graphs replay, in either order, to the eager result
+    (top = 4: head pass with the tensor-store final pass; 0: three-pass split)."""
+    M, s = 21, 16
+    rng = np.random.default_rng(77 + top)
+    piv = sorted(rng.choice(M - top, size=s - top, replace=False).tolist()) + list(range(M - top, M))
+    Jn = O.gen_homogeneous(piv, M, 5)
+    J = S.SupportSet(1 << M, Jn)
+    sig = torch.randn(5, 1 << M, dtype=torch.complex64, device="cuda")
+    want = S.hidft_to_dft_batched(sig, J).clone()
+    torch.cuda.synchronize()
+    outs = [torch.zeros(1, Jn.size, dtype=torch.complex64, device="cuda"),
+            torch.zeros(5, Jn.size, dtype=torch.complex64, device="cuda")]
+    graphs = []
+    for o in outs:  # torch.cuda.graph captures on its own side stream: first use of that stream's scratch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            S.hidft_to_dft_batched(sig[: o.shape[0]], J, out=o, check=False)
+        graphs.append(g)
+    for order in ((0, 1), (1, 0), (0, 1)):
+        for o in outs:
+            o.zero_()
+        for i in order:
+            graphs[i].replay()
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], want[:1])
+        assert torch.equal(outs[1], want)
+    ref = O.hidft_to_dft(sig[4].cpu().numpy(), Jn, M)
+    assert rel_l2(want[4].cpu().numpy(), ref) < 1e-5
