@@ -472,9 +472,31 @@ def measure_interleaved(args, cfg: int, S, W, torch, dev, steps: int) -> dict:
                   f"samples per cycle vs 126 MB L2"}
 
 
+_FMA_LIVE: dict | None = None
+
+
 def fma_peaks() -> dict:
-    """Non-tensor FMA peaks: profiles/fma_peak.json (tools/fma_peak.cu on the
-    GPU box, committed) or the round-1 measurement."""
+    """Non-tensor FMA peaks measured in this run (sfft_probe_fma_peak: FMA
+    chains on every SM, CUDA events, once per process, outside every timed
+    region); profiles/fma_peak.json (tools/fma_peak.cu on the GPU box,
+    committed) when the probe is unavailable."""
+    global _FMA_LIVE
+    if _FMA_LIVE is None:
+        try:
+            import ctypes
+            from paper_2211_15299_b200 import _lib
+            lib = _lib.load()
+            out = {}
+            for name, code in (("fp32_tflops", 0), ("fp64_tflops", 1)):
+                v = ctypes.c_double(0.0)
+                _lib.check(lib.sfft_probe_fma_peak(code, ctypes.byref(v), _lib.stream_ptr()))
+                out[name] = round(float(v.value), 2)
+            out["source"] = "measured in this run (sfft_probe_fma_peak: FMA chains on every SM, CUDA events)"
+            _FMA_LIVE = out
+        except Exception:  # noqa: BLE001  (no device / older library: the committed measurement)
+            _FMA_LIVE = {}
+    if _FMA_LIVE:
+        return _FMA_LIVE
     try:
         with open(os.path.join(ROOT, "profiles", "fma_peak.json")) as fh:
             d = json.load(fh)

@@ -186,6 +186,13 @@ SFFT_API int sfft_plan_apply_map(const sfft_plan* plan, int out_kind, const void
                                  int64_t B, int64_t ld, void* out, int64_t ld_out,
                                  sfft_stream_t stream);
 
+/* Measurement aid (no reference counterpart): the device's non-tensor FMA
+ * throughput in the plan dtypes, from independent FMA chains on every SM
+ * timed with CUDA events on `stream` (about 1 ms).  The flop side of the
+ * roofline SURVEY.md 8(d) asks for; bench.py calls it in the run it reports.
+ * dtype: SFFT_C64 -> fp32 FMA, SFFT_C128 -> fp64 FMA; *tflops on the host. */
+SFFT_API int sfft_probe_fma_peak(int dtype, double* tflops, sfft_stream_t stream);
+
 /* BandlimitedSignal.sample_block (core.py:164-173) on the device:
  * out[i] = (1/N) sum_e coeffs[e] exp(+2 pi i (locations[i] * J[e] mod N) / N),
  * complex128, J / coeffs / locations / out device pointers. */

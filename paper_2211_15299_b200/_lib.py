@@ -70,6 +70,7 @@ SIGNATURES = [
     ("sfft_hidft_staged", _c.c_int, [_P, _P, _I64, _I64, _c.c_int, _c.c_int, _P, _I64, _P, _I64, _P]),
     ("sfft_hidft_to_dft_fused", _c.c_int, [_P, _I64, _I64, _c.c_int, _P, _I64, _I64, _c.c_int, _P,
                                            _I64, _P, _P]),
+    ("sfft_probe_fma_peak", _c.c_int, [_c.c_int, _c.POINTER(_c.c_double), _P]),
     ("sfft_peer_alloc", _c.c_int, [_I64, _c.POINTER(_P), _P]),
     ("sfft_peer_free", _c.c_int, [_P]),
     ("sfft_peer_open", _c.c_int, [_P, _c.POINTER(_P)]),

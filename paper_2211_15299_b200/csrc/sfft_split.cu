@@ -1434,8 +1434,14 @@ struct Fin2Geo {
   static constexpr size_t SMEM = 2 * (size_t)NW * EXL * 32 * sizeof(Cx<T>);  // output staging, two buffers per warp
 };
 
+#ifndef SFFT_FIN2_MINB  // resident final-pass CTAs per SM the register budget is set for
+#define SFFT_FIN2_MINB 4
+#endif
+#ifndef SFFT_FIN2_NOPF
+#define SFFT_FIN2_NOPF 0
+#endif
 template <typename T, int S>
-__global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T>* __restrict__ scr2, int64_t row0,
+__global__ void __launch_bounds__(128, SFFT_FIN2_MINB) k_fin2(const PlanArgs args, const Cx<T>* __restrict__ scr2, int64_t row0,
                                                  int64_t nrows, int nper, const Cx<T>* __restrict__ twf,
                                                  const int32_t* __restrict__ invf, const int32_t* __restrict__ perm,
                                                  int blocked, const __grid_constant__ CUtensorMap otm, int tmaout,
@@ -1493,12 +1499,18 @@ __global__ void __launch_bounds__(128, 4) k_fin2(const PlanArgs args, const Cx<T
     }
     HCLK(0);
 #endif
+#if SFFT_FIN2_NOPF  // no register prefetch of the next row: fewer registers, more resident CTAs
+    if (rr != first) fetch(rr);
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) v[b] = nx[b];
+#else
 #pragma unroll
     for (int b = 0; b < EXL; ++b) v[b] = nx[b];
 #if defined(SFFT_FIN_PROBE) && SFFT_FIN_PROBE == 1  // timing probe: no scratch loads after the first row
     if (false)
 #endif
     if (rr + nper < nrows) fetch(rr + nper);
+#endif
     HCLK(1);
 #pragma unroll
     for (int t = 0; t < L; ++t) {  // global stage SQ + t + 1 pairs slot bit SQ + t = b bit t

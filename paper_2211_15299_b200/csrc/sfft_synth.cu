@@ -64,3 +64,59 @@ extern "C" int sfft_synthesize(const int64_t* J, const void* coeffs, int64_t k, 
   SFFT_CUDA(cudaGetLastError());
   return SFFT_OK;
 }
+
+// ------------------------------------------------- FMA throughput probe ---
+namespace sfft {
+
+template <typename T, int CH>
+__global__ void __launch_bounds__(256) k_fma_probe(T* out, int iters, T a, T b) {
+  T x[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) x[c] = (T)(threadIdx.x + c);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = x[c] * a + b;
+  }
+  T s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c];
+  if (s == (T)12345) out[0] = s;  // never true: keeps the chains alive
+}
+
+template <typename T>
+static int fma_probe(double* tflops, cudaStream_t st) {
+  constexpr int CH = 8, NT = 256, ITERS = 4096;
+  const int grid = num_sms() * 8;
+  T* out = nullptr;
+  SFFT_CUDA(cudaMalloc(&out, sizeof(T)));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  float best = 0.f;
+  for (int rep = 0; rep < 4 && e == cudaSuccess; ++rep) {  // rep 0 warms up
+    e = cudaEventRecord(e0, st);
+    k_fma_probe<T, CH><<<grid, NT, 0, st>>>(out, rep == 0 ? 64 : ITERS, (T)0.999, (T)0.001);
+    if (e == cudaSuccess) e = cudaEventRecord(e1, st);
+    if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && e == cudaSuccess && (best == 0.f || ms < best)) best = ms;
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFree(out);
+  if (e != cudaSuccess) return cuda_fail(e, "FMA probe");
+  *tflops = 2.0 * grid * NT * (double)ITERS * CH / (best * 1e-3) / 1e12;
+  return SFFT_OK;
+}
+
+}  // namespace sfft
+
+extern "C" int sfft_probe_fma_peak(int dtype, double* tflops, sfft_stream_t stream) {
+  SFFT_NVTX("sfft_probe_fma_peak");
+  if (!tflops) return sfft::fail(SFFT_ERR_INVALID, "sfft_probe_fma_peak: null output");
+  if (dtype != SFFT_C64 && dtype != SFFT_C128) return sfft::fail(SFFT_ERR_INVALID, "sfft_probe_fma_peak: dtype");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return dtype == SFFT_C64 ? sfft::fma_probe<float>(tflops, st) : sfft::fma_probe<double>(tflops, st);
+}
