@@ -1583,6 +1583,108 @@ __global__ void __launch_bounds__(128, SFFT_FIN2_MINB) k_fin2(const PlanArgs arg
   tl_mark(tl, 2);
 }
 
+// Final pass with both directions asynchronous (blocked output maps only):
+// a warp's 32 pi x 16 b values of a row arrive by one tensor load (box 32 x
+// 16 x 1 of the scratch viewed as [pi, b, row]) into a two-slot ring, two
+// rows ahead of the butterflies, and leave by one tensor store as in k_fin2;
+// the thread keeps only its 16 values and 15 twiddles in registers.
+#ifndef SFFT_FIN3_MINB
+#define SFFT_FIN3_MINB 4
+#endif
+template <typename T, int S>
+struct Fin3Geo {
+  static constexpr int L = 4, EXL = 16, SQ = S - L, NQ = 1 << SQ, NT = 128, NW = NT / 32, NQB = NQ / NT;
+  static constexpr int TILE = EXL * 32;  // values per warp and row
+  // per warp: 2 landing slots + 1 output staging tile; then 2 mbarriers per warp
+  static constexpr size_t SMEM = (size_t)NW * 3 * TILE * sizeof(Cx<T>) + (size_t)NW * 2 * 8;
+};
+
+template <typename T, int S>
+__global__ void __launch_bounds__(128, SFFT_FIN3_MINB)
+k_fin3(const PlanArgs args, const __grid_constant__ CUtensorMap itm, const __grid_constant__ CUtensorMap otm,
+       int64_t row0, int64_t nrows, int nper, const Cx<T>* __restrict__ twf, const int32_t* __restrict__ invf,
+       const int32_t* __restrict__ perm, unsigned long long* tl) {
+  tl_mark(tl, 0);
+  using FG = Fin3Geo<T, S>;
+  constexpr int NQ = FG::NQ, SQ = FG::SQ, EXL = FG::EXL, L = FG::L, NT = FG::NT, TILE = FG::TILE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int qb = blockIdx.x % FG::NQB;
+  const int64_t first = blockIdx.x / FG::NQB;
+  if (first >= nrows) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pi = qb * NT + threadIdx.x;
+  const int pib = qb * NT + wid * 32;  // this warp's first pi
+  Cx<T>* in = reinterpret_cast<Cx<T>*>(smem_raw) + (size_t)wid * 3 * TILE;  // [slot][b][lane]
+  Cx<T>* ob = in + 2 * TILE;                                                 // [T][lane]
+  const uint32_t bar0 = smem_addr(reinterpret_cast<Cx<T>*>(smem_raw) + (size_t)FG::NW * 3 * TILE) + 16 * wid;
+  if (lane == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int q = perm[pi];
+  Cx<T> wr[EXL - 1];
+#pragma unroll
+  for (int j = 0; j < EXL - 1; ++j) wr[j] = twf[(int64_t)j * NQ + pi];
+  uint64_t epk = 0;
+#pragma unroll
+  for (int b = 0; b < EXL; ++b)
+    epk |= (uint64_t)((invf ? invf[(int64_t)b * NQ + pi] : ((b << SQ) | q)) >> SQ) << (4 * b);
+  pdl_wait();  // scratch written by this chunk's head pass
+  pdl_release();
+  tl_mark(tl, 1);
+  auto load = [&](int64_t rr, int slot) {  // lane 0: the warp's tile of scratch row rr into ring slot `slot`
+    const uint32_t bar = bar0 + 8 * slot;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(bar), "r"((uint32_t)(TILE * sizeof(Cx<T>))) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        :: "r"(smem_addr(in + slot * TILE)), "l"(&itm), "r"(pib), "r"(0), "r"((int)rr), "r"(bar) : "memory");
+  };
+  if (lane == 0) {
+    load(first, 0);
+    if (first + nper < nrows) load(first + nper, 1);
+  }
+  const T scale = (T)args.scale1;
+  uint32_t it = 0;
+  for (int64_t rr = first; rr < nrows; rr += nper, ++it) {
+    const int slot = it & 1;
+    mbar_wait(bar0 + 8 * slot, (it >> 1) & 1);
+    Cx<T> v[EXL];
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) v[b] = in[slot * TILE + b * 32 + lane];
+#pragma unroll
+    for (int t = 0; t < L; ++t) {  // global stage SQ + t + 1 pairs slot bit SQ + t = b bit t
+#pragma unroll
+      for (int b = 0; b < EXL; ++b) {
+        if (b & (1 << t)) continue;
+        const int j = (1 << t) - 1 + (b & ((1 << t) - 1));
+        const Cx<T> w = wr[j];
+        bfly2(v[b], v[b | (1 << t)], w, rot_i(w));
+      }
+    }
+    // the slot's values are in registers (consumed above): refill it two rows ahead
+    __syncwarp();
+    if (lane == 0) {
+      if (rr + 2 * (int64_t)nper < nrows) load(rr + 2 * (int64_t)nper, slot);
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the previous row's store has read `ob`
+    }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < EXL; ++b) ob[(int)((epk >> (4 * b)) & 15) * 32 + lane] = cscale(v[b], scale);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                   :: "l"(&otm), "r"(pib), "r"(0), "r"((int)(row0 + rr)), "r"(smem_addr(ob)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  tl_mark(tl, 2);
+}
+
 // host: the tensor-map decomposition of a plan's pattern (false: not eligible)
 static bool head_plan(const sfft_plan* p, int P, HeadTma* ht) {
   const int S = p->s, M = p->M, SQ = S - 4;
@@ -1796,6 +1898,26 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
       {(uintptr_t)a.out1, (uintptr_t)a.out1 + (size_t)((rows - 1) * a.ld1 + a.n1) * sizeof(Cx<T>)},
       {(uintptr_t)a.out2, a.out2 ? (uintptr_t)a.out2 + (size_t)((rows - 1) * a.ld2 + (1ll << S)) * sizeof(Cx<T>) : 0}};
   const bool pdl_first = pdl_join(st, in, 1, outs, 2, pdl && !pooled);
+  // final pass with tensor loads as well (k_fin3, under the tensor-store conditions; SFFT_FIN3=0: k_fin2)
+  static const bool fin3_on = [] {
+    const char* e = getenv("SFFT_FIN3");
+    return !(e && atoi(e) == 0);
+  }();
+  using F3 = Fin3Geo<T, S>;
+  auto fin3 = k_fin3<T, S>;
+  int occ_f3 = 0;
+  CUtensorMap itm;
+  std::memset(&itm, 0, sizeof(itm));
+  bool use_fin3 = false;
+  if (fin3_on && tmaout && soft(kernel_occupancy(fin3, F3::NT, F3::SMEM, &occ_f3)) == 0 && occ_f3 > 0) {
+    const cuuint64_t id[3] = {(cuuint64_t)HG::NQ, 16, (cuuint64_t)chunk};
+    const cuuint64_t is[2] = {(cuuint64_t)sizeof(Cx<T>) << HG::SQ, (cuuint64_t)sizeof(Cx<T>) << S};
+    const cuuint32_t ib[3] = {32, 16, 1};
+    const cuuint32_t ie[3] = {1, 1, 1};
+    use_fin3 = enc(&itm, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, scr, id, is, ib, ie, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   cudaError_t e = cudaSuccess;
   for (int64_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += chunk) {
     const int64_t n = std::min(chunk, rows - r0);
@@ -1816,7 +1938,11 @@ static int run_head(const sfft_plan* p, const PlanArgs& a, const int32_t* inv1, 
       return e ? atoi(e) : 0;
     }();
     if (nper_env > 0) nper = (int)std::min<int64_t>(n, nper_env);  // probe: more, shorter final-pass CTAs
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && use_fin3) {
+      const int nper3 = (int)std::max<int64_t>(1, std::min<int64_t>(n, sms * occ_f3 / F3::NQB));
+      e = launch_k(fin3, (unsigned)(nper3 * F3::NQB), F3::NT, F3::SMEM, st, pdl, a, itm, otm, r0, n, nper3, twf,
+                   invf, (const int32_t*)p->d_tri_perm, timeline_slot("fin"));
+    } else if (e == cudaSuccess)
       e = launch_k(fin, (unsigned)(nper * FG::NQB), FG::NT, FG::SMEM, st, pdl, a, (const Cx<T>*)scr, r0, n, nper, twf,
                    invf, (const int32_t*)p->d_tri_perm, blocked, otm, tmaout, timeline_slot("fin"));
   }

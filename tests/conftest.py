@@ -36,3 +36,26 @@ def kats():
 def golden_sas():
     import numpy as np
     return np.load(os.path.join(ROOT, "tests", "golden", "golden_sas.npz"))
+
+
+@pytest.fixture(scope="session")
+def plan_digests():
+    """sha256 digests of the unmodified reference's plan tables at the BASELINE
+    config sizes (tests/golden/make_golden_plan_digests.py)."""
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "plan_digests.json")) as fh:
+        return json.load(fh)
+
+
+def table_digest(a, dt):
+    import hashlib
+    import numpy as np
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(a).astype(dt)).tobytes()).hexdigest()
+
+
+def twiddle_sample_index(n):
+    """The positions make_golden_plan_digests.py sampled from a table of n twiddles."""
+    import numpy as np
+    if n <= 512:
+        return np.arange(n, dtype=np.int64)
+    return np.unique(np.concatenate([np.arange(64), (np.arange(448) * 2654435761 % n)])).astype(np.int64)

@@ -686,6 +686,32 @@ def test_plan_tables_at_config_size(S, cfg):
     assert np.array_equal(S.pivoted_pattern(r, M).as_array(), O.pivoted_pattern(r, M))
 
 
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg3", "cfg5", "cfg4_b0", "cfg4_b1"])
+def test_plan_tables_match_reference_digests(S, plan_digests, case):
+    """The device plan at the BASELINE config sizes against digests of the
+    UNMODIFIED reference's own tables (tests/golden/make_golden_plan_digests.py):
+    pivots, level and every index table bit-exact by sha256, sampled twiddles
+    to 1e-15 -- the full-size pin that does not pass through the oracle."""
+    from conftest import table_digest, twiddle_sample_index
+    want = plan_digests[case]
+    cfg = int(case[3])
+    J, M = O.config_support(cfg, int(case[-1]) if "_b" in case else 0)
+    assert table_digest(J, "<i8") == want["sha256"]["J"]
+    Js = S.SupportSet(1 << M, J)
+    r = S.pivots(Js)
+    assert list(r) == want["pivots"]
+    plan = S.get_plan(Js, r, 0, 1, S._lib.require_device())
+    assert plan.level == want["level"]
+    t = plan.tables()
+    for name, dt in (("element_slots", "<i8"), ("slot_residues", "<i8"), ("slot_real", "u1"),
+                     ("node_residues", "<i8"), ("offsets", "<i8")):
+        assert table_digest(t[name], dt) == want["sha256"][name], name
+    tw = np.asarray(t["twiddles"])
+    assert tw.size == want["twiddle_count"]
+    ref = np.array([complex(float.fromhex(a), float.fromhex(b)) for a, b in want["twiddle_sample"]])
+    assert np.max(np.abs(tw[twiddle_sample_index(tw.size)] - ref)) < 1e-15
+
+
 _ALT_SPLIT = r"""
 import sys
 import numpy as np
@@ -714,13 +740,14 @@ sys.exit(0 if ok else 1)
 
 
 @pytest.mark.parametrize("env", [{"SFFT_SPLIT_PASSES": "2"}, {"SFFT_TRI_SCRATCH_MB": "1"}, {"SFFT_HEAD_BULK": "0"},
-                                 {"SFFT_FIN_TMA": "0"}, {"SFFT_HEAD": "0"}])
+                                 {"SFFT_FIN_TMA": "0"}, {"SFFT_FIN3": "0"}, {"SFFT_HEAD": "0"}])
 def test_alternate_split_configurations(S, env):
     """The two-pass split (SFFT_SPLIT_PASSES=2, kept for A/B measurements),
     the three-pass split with many small row chunks (a 1 MiB scratch
     budget: 1-4 rows per chunk, the PDL chain across chunks), the head pass
     with its register epilogue (SFFT_HEAD_BULK=0) or the final pass with
-    per-thread stores (SFFT_FIN_TMA=0) and head-eligible patterns on the
+    per-thread stores (SFFT_FIN_TMA=0) or per-thread loads (SFFT_FIN3=0:
+    k_fin2 with the tensor store) and head-eligible patterns on the
     three-pass split (SFFT_HEAD=0), against the oracle.  Each runs in a
     fresh process: the settings are read once."""
     import os

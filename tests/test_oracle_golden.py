@@ -130,3 +130,29 @@ def test_reference_call_shapes_match():
     assert np.array_equal(a, b)
     c = O.reference_sas_call(f, J, M)
     assert np.linalg.norm(c - b) / np.linalg.norm(b) < 1e-14
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg3", "cfg5", "cfg4_b0", "cfg4_b1"])
+def test_plan_tables_at_config_size_match_reference_digests(plan_digests, case):
+    """The oracle's plan restatement at the BASELINE config sizes (up to 2^16
+    slots) against digests of the unmodified reference's own tables: supports,
+    pivots, level, element_slots, slot_residues, slot_real, node_residues and
+    slot-order offsets bit-exact (sha256), sampled twiddles to 1e-15."""
+    from conftest import table_digest, twiddle_sample_index
+    want = plan_digests[case]
+    cfg = int(case[3])
+    J, M = O.config_support(cfg, int(case[-1]) if "_b" in case else 0)
+    assert M == want["M"] and J.size == want["k"]
+    assert table_digest(J, "<i8") == want["sha256"]["J"]
+    r = O.pivots(J, M)
+    assert list(r) == want["pivots"]
+    plan = O.build_plan(J, M, r)
+    assert plan.level == want["level"]
+    for name, arr, dt in (("element_slots", plan.element_slots, "<i8"), ("slot_residues", plan.slot_residues, "<i8"),
+                          ("slot_real", plan.slot_real, "u1"), ("node_residues", plan.node_residues, "<i8"),
+                          ("offsets", plan.offsets, "<i8")):
+        assert table_digest(arr, dt) == want["sha256"][name], name
+    tw = np.concatenate(plan.twiddles)
+    assert tw.size == want["twiddle_count"]
+    ref = np.array([complex(float.fromhex(a), float.fromhex(b)) for a, b in want["twiddle_sample"]])
+    assert np.max(np.abs(tw[twiddle_sample_index(tw.size)] - ref)) < 1e-15
