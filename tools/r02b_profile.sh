@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu --no-e2e --no-graph > gpurun_out/r02b_plain5.log 2>&1 || { tail -5 gpurun_out/r02b_plain5.log; exit 1; }
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_head|k_fin2" --launch-skip 8 --launch-count 2 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_head|k_fin" --launch-skip 8 --launch-count 2 \
   -o gpurun_out/r02b_cfg5_flush -f python bench.py --config 5 --steps 3 --warmup 3 --no-cpu --no-e2e --no-graph > gpurun_out/r02b_cfg5_flush.log 2>&1
 echo full=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"^k_|sfft" -c 400 \
