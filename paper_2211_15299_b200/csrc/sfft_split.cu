@@ -951,9 +951,24 @@ struct HeadGeo {
   static_assert(sizeof(T) == 4 && SQ >= 2 * LE && E <= TPB, "head pass: complex64, at least 2 register passes");
 };
 
-// L2 eviction priorities for the scratch round trip (SFFT_L2_HINTS=0: none)
-#ifndef SFFT_L2_HINTS
-#define SFFT_L2_HINTS 1
+// L2 eviction priorities of the head path's four streams (each -D...=0/1;
+// config 5, one box, 256-row step): none 110.3 us; signal copies, scratch
+// loads and output stores evict_first 100.4-101.4 us; the same with the
+// scratch copies evict_last 104.0 us; without the output hint 105.7-106.3 us;
+// signal / scratch-load hint alone 103.2 / 105.4 us.  Everything that is
+// read or written once leaves L2 first, and the scratch (default priority)
+// survives from the head pass to the final pass.
+#ifndef SFFT_SIG_HINT  // evict_first on the head pass's signal copies
+#define SFFT_SIG_HINT 1
+#endif
+#ifndef SFFT_FIN_LOAD_HINT  // evict_first on the final pass's scratch loads (k_fin3)
+#define SFFT_FIN_LOAD_HINT 1
+#endif
+#ifndef SFFT_SCR_HINT  // evict_last on the head pass's scratch copies
+#define SFFT_SCR_HINT 0
+#endif
+#ifndef SFFT_OUT_HINT  // evict_first on the final pass's output stores
+#define SFFT_OUT_HINT 1
 #endif
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
@@ -1096,10 +1111,18 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
         const int c2 = (int)((e >> ht.k2) & ((1u << (ht.k3 - ht.k2)) - 1u));
         const int c3 = (int)(e >> ht.k3);
         const int c4 = (int)(row0 + rr);
+#if SFFT_SIG_HINT
+        // probe: signal lines first out of L2 (they are read by the 8 units of a row within a short window)
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;"
+            :: "r"(smem_addr(lbuf + (size_t)o * box)), "l"(&tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+               "r"(full), "l"(l2_policy_evict_first()) : "memory");
+#else
         asm volatile(
             "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
             :: "r"(smem_addr(lbuf + (size_t)o * box)), "l"(&tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
                "r"(full) : "memory");
+#endif
       }
     }
     return;
@@ -1250,7 +1273,7 @@ k_head(const __grid_constant__ CUtensorMap tm, const HeadTma ht, const FrontTw2 
         for (int j = 0; j < P; ++j) {
           if (SFFT_HEAD_GROUPS && j != bl) continue;
           const int bj = c | (LP == 1 ? (j << 3) : (((j & 1) << 3) | ((j >> 1) << 2)));
-#if SFFT_L2_HINTS
+#if SFFT_SCR_HINT
           // scratch is read once more, by this chunk's final pass: keep it in L2
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
                        :: "l"(scratch + ((int64_t)rr << S) + ((int64_t)bj << SQ)), "r"(smem_addr(work + j * NQ)),
@@ -1540,7 +1563,7 @@ __global__ void __launch_bounds__(128, SFFT_FIN2_MINB) k_fin2(const PlanArgs arg
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-#if SFFT_L2_HINTS
+#if SFFT_OUT_HINT
         // outputs are not read again by this call: first out of L2
         asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
                      :: "l"(&otm), "r"(pib), "r"(0), "r"((int)r), "r"(smem_addr(sw)), "l"(l2_policy_evict_first())
@@ -1638,9 +1661,17 @@ k_fin3(const PlanArgs args, const __grid_constant__ CUtensorMap itm, const __gri
     const uint32_t bar = bar0 + 8 * slot;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  :: "r"(bar), "r"((uint32_t)(TILE * sizeof(Cx<T>))) : "memory");
+#if SFFT_FIN_LOAD_HINT
+    // probe: scratch rows are dead once read
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;"
+        :: "r"(smem_addr(in + slot * TILE)), "l"(&itm), "r"(pib), "r"(0), "r"((int)rr), "r"(bar),
+           "l"(l2_policy_evict_first()) : "memory");
+#else
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
         :: "r"(smem_addr(in + slot * TILE)), "l"(&itm), "r"(pib), "r"(0), "r"((int)rr), "r"(bar) : "memory");
+#endif
   };
   if (lane == 0) {
     load(first, 0);
@@ -1676,8 +1707,14 @@ k_fin3(const PlanArgs args, const __grid_constant__ CUtensorMap itm, const __gri
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) {
+#if SFFT_OUT_HINT
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
+                   :: "l"(&otm), "r"(pib), "r"(0), "r"((int)(row0 + rr)), "r"(smem_addr(ob)),
+                      "l"(l2_policy_evict_first()) : "memory");
+#else
       asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
                    :: "l"(&otm), "r"(pib), "r"(0), "r"((int)(row0 + rr)), "r"(smem_addr(ob)) : "memory");
+#endif
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
