@@ -1,4 +1,5 @@
-"""Device time of hidft_to_dft_interleaved on config-2-shaped data stored (N, B) (profiling driver)."""
+"""Device time of hidft_to_dft_interleaved on config-2-shaped data stored (N, B): a CUDA graph of 32 calls over
+32 shifts (disjoint sample rows, as bench.py's layouts.interleaved) inside a stream_chain scope."""
 import os
 import sys
 
@@ -18,10 +19,18 @@ out = torch.empty((wl.B, wl.k), dtype=torch.complex64, device="cuda")
 for i in range(4):
     S.hidft_to_dft_interleaved(nb, J, out=out, shift=i)
 torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    with S.stream_chain():
+        for i in range(32):
+            S.hidft_to_dft_interleaved(nb, J, out=out, shift=i)
+for _ in range(3):
+    g.replay()
+torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
-for i in range(32):
-    S.hidft_to_dft_interleaved(nb, J, out=out, shift=i)
+for _ in range(10):
+    g.replay()
 ev[1].record()
 torch.cuda.synchronize()
-print(f"interleaved cfg2: {ev[0].elapsed_time(ev[1]) / 32 * 1e3:.2f} us per call (eager, no scope)")
+print(f"interleaved cfg2 lib {os.environ.get('SFFT_LIB', 'default')}: {ev[0].elapsed_time(ev[1]) / 320 * 1e3:.2f} us per call (32-call graphs)")
