@@ -212,7 +212,7 @@ static int temp_pool(cudaMemPool_t* pool) {
   props.location.id = dev;
   cudaMemPool_t p;
   SFFT_CUDA(cudaMemPoolCreate(&p, &props));
-  uint64_t keep = 256ull << 20;  // keep up to 256 MiB between builds
+  uint64_t keep = 1024ull << 20;  // keep up to 1 GiB between builds (temporaries and destroyed plans' tables)
   SFFT_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep));
   pools[dev] = p;
   *pool = p;
@@ -1004,8 +1004,17 @@ extern "C" int sfft_plan_create(const int64_t* J, int64_t k, int M, const int32_
   for (int i = 0; i < s; ++i) p->used[i] = r[i];
   const size_t csz = dtype == SFFT_C64 ? 8 : 16;
   cudaError_t e = cudaSuccess;
+  // the plan's tables come from the library's stream-ordered pool as well
+  // (a destroyed plan's memory serves the next build without a driver
+  // allocation per table; plan_free releases them with cudaFree, which
+  // synchronises as before)
+  cudaMemPool_t tpool;
+  if (int prc = temp_pool(&tpool)) {
+    delete p;
+    return prc;
+  }
   auto M_ = [&](void** ptr, size_t bytes) {
-    if (e == cudaSuccess) e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(ptr, std::max<size_t>(bytes, 16), tpool, st);
   };
   M_((void**)&p->d_element_slots, 4 * k);
   M_((void**)&p->d_slot_residues, 4 * A);
