@@ -98,6 +98,8 @@ static HostPool* g_pool = nullptr;
 // default: every core but the calling thread's (which gathers too), shared
 // between the processes of one node under torchrun (LOCAL_WORLD_SIZE)
 static int default_threads() {
+  if (const char* e = getenv("SFFT_HOST_THREADS"))  // explicit pool size (probes)
+    if (atoi(e) > 0) return atoi(e);
   int hw = (int)std::thread::hardware_concurrency();
   if (const char* e = getenv("LOCAL_WORLD_SIZE")) hw /= std::max(1, atoi(e));
   return std::max(1, hw - 1);
