@@ -920,9 +920,13 @@ static bool use_tri() {
 // LSU never issues a gather instruction.  The landing layout is a bit
 // permutation of q (HeadTma::qw); pass 0 reads it into registers, runs
 // stages 1-4 and continues with the swizzled single-CTA layout for stages
-// 5..SQ, and the epilogue writes scratch[row][b][pi] (pi: the final pass's
-// output order, coalesced).  The final pass (k_tri_final) is shared with
-// the three-pass split.  Reference: hidft.py:34-49 (gather), 160-167.
+// 5..SQ; the last pass stores each value at its final-pass position pi and
+// the b value's block leaves for scratch[row][b][pi] by one bulk copy (pi:
+// the final pass's output order).  The final pass is k_fin3 (tensor loads
+// and stores) for blocked output maps, else k_fin2 (k_tri_final's scheme
+// with FFMA2 and register twiddles).  Every stream of the path carries an L2
+// eviction priority so that the scratch chunk stays in L2 between the two
+// kernels.  Reference: hidft.py:34-49 (gather), 160-167.
 struct HeadTma {
   int nops, nleft, P;
   uint32_t left_d[16];  // element offset of each enumerated (leftover) q bit
@@ -1025,9 +1029,11 @@ __device__ __forceinline__ void tl_mark(unsigned long long* tl, int what) {
 template <int NT>
 __device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
 // barrier among the warps of one b value's group (named barrier 2 + group);
-// SFFT_HEAD_GROUPS=0 (default): one barrier over all transform threads
-// (config 5: per-group barriers 126.1-126.4 us against 126.5 us per step; the
-// pass is bound by the TMA row rate and the transform's latency, tools/tma_box_probe.cu)
+// SFFT_HEAD_GROUPS=0: one barrier over all transform threads.  With the
+// register epilogue the groups made no difference (126.1-126.4 against 126.5
+// us per config-5 step); with the bulk epilogue and two landing buffers
+// nothing couples the two b values of a unit any more and the groups' FMA
+// and shared-memory phases interleave (120.4 -> 116.3 us)
 #ifndef SFFT_HEAD_GROUPS
 #define SFFT_HEAD_GROUPS 1
 #endif
