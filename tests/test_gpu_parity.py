@@ -1063,3 +1063,30 @@ def test_graph_capture_with_growing_scratch(S, torch, top):
         assert torch.equal(outs[1], want)
     ref = O.hidft_to_dft(sig[4].cpu().numpy(), Jn, M)
     assert rel_l2(want[4].cpu().numpy(), ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,top,B,seed", [(20, 4, 131, 1), (21, 2, 5, 2), (22, 4, 2, 3), (20, 3, 67, 4)])
+def test_head_path_patterns_and_chunk_boundaries(S, torch, M, top, B, seed):
+    """2^16-slot supports whose `top` largest levels are pivots (the TMA head
+    pass; top = 4: blocked output map, tensor-copy final pass), random other
+    pivots and multipliers, batches that cross the 128-row scratch chunk
+    (131 rows: chunks of 128 + 3) or stay far below it: every row against
+    the planted spectrum, seeded rows and both sides of the chunk boundary
+    against the oracle."""
+    rng = np.random.default_rng(9000 + seed)
+    s = 16
+    piv = sorted(rng.choice(M - top, size=s - top, replace=False).tolist()) + list(range(M - top, M))
+    Jn = O.gen_homogeneous(piv, M, int(rng.integers(0, 2 ** 62)))
+    N = 1 << M
+    coef = (rng.normal(size=(B, Jn.size)) + 1j * rng.normal(size=(B, Jn.size))).astype(np.complex128)
+    sig = torch.empty((B, N), dtype=torch.complex64, device="cuda")
+    from paper_2211_15299_b200 import workloads as W
+    W.synthesize_into(sig, Jn, coef)
+    J = S.SupportSet(N, Jn)
+    got = S.hidft_to_dft_batched(sig, J).cpu().numpy()
+    err = np.linalg.norm(got - coef, axis=1) / np.linalg.norm(coef, axis=1)
+    assert err.max() < 1e-5
+    rows = sorted({0, B - 1} | ({127, 128} if B > 128 else set()) | {int(rng.integers(0, B))})
+    for b in rows:
+        want = O.hidft_to_dft(sig[b].cpu().numpy(), Jn, M)
+        assert rel_l2(got[b], want) < 1e-5, b
